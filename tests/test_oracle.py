@@ -1,0 +1,160 @@
+"""CPU tests: pin the oracle (C restatement) against the reference.
+
+* against the committed golden fixtures (generated from the unmodified
+  reference by tests/golden/make_golden.py) -- always runs;
+* against the live reference (oracle/_ref, compiled in place) -- where built.
+
+The restatement reproduces the reference's operand order, so the expected
+agreement is bitwise; the asserted bound is 1e-13 relative to stay robust to
+libm differences across hosts.
+"""
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, preset
+from oracle import Oracle, OracleError, RefOracle, load_preset, rel_err
+
+GOLD = os.path.join(ROOT, "tests", "golden")
+TOL = 1e-13
+
+
+def gold(name):
+    return np.load(os.path.join(GOLD, name + ".npz"))
+
+
+@pytest.fixture(scope="module", params=["mini", "small_mcao"])
+def case(request):
+    name = request.param
+    return name, gold(name), Oracle(preset(name + ".json"))
+
+
+def test_filter_table_matches_reference_values():
+    """tools/gen_daubechies.py derives the filters by spectral factorisation;
+    their doubles must equal the reference table (wavelet.hpp:39-75): checked
+    through the transforms of every order on a 16x16 grid."""
+    g = gold("wavelet_orders")
+    for order in range(1, 11):
+        x = g[f"x{order}"]
+        assert rel_err(Oracle.wavelet_grid(order, x, False), g[f"fwd{order}"]) <= TOL
+        assert rel_err(Oracle.wavelet_grid(order, x, True), g[f"inv{order}"]) <= TOL
+        # perfect reconstruction (test_wavelet.cpp:103-116)
+        y = Oracle.wavelet_grid(order, Oracle.wavelet_grid(order, x, False), True)
+        assert rel_err(y, x) < 1e-13
+
+
+def test_geometry_bitwise(case):
+    _, g, o = case
+    ext, dext, masks = o.geometry()
+    assert np.array_equal(ext, g["layer_extent"])
+    assert np.array_equal(dext, g["dm_extent"])
+    assert np.array_equal(masks, g["masks"])
+
+
+def test_elt_geometry_bitwise():
+    g = gold("elt_mcao84_geometry")
+    ext, dext, masks = Oracle(preset("elt_mcao84.json")).geometry()
+    assert np.array_equal(ext, g["layer_extent"])
+    assert np.array_equal(dext, g["dm_extent"])
+    assert np.array_equal(masks, g["masks"])
+    assert int(masks.sum()) == 23910  # SURVEY.md key fact 5: active subapertures at ELT MCAO-84
+
+
+@pytest.mark.parametrize("op", ["winv", "wfwd", "P", "PT", "G", "GT", "M", "rhs", "dm_slopes", "fit"])
+def test_operators_vs_golden(case, op):
+    _, g, o = case
+    x, wf, m, a = g["in_x"], g["in_wf"], g["in_meas"], g["in_a"]
+    got = {
+        "winv": lambda: o.wavelet(x, True), "wfwd": lambda: o.wavelet(x, False),
+        "P": lambda: o.propagate(x), "PT": lambda: o.propagate_transpose(wf),
+        "G": lambda: o.sh(wf), "GT": lambda: o.sh_transpose(m),
+        "M": lambda: o.apply_M(x), "rhs": lambda: o.build_rhs(m),
+        "dm_slopes": lambda: o.add_dm_slopes(a, m), "fit": lambda: o.fit(x),
+    }[op]()
+    assert rel_err(got, g[op]) <= TOL
+
+
+def test_preconditioner_vs_golden(case):
+    _, g, o = case
+    o.build_preconditioner()
+    assert rel_err(o.preconditioner(), g["precond"]) <= TOL
+
+
+def test_closed_loop_replay_vs_golden(case):
+    """Replay protocol: feed the recorded slopes, compare c, a, rho per frame."""
+    name, g, _ = case
+    o = Oracle(preset(name + ".json"))
+    for k in range(g["loop_meas"].shape[0]):
+        c, a, rho = o.step(g["loop_meas"][k])
+        assert rel_err(c, g["loop_c"][k]) <= TOL, k
+        assert rel_err(a, g["loop_a"][k]) <= TOL, k
+        assert rel_err(rho, g["loop_rho"][k]) <= TOL, k
+    st = o.get_state()
+    for key in ("c", "b", "r", "p", "q", "scalars", "a_prev2", "a_prev"):
+        assert rel_err(st[key], g["final_" + key]) <= TOL, key
+
+
+def test_set_state_single_step(case):
+    """Single-step protocol: inject the state, run one step, compare."""
+    name, g, _ = case
+    o = Oracle(preset(name + ".json"))
+    for k in range(g["loop_meas"].shape[0] - 1):
+        o.step(g["loop_meas"][k])
+    st = o.get_state()
+    o2 = Oracle(preset(name + ".json"))
+    o2.set_state(st)
+    c2, a2, _ = o2.step(g["loop_meas"][-1])
+    assert rel_err(c2, g["loop_c"][-1]) <= TOL
+    assert rel_err(a2, g["loop_a"][-1]) <= TOL
+
+
+def test_reset_restores_cold_start():
+    """test_reconstructor.cpp:339-360."""
+    g = gold("small_mcao")
+    o = Oracle(preset("small_mcao.json"))
+    c0, a0, _ = o.step(g["loop_meas"][0])
+    o.step(g["loop_meas"][1])
+    o.reset()
+    c1, a1, _ = o.step(g["loop_meas"][0])
+    assert np.array_equal(c0, c1) and np.array_equal(a0, a1)
+
+
+def test_rejects_l_ne_m():
+    """geometry.hpp:294-296: only L = M is supported by the reference."""
+    g = load_preset(preset("small_mcao.json"))
+    g["n_act"] = g["n_act"][:2]
+    g["dm_height"] = g["dm_height"][:2]
+    with pytest.raises(OracleError, match=re.escape("dm count 2 != layer count 3")) as ei:
+        Oracle(g)
+    assert ei.value.code == 2
+
+
+ref_only = pytest.mark.skipif(not RefOracle.available(), reason="oracle/_ref not built (needs /root/reference)")
+
+
+@ref_only
+@pytest.mark.parametrize("name", ["mini", "small_mcao"])
+def test_live_reference_open_loop_and_fault(name):
+    """Modes the fixtures do not cover: open loop and the sh_adjoint fault fixture."""
+    path = preset(name + ".json")
+    o, r = Oracle(path, loop_mode="open", gain=1.0), RefOracle(path, threads=1, loop_mode="open", gain=1.0)
+    rng = np.random.default_rng(7)
+    for _ in range(3):
+        m = rng.standard_normal(o.dims.S)
+        co, ao, ro = o.step(m)
+        cr, ar, rr = r.step(m)
+        assert rel_err(co, cr) <= TOL and rel_err(ao, ar) <= TOL and rel_err(ro, rr) <= TOL
+
+
+@ref_only
+@pytest.mark.slow
+def test_live_reference_elt_operators():
+    path = preset("elt_mcao84.json")
+    o, r = Oracle(path), RefOracle(path)
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal(o.dims.n)
+    assert rel_err(o.apply_M(x), r.apply_M(x)) <= TOL
+    m = rng.standard_normal(o.dims.S)
+    assert rel_err(o.build_rhs(m), r.build_rhs(m)) <= TOL
