@@ -1,0 +1,442 @@
+#!/usr/bin/env python
+"""Benchmark of the FEWHA reconstruction frame (Reconstructor::step) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--precision 64|32] [--preset presets/elt_mcao84.json]
+
+Workload (BASELINE.json metric "per-frame reconstruction latency p50/p99 (ms)
+and recon/sec vs memory roofline"): ELT MCAO-84 -- 39 m, 6 LGS 84x84 + 3 NGS,
+9 layers of 128^2 (J=7), closed loop, 4 warm-started PCG iterations, fp64 --
+in its reference-runnable L=M=9 form (presets/elt_mcao84.json; the 3-DM
+fitting is SURVEY.md 8f "next").  One step = one frame of one instance.
+
+  value      reconstructions/s over all ranks, slopes resident in HBM, timed with
+             CUDA events around each frame's graph launch; L2 flushed (256 MiB
+             write) before every timed frame.
+  e2e        the same metric through the C-ABI fewha_gpu_step with pinned HOST
+             buffers: H2D of the frame's slopes + D2H of a^(1), rho and status
+             inside the timed region.
+  roofline   dominant kernel (largest share of the frame in a per-launch event
+             profile): algorithmic bytes per launch / its mean event duration.
+  cpu_baseline  the reference solver (oracle/_ref, compiled from the unmodified
+             reference) timed on this host's cores on a bounded frame sample.
+
+--impl reference runs the reference CPU solver alone (rank 0), with every
+host thread, on the same config and slope stream.
+N > 1: one process per GPU, independent instances per rank (replicas,
+"scaling": "weak"); the path has no exchange step in this mode.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "per-frame reconstruction latency p50/p99 (ms) and recon/sec vs memory roofline"
+UNIT = "recon/s"
+DEFAULT_PRESET = os.path.join(ROOT, "presets", "elt_mcao84.json")
+L2_FLUSH_BYTES = 256 << 20
+
+
+def load_json(path):
+    with open(path) as f:
+        return json.load(f)
+
+
+def preset_dims(preset):
+    j = load_json(preset)
+    ns = [w["n_subap"] for w in j["wfs"]]
+    n = sum((1 << l["grid_order"]) ** 2 for l in j["layers"])
+    S = sum(2 * k * k for k in ns)
+    Nw = sum((k + 1) ** 2 for k in ns)
+    A = sum(d["n_act"] ** 2 for d in j["dms"])
+    return dict(n=n, S=S, Nw=Nw, A=A, L=len(j["layers"]), W=len(ns), M=len(j["dms"]),
+                iters=j["solver"]["pcg_max_iter"], closed=j["loop"]["mode"] == "closed")
+
+
+def frame_bytes(d, b):
+    """Fused-minimum algorithmic traffic of one frame (SURVEY.md 8d / BASELINE.md 4)."""
+    n, S, Nw, A, it = d["n"], d["S"], d["Nw"], d["A"], d["iters"]
+    A_cl = A if d["closed"] else 0
+    return b * (it * (13 * n + 2 * Nw) + (4 * n + 2 * Nw + A_cl) + (n + 3 * A)) + 8 * S
+
+
+def kernel_bytes(kind, d, b):
+    """Algorithmic bytes of one launch of each kernel kind (one instance):
+    every array the kernel must read or write crosses memory once."""
+    n, S, Nw, A = d["n"], d["S"], d["Nw"], d["A"]
+    return {
+        "wfs_rhs": 8 * S + b * (A + Nw),          # slopes (fp64) + a_prev2 -> psi
+        "adjoint": b * (Nw + n),                  # psi -> y
+        "fwd_rhs": b * (3 * n + 2 * n),           # y, r, b -> r, b
+        "inv_pcg0": b * (2 * n + n),              # r, J -> phi
+        "inv_pcg": b * (6 * n + 4 * n + n),       # r, J, p, q, c, Mz -> p, q, c, r, phi
+        "wfs": b * (n + Nw),                      # phi -> psi
+        "fwd_pcg": b * (3 * n + n),               # y, r, J -> Mz
+        "inv_fit": b * (6 * n + 4 * n + n),       # last update + c -> phi
+        "fit_control": b * (n + 5 * A),           # phi, a_prev, a_prev2 -> a_prev2, a_prev, a_out
+    }[kind]
+
+
+def synthetic_layers(preset, seed):
+    """Von Karman layer screens (FFT-shaped complex noise, simulation.hpp:76-127
+    spectrum (k^2 + k0^2)^(-11/12)), strength-scaled; nodal [n]."""
+    j = load_json(preset)
+    L0 = j["solver"].get("outer_scale", 25.0)
+    rng = np.random.default_rng(seed)
+    out = []
+    for lay in j["layers"]:
+        n = 1 << lay["grid_order"]
+        ext = 1.0  # physical scale irrelevant for the synthetic stream shape
+        f = np.fft.fftfreq(n, d=ext / n)
+        kk = (2 * np.pi) ** 2 * (f[:, None] ** 2 + f[None, :] ** 2) + (2 * np.pi / L0) ** 2
+        amp = kk ** (-11.0 / 12.0)
+        amp[0, 0] = 0.0
+        scr = np.real(np.fft.ifft2((rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) * amp))
+        scr -= scr.mean()
+        scr *= math.sqrt(lay["relative_strength"]) / max(scr.std(), 1e-30)
+        out.append(scr.ravel())
+    return np.concatenate(out)
+
+
+def slope_stream(rec, preset, frames, seed):
+    """Noisy slopes of frozen-flow-free random atmospheres: s = Gamma P phi + n
+    (forward model on the GPU through the library, noise sigma_w per WFS)."""
+    j = load_json(preset)
+    layers = np.stack([synthetic_layers(preset, seed * 1000 + k) for k in range(frames)])
+    s = rec.forward_slopes(layers).reshape(frames, -1)
+    rng = np.random.default_rng(seed)
+    sig = np.repeat([math.sqrt(w["noise_variance"]) for w in j["wfs"]], [2 * w["n_subap"] ** 2 for w in j["wfs"]])
+    return np.ascontiguousarray(s + sig[None, :] * rng.standard_normal(s.shape))
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    try:
+        p = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json"))
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def cpu_reference_time(preset, stream, frames, threads):
+    """Reference solver (oracle/_ref) on this host: per-frame wall times (us)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import RefOracle  # noqa: E402
+    r = RefOracle(preset, threads=threads)
+    r.build_preconditioner()
+    r.time_steps(stream[:2], 2)  # warm-up frames
+    us = r.time_steps(stream, frames)
+    return us, r.threads
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import RefOracle  # noqa: E402
+    if not RefOracle.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference at build time)"}))
+        return 0
+    d = preset_dims(args.preset)
+    threads = os.cpu_count() or 1
+    rng = np.random.default_rng(7)
+    # reference-side slope stream: the reference's own synthesis (bench.hpp:144-154 pattern)
+    r = RefOracle(args.preset, threads=threads)
+    stream = np.stack([r.synthesize(1, k) for k in range(4)])
+    r.build_preconditioner()
+    r.time_steps(stream, max(args.warmup, 1))
+    us = r.time_steps(stream, args.steps)
+    ms = us / 1000.0
+    val = 1000.0 / float(np.mean(ms))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(val, 3), "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(float(np.mean(ms)), 4),
+        "p50_ms": round(float(np.percentile(ms, 50)), 4), "p99_ms": round(float(np.percentile(ms, 99)), 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "ELT MCAO-84 (L=M=9) single-instance frame, reference CPU solver",
+                   "preset": os.path.relpath(args.preset, ROOT), "threads": r.threads},
+        "cpu_baseline": {"value": round(val, 3), "unit": UNIT, "cores": r.threads, "kind": "reference",
+                         "sample": f"{args.steps} frames of Reconstructor::step after {max(args.warmup,1)} warm-up, "
+                                   f"{r.threads} pool threads on {os.cpu_count()} host cpus"},
+        "e2e": {"value": round(val, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import paper_2009_00946_b200 as fg
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    d = preset_dims(args.preset)
+    b = args.precision // 8
+
+    rec = fg.Reconstructor(args.preset, precision=args.precision, batch=1, device=local)
+    rec.build_preconditioner()
+    F = 16
+    stream_host = slope_stream(rec, args.preset, F, seed=1 + rank)
+    stream = torch.from_numpy(stream_host).to(dev)
+    st = torch.cuda.current_stream(dev)
+    rec.set_stream(st.cuda_stream)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    S = d["S"]
+
+    def load(k):
+        # slopes for frame k into the library's resident slot (outside timing)
+        rec.load_slopes_device(stream[k % F].data_ptr())
+
+    for k in range(max(args.warmup, 3)):
+        load(k)
+        rec.step_device(None)
+    rec.sync()
+
+    # ---- device-resident timed region -------------------------------------------
+    K = args.steps
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with Clocks(local) as clk:
+        for k in range(K):
+            load(k)
+            flush.zero_()
+            starts[k].record(st)
+            rec.step_device(None)
+            ends[k].record(st)
+        torch.cuda.synchronize(dev)
+    rec.sync()
+    if dist:
+        dist.barrier()
+    ms = np.array([s.elapsed_time(e) for s, e in zip(starts, ends)])
+    total_ms = float(ms.sum())
+    p50, p99 = float(np.percentile(ms, 50)), float(np.percentile(ms, 99))
+    if dist:
+        t = torch.tensor([total_ms, p50, p99], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, p50, p99 = (float(x) for x in t.tolist())
+    value = world * K / (total_ms / 1000.0)
+
+    # ---- per-launch profile (events between launches on the launching stream) ----
+    prof = {}
+    for _ in range(20):
+        load(0)
+        flush.zero_()
+        for kind, t in rec.profile_step():
+            prof.setdefault(kind, []).append(t)
+    frame_prof_ms = sum(sum(v) for v in prof.values()) / 20.0
+    share = {k: sum(v) / 20.0 / frame_prof_ms for k, v in prof.items()}
+    dom = max(share, key=share.get)
+    dom_ms = float(np.mean(prof[dom]))
+    dom_bytes = kernel_bytes(dom, d, b)
+    peak, peak_kind = peaks()
+    achieved = dom_bytes / (dom_ms / 1000.0) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "dram_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = load_json(tpath).get(f"fp{args.precision}", {}).get(dom)
+        except Exception:
+            traffic = None
+
+    # ---- e2e through the C-ABI with pinned host buffers ------------------------------
+    pin_s = torch.from_numpy(stream_host).pin_memory()
+    pin_a = torch.zeros(d["A"], dtype=torch.float64).pin_memory()
+    pin_rho = torch.zeros(d["iters"], dtype=torch.float64).pin_memory()
+    lib = fg.lib()
+    import ctypes as C
+    dp = C.POINTER(C.c_double)
+    nr = (C.c_int * 1)()
+    e2e_ms = []
+    for k in range(max(args.warmup, 3) + min(K, 300)):
+        flush.zero_()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        rc = lib.fewha_gpu_step(rec._h, C.cast(pin_s[k % F].data_ptr(), dp), None, C.cast(pin_a.data_ptr(), dp),
+                                C.cast(pin_rho.data_ptr(), dp), nr)
+        t1 = time.perf_counter()
+        rec._chk(rc)
+        if k >= max(args.warmup, 3):
+            e2e_ms.append((t1 - t0) * 1000.0)
+    e2e_ms = np.array(e2e_ms)
+    e2e_val = world * 1000.0 / float(np.mean(e2e_ms))
+    if dist:
+        t = torch.tensor([float(np.mean(e2e_ms))], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_val = world * 1000.0 / float(t.item())
+
+    # ---- batch-64 throughput (HBM-bound regime) ----------------
+    batch_info = None
+    if args.batch64 and rank == 0 or (args.batch64 and dist):
+        B = 64
+        rb = fg.Reconstructor(args.preset, precision=args.precision, batch=B, device=local)
+        rb.build_preconditioner()
+        rb.set_stream(st.cuda_stream)
+        big = stream.repeat((B + F - 1) // F, 1)[:B].contiguous()
+        rb.load_slopes_device(big.data_ptr())
+        for _ in range(3):
+            rb.step_device(None)
+        rb.sync()
+        KB = 30
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(KB):
+            rb.step_device(None)
+        e1.record(st)
+        rb.sync()
+        bms = e0.elapsed_time(e1) / KB
+        fb = frame_bytes(d, b) * B
+        batch_info = {"batch": B, "ms_per_step": round(bms, 4), "recon_per_s": round(B * 1000.0 / bms, 1),
+                      "roofline_frac_frame_model": round(fb / (bms / 1000.0) / 1e9 / peak, 4),
+                      "note": "inputs resident, no flush between steps (working set 64 x ~15 MB > L2)"}
+        rb.close()
+
+    # ---- CPU baseline (rank 0, N=1 only) -------------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        from oracle import RefOracle  # noqa: E402
+        if RefOracle.available():
+            threads = min(max(d["L"], d["W"]), os.cpu_count() or 1)
+            frames = args.cpu_frames
+            us, thr = cpu_reference_time(args.preset, stream_host, frames, threads)
+            cms = us / 1000.0
+            cpu = {"value": round(1000.0 / float(np.mean(cms)), 3), "unit": UNIT, "cores": thr, "kind": "reference",
+                   "sample": f"{frames} frames of the reference Reconstructor::step (oracle/_ref) on this slope stream, "
+                             f"{thr} pool threads (min(max(L,W), nproc)), {os.cpu_count()} host cpus; "
+                             f"p50 {np.percentile(cms, 50):.2f} ms p99 {np.percentile(cms, 99):.2f} ms"}
+
+    if rank == 0:
+        fb = frame_bytes(d, b)
+        launches = rec.launches_per_step()
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": round(total_ms / K, 5), "p50_ms": round(p50, 5),
+            "p99_ms": round(p99, 5), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64" if args.precision == 64 else "f32", "data": "synthetic",
+            "config": {"workload": "ELT MCAO-84 (L=M=9 reference-runnable form), 1 instance/rank, closed loop, "
+                                   "4 PCG iters, frame latency",
+                       "preset": os.path.relpath(args.preset, ROOT), "n_coeff": d["n"], "n_slopes": S,
+                       "n_act": d["A"], "l2": "flushed (256 MiB write) before every timed frame",
+                       "parallelism": f"replicas x{world}"},
+            "frame_roofline": {"bytes_per_frame": fb, "achieved_gbs": round(fb / (p50 / 1000.0) / 1e9, 2),
+                               "frac_at_p50": round(fb / (p50 / 1000.0) / 1e9 / peak, 5),
+                               "roofline_us": round(fb / (peak * 1e9) * 1e6, 3)},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 2), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "bytes_per_launch": dom_bytes, "launch_ms": round(dom_ms, 5),
+                         "share_of_frame": round(share[dom], 3), "peak_source": peak_kind,
+                         "kernel_shares": {k: round(v, 3) for k, v in sorted(share.items(), key=lambda x: -x[1])}},
+            "e2e": {"value": round(e2e_val, 3), "unit": UNIT, "h2d_bytes_per_step": S * 8,
+                    "d2h_bytes_per_step": d["A"] * 8 + d["iters"] * 8 + 8,
+                    "p50_ms": round(float(np.percentile(e2e_ms, 50)), 5),
+                    "p99_ms": round(float(np.percentile(e2e_ms, 99)), 5)},
+            "gpu_launches": launches * K,
+            "clocks": clk.summary(),
+        }
+        if cpu:
+            line["cpu_baseline"] = cpu
+        if batch_info:
+            line["batch64"] = batch_info
+        print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--precision", type=int, default=64, choices=[64, 32])
+    ap.add_argument("--preset", default=DEFAULT_PRESET)
+    ap.add_argument("--cpu-frames", type=int, default=150)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-batch64", dest="batch64", action="store_false")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,152 @@
+/* include/fewha_gpu.h -- C-ABI of the B200-native FEWHA reconstructor.
+ *
+ * Drop-in boundary for the reference's hot path, reference
+ * /root/reference/proj/include/fewha/ (file:line of the API each entry
+ * replaces is given per function).  Plain pointers and sizes only; every
+ * entry returns a status:
+ *   FEWHA_OK (0)      success
+ *   FEWHA_RUNTIME (1) runtime failure: non-finite PCG scalar, out-of-grid
+ *                     interpolation, non-positive preconditioner, CUDA error
+ *                     (reference: std::runtime_error; CLI exit code 1,
+ *                     tools/fewha_cli.cpp:31-33, :157-163)
+ *   FEWHA_CONFIG (2)  configuration error (reference: fewha::config_error;
+ *                     CLI exit code 2)
+ *   FEWHA_ARG (3)     bad argument / size mismatch (reference:
+ *                     std::invalid_argument)
+ * The message of the last failure is returned by fewha_gpu_last_error(h)
+ * (or fewha_gpu_create_error() when no handle exists yet).
+ *
+ * Threading: one handle is externally single-threaded, like
+ * Reconstructor::step.  Host buffers are caller-owned and
+ * complete on return; device state is library-owned and resident in HBM.
+ * Host vectors are always fp64; precision 32 computes in fp32 on the device.
+ *
+ * Layouts follow the reference exactly:
+ *   slopes       per WFS [sx (n_s^2 row-major) | sy (n_s^2)]      operators.hpp:35-65
+ *   coefficients per layer 2^J x 2^J Mallat layout, row-major   operators.hpp:67-91
+ *   wavefronts   per WFS (n_s+1)^2 row-major                     operators.hpp:141-145
+ *   DM commands  per DM n_act^2 row-major                        reconstructor.hpp:34-41
+ * A `batch` handle holds `batch` independent instances (same geometry);
+ * per-frame arrays are then batch-major ([instance][...]).
+ */
+#ifndef FEWHA_GPU_H
+#define FEWHA_GPU_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FEWHA_OK 0
+#define FEWHA_RUNTIME 1
+#define FEWHA_CONFIG 2
+#define FEWHA_ARG 3
+
+typedef struct fewha_gpu_handle* fewha_gpu_t;
+
+typedef struct {
+    long long n_coeff;     /* n   = sum_l 4^J_l            (SystemGeometry::coeff_dim, geometry.hpp:171) */
+    long long n_slopes;    /* S   = sum_w 2 n_s^2          (measurement_dim, geometry.hpp:176)          */
+    long long n_act;       /* A   = sum_m n_act^2          (MirrorShapes, reconstructor.hpp:34-41)      */
+    long long n_wavefront; /* N_w = sum_w (n_s+1)^2                                                    */
+    int n_layers, n_wfs, n_dms, pcg_iters, batch, precision;
+} fewha_gpu_dims_t;
+
+/* Caller-owned host buffers for ReconstructorState (reconstructor.hpp:61-92). */
+typedef struct {
+    double *c, *b, *r, *p, *q; /* n each */
+    double scalars[3];         /* PcgScalars {rho_old, alpha, fresh}, pcg.hpp:32-38 */
+    double *a_prev2, *a_prev;  /* A each */
+} fewha_gpu_state_t;
+
+/* Device pointers (for CUDA-resident callers; valid until destroy). */
+typedef struct {
+    void* slopes;   /* [batch][S]  fp64 input slot read by fewha_gpu_step_device  */
+    void* coeffs;   /* [batch][n]  st.c, element type = precision                  */
+    void* dm;       /* [batch][A]  a^(1) of the last frame, element type = precision */
+    double* rho;    /* [batch][iters] rho log of the last frame                   */
+    int* status;    /* [batch] 0 ok, 1 non-finite PCG scalar                      */
+    int* n_rho;     /* [batch] rho log length (< iters only with pcg_tolerance)    */
+} fewha_gpu_device_t;
+
+/* --- lifecycle ------------------------------------------------------------ */
+
+/* load_config (config_io.hpp:181) + Reconstructor(geometry) (reconstructor.hpp:112).
+ * precision: 64 or 32.  batch >= 1 independent instances.  device: CUDA ordinal.
+ * Parses the JSON preset, validates it (geometry.hpp:281-362, same messages)
+ * and derives extents and active masks (finalize_geometry, geometry.hpp:366-377).
+ * L != M presets are accepted only with "fitting": see DESIGN.md (L=M otherwise,
+ * as the reference).  */
+int fewha_gpu_create(const char* preset_json_path, int precision, int batch, int device, fewha_gpu_t* out);
+int fewha_gpu_create_from_json(const char* json_text, int precision, int batch, int device, fewha_gpu_t* out);
+/* loop_mode: -1 keep, 0 closed, 1 open; gain < 0 keeps (test hooks, like editing SystemGeometry) */
+int fewha_gpu_override_loop(fewha_gpu_t h, int loop_mode, double gain);
+const char* fewha_gpu_create_error(void);
+const char* fewha_gpu_last_error(fewha_gpu_t h);
+void fewha_gpu_destroy(fewha_gpu_t h);
+
+int fewha_gpu_dims(fewha_gpu_t h, fewha_gpu_dims_t* out);
+/* Host-only preset derivation (no device touched): load_config + finalize_geometry
+ * (config_io.hpp:181, geometry.hpp:366-377).  Any output may be NULL. */
+int fewha_gpu_preset_info(const char* preset_json_path, fewha_gpu_dims_t* dims, double* layer_extent,
+                          double* dm_extent, unsigned char* masks);
+/* derived geometry: layer extents [L], DM extents [M], masks [sum n_s^2] (uint8) */
+int fewha_gpu_geometry(fewha_gpu_t h, double* layer_extent, double* dm_extent, unsigned char* masks);
+
+/* --- preconditioner (Reconstructor::build_preconditioner, reconstructor.hpp:250;
+ *     preconditioner_build, operators.hpp:367-425).  Built on the device from
+ *     batched apply_M probes; lazily by the first step if never called. */
+int fewha_gpu_build_preconditioner(fewha_gpu_t h);
+int fewha_gpu_preconditioner(fewha_gpu_t h, double* out /* n */);
+
+/* --- the hot path: Reconstructor::step (reconstructor.hpp:310-355) ---------
+ * slopes [batch][S] (host, fp64).  Outputs may be NULL:
+ *   coeffs_out [batch][n] = st.c after the step; dm_out [batch][A] = a^(1);
+ *   rho_out [batch][iters] = last_telemetry().rho; n_rho [batch].  */
+int fewha_gpu_step(fewha_gpu_t h, const double* slopes, double* coeffs_out, double* dm_out, double* rho_out,
+                   int* n_rho);
+/* ReconstructorState::reset (reconstructor.hpp:81-91) on every instance */
+int fewha_gpu_reset(fewha_gpu_t h);
+int fewha_gpu_get_state(fewha_gpu_t h, int instance, fewha_gpu_state_t* st);
+int fewha_gpu_set_state(fewha_gpu_t h, int instance, const fewha_gpu_state_t* st);
+
+/* --- CUDA-resident path (benchmarks, pipelines) ------------------------- */
+int fewha_gpu_set_stream(fewha_gpu_t h, void* cuda_stream);
+int fewha_gpu_device_buffers(fewha_gpu_t h, fewha_gpu_device_t* out);
+/* Stage slopes [batch][S] fp64 into the resident slot, asynchronously on the
+ * handle's stream (src on the device when on_device != 0, else host). */
+int fewha_gpu_load_slopes(fewha_gpu_t h, const void* src, int on_device);
+/* One frame from device slopes [batch][S] fp64 (NULL: use the library's slopes
+ * slot).  Asynchronous on the handle's stream; no status check. */
+int fewha_gpu_step_device(fewha_gpu_t h, const void* d_slopes);
+/* Synchronise the stream and report the per-instance PCG status. */
+int fewha_gpu_sync(fewha_gpu_t h);
+/* Kernel launches of one step_device frame (for launch accounting). */
+int fewha_gpu_launches_per_step(fewha_gpu_t h);
+/* Runs ONE frame eagerly (not from the graph) with a CUDA event after every
+ * launch on the handle's stream; writes per-launch device ms and kernel kind
+ * (0 wfs_rhs, 1 adjoint, 2 fwd_rhs, 3 inv_pcg0, 4 inv_pcg, 5 wfs, 6 fwd_pcg,
+ * 7 inv_fit, 8 fit_control).  Advances the state like a step.  Returns the
+ * number of launches (< 0 on error). */
+int fewha_gpu_profile_step(fewha_gpu_t h, float* ms, int* kinds, int max);
+
+/* --- operator entry points (reconstructor.hpp:141-305, operators.hpp) ------
+ * Each applies the operator to `count` stacked inputs (host, fp64). */
+int fewha_gpu_apply_M(fewha_gpu_t h, const double* in, double* out, int count);              /* :166-212 */
+int fewha_gpu_build_rhs(fewha_gpu_t h, const double* meas, double* b_out, int count);        /* :215-247 */
+int fewha_gpu_add_dm_slopes(fewha_gpu_t h, const double* a, double* meas_inout, int count);  /* :259-280 */
+int fewha_gpu_fit_to_mirrors(fewha_gpu_t h, const double* c, double* a_out, int count);      /* :284-305 */
+int fewha_gpu_wavelet(fewha_gpu_t h, int inverse, double* data, int count); /* wavelet.hpp:115-143 per layer */
+int fewha_gpu_propagate(fewha_gpu_t h, const double* layers, double* wf, int count);         /* operators.hpp:217 */
+int fewha_gpu_propagate_transpose(fewha_gpu_t h, const double* wf, double* layers, int count); /* :241-268 */
+int fewha_gpu_sh(fewha_gpu_t h, const double* wf, double* meas, int count);                  /* :145-164 */
+int fewha_gpu_sh_transpose(fewha_gpu_t h, const double* meas, double* wf, int count);        /* :168-188 */
+/* Noise-free forward model s = Gamma (P phi - P_dm a) (simulation.hpp:164-199);
+ * a may be NULL (no correction).  layers: nodal [count][n]. */
+int fewha_gpu_forward_slopes(fewha_gpu_t h, const double* layers, const double* a, double* meas, int count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,212 @@
+// extern "C" boundary (include/fewha_gpu.h): maps C++ exceptions onto the
+// reference's error taxonomy -- config_error -> FEWHA_CONFIG (CLI exit 2),
+// runtime_error -> FEWHA_RUNTIME (exit 1), invalid_argument -> FEWHA_ARG
+// (tools/fewha_cli.cpp:31-33, :157-163).
+#include "fewha_gpu.h"
+
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "engine.hpp"
+
+using fewha_gpu::ArgError;
+using fewha_gpu::ConfigError;
+using fewha_gpu::Engine;
+
+struct fewha_gpu_handle {
+    std::unique_ptr<Engine> eng;
+    std::string err;
+};
+
+namespace {
+thread_local std::string g_create_error;
+
+template <typename F>
+int guard(std::string& err, F&& f) {
+    try {
+        f();
+        err.clear();
+        return FEWHA_OK;
+    } catch (const ConfigError& e) {
+        err = e.what();
+        return FEWHA_CONFIG;
+    } catch (const ArgError& e) {
+        err = e.what();
+        return FEWHA_ARG;
+    } catch (const std::invalid_argument& e) {
+        err = e.what();
+        return FEWHA_ARG;
+    } catch (const std::exception& e) {
+        err = e.what();
+        return FEWHA_RUNTIME;
+    }
+}
+
+int create(fewha_gpu::Geometry (*parse)(const std::string&), const char* src, int precision, int batch, int device,
+           fewha_gpu_t* out) {
+    if (!out || !src) {
+        g_create_error = "null argument";
+        return FEWHA_ARG;
+    }
+    *out = nullptr;
+    return guard(g_create_error, [&] {
+        auto h = std::make_unique<fewha_gpu_handle>();
+        h->eng = std::make_unique<Engine>(parse(src), precision, batch, device);
+        *out = h.release();
+    });
+}
+
+#define H_GUARD(body)                    \
+    if (!h) return FEWHA_ARG;            \
+    return guard(h->err, [&] { body; });
+}  // namespace
+
+extern "C" {
+
+int fewha_gpu_create(const char* path, int precision, int batch, int device, fewha_gpu_t* out) {
+    return create(&fewha_gpu::parse_preset_file, path, precision, batch, device, out);
+}
+
+int fewha_gpu_create_from_json(const char* text, int precision, int batch, int device, fewha_gpu_t* out) {
+    return create(&fewha_gpu::parse_preset_text, text, precision, batch, device, out);
+}
+
+int fewha_gpu_override_loop(fewha_gpu_t h, int loop_mode, double gain) { H_GUARD(h->eng->override_loop(loop_mode, gain)) }
+
+const char* fewha_gpu_create_error(void) { return g_create_error.c_str(); }
+const char* fewha_gpu_last_error(fewha_gpu_t h) { return h ? h->err.c_str() : "null handle"; }
+void fewha_gpu_destroy(fewha_gpu_t h) { delete h; }
+
+int fewha_gpu_dims(fewha_gpu_t h, fewha_gpu_dims_t* d) {
+    H_GUARD({
+        const auto& g = h->eng->geometry();
+        d->n_coeff = static_cast<long long>(g.coeff_dim());
+        d->n_slopes = static_cast<long long>(g.measurement_dim());
+        d->n_act = static_cast<long long>(g.act_dim());
+        d->n_wavefront = static_cast<long long>(g.wavefront_dim());
+        d->n_layers = static_cast<int>(g.layers.size());
+        d->n_wfs = static_cast<int>(g.wfs.size());
+        d->n_dms = static_cast<int>(g.dms.size());
+        d->pcg_iters = g.pcg_iters;
+        d->batch = h->eng->batch();
+        d->precision = h->eng->precision();
+    })
+}
+
+int fewha_gpu_preset_info(const char* path, fewha_gpu_dims_t* d, double* layer_extent, double* dm_extent,
+                          unsigned char* masks) {
+    if (!path) return FEWHA_ARG;
+    return guard(g_create_error, [&] {
+        const auto g = fewha_gpu::parse_preset_file(path);
+        if (d) {
+            d->n_coeff = static_cast<long long>(g.coeff_dim());
+            d->n_slopes = static_cast<long long>(g.measurement_dim());
+            d->n_act = static_cast<long long>(g.act_dim());
+            d->n_wavefront = static_cast<long long>(g.wavefront_dim());
+            d->n_layers = static_cast<int>(g.layers.size());
+            d->n_wfs = static_cast<int>(g.wfs.size());
+            d->n_dms = static_cast<int>(g.dms.size());
+            d->pcg_iters = g.pcg_iters;
+            d->batch = 0;
+            d->precision = 0;
+        }
+        if (layer_extent)
+            for (size_t l = 0; l < g.layers.size(); ++l) layer_extent[l] = g.layers[l].extent;
+        if (dm_extent)
+            for (size_t m = 0; m < g.dms.size(); ++m) dm_extent[m] = g.dms[m].extent;
+        if (masks)
+            for (const auto& w : g.wfs) {
+                std::memcpy(masks, w.mask.data(), w.mask.size());
+                masks += w.mask.size();
+            }
+    });
+}
+
+int fewha_gpu_geometry(fewha_gpu_t h, double* layer_extent, double* dm_extent, unsigned char* masks) {
+    H_GUARD({
+        const auto& g = h->eng->geometry();
+        for (size_t l = 0; l < g.layers.size(); ++l) layer_extent[l] = g.layers[l].extent;
+        for (size_t m = 0; m < g.dms.size(); ++m) dm_extent[m] = g.dms[m].extent;
+        for (const auto& w : g.wfs) {
+            std::memcpy(masks, w.mask.data(), w.mask.size());
+            masks += w.mask.size();
+        }
+    })
+}
+
+int fewha_gpu_build_preconditioner(fewha_gpu_t h) { H_GUARD(h->eng->build_preconditioner()) }
+
+int fewha_gpu_preconditioner(fewha_gpu_t h, double* out) {
+    H_GUARD({
+        if (!h->eng->has_preconditioner()) h->eng->build_preconditioner();
+        const auto v = h->eng->preconditioner();
+        std::memcpy(out, v.data(), v.size() * sizeof(double));
+    })
+}
+
+int fewha_gpu_step(fewha_gpu_t h, const double* slopes, double* coeffs, double* dm, double* rho, int* n_rho) {
+    H_GUARD({
+        if (!slopes) throw ArgError("step: null slopes");
+        h->eng->step(slopes, coeffs, dm, rho, n_rho);
+    })
+}
+
+int fewha_gpu_reset(fewha_gpu_t h) { H_GUARD(h->eng->reset()) }
+
+int fewha_gpu_get_state(fewha_gpu_t h, int instance, fewha_gpu_state_t* st) {
+    H_GUARD(h->eng->get_state(instance, st->c, st->b, st->r, st->p, st->q, st->scalars, st->a_prev2, st->a_prev))
+}
+
+int fewha_gpu_set_state(fewha_gpu_t h, int instance, const fewha_gpu_state_t* st) {
+    H_GUARD(h->eng->set_state(instance, st->c, st->b, st->r, st->p, st->q, st->scalars, st->a_prev2, st->a_prev))
+}
+
+int fewha_gpu_set_stream(fewha_gpu_t h, void* stream) { H_GUARD(h->eng->set_stream(stream)) }
+
+int fewha_gpu_device_buffers(fewha_gpu_t h, fewha_gpu_device_t* o) {
+    H_GUARD(h->eng->device_buffers(&o->slopes, &o->coeffs, &o->dm, &o->rho, &o->status, &o->n_rho))
+}
+
+int fewha_gpu_load_slopes(fewha_gpu_t h, const void* src, int on_device) {
+    H_GUARD({
+        if (!src) throw ArgError("load_slopes: null source");
+        h->eng->load_slopes(src, on_device != 0);
+    })
+}
+int fewha_gpu_step_device(fewha_gpu_t h, const void* d_slopes) { H_GUARD(h->eng->step_device(d_slopes)) }
+int fewha_gpu_sync(fewha_gpu_t h) { H_GUARD(h->eng->sync_check()) }
+int fewha_gpu_launches_per_step(fewha_gpu_t h) { return h ? h->eng->launches_per_step() : -1; }
+int fewha_gpu_profile_step(fewha_gpu_t h, float* ms, int* kinds, int max) {
+    if (!h) return -1;
+    int n = -1;
+    const int rc = guard(h->err, [&] { n = h->eng->profile_step(ms, kinds, max); });
+    return rc ? -rc : n;
+}
+
+int fewha_gpu_apply_M(fewha_gpu_t h, const double* in, double* out, int count) { H_GUARD(h->eng->apply_M(in, out, count)) }
+int fewha_gpu_build_rhs(fewha_gpu_t h, const double* meas, double* out, int count) {
+    H_GUARD(h->eng->build_rhs(meas, out, count))
+}
+int fewha_gpu_add_dm_slopes(fewha_gpu_t h, const double* a, double* meas, int count) {
+    H_GUARD(h->eng->add_dm_slopes(a, meas, count))
+}
+int fewha_gpu_fit_to_mirrors(fewha_gpu_t h, const double* c, double* a, int count) { H_GUARD(h->eng->fit(c, a, count)) }
+int fewha_gpu_wavelet(fewha_gpu_t h, int inverse, double* data, int count) {
+    H_GUARD(h->eng->wavelet(inverse, data, count))
+}
+int fewha_gpu_propagate(fewha_gpu_t h, const double* layers, double* wf, int count) {
+    H_GUARD(h->eng->propagate(layers, wf, count))
+}
+int fewha_gpu_propagate_transpose(fewha_gpu_t h, const double* wf, double* layers, int count) {
+    H_GUARD(h->eng->propagate_transpose(wf, layers, count))
+}
+int fewha_gpu_sh(fewha_gpu_t h, const double* wf, double* meas, int count) { H_GUARD(h->eng->sh(wf, meas, count)) }
+int fewha_gpu_sh_transpose(fewha_gpu_t h, const double* meas, double* wf, int count) {
+    H_GUARD(h->eng->sh_transpose(meas, wf, count))
+}
+int fewha_gpu_forward_slopes(fewha_gpu_t h, const double* layers, const double* a, double* meas, int count) {
+    H_GUARD(h->eng->forward_slopes(layers, a, meas, count))
+}
+
+}  // extern "C"

@@ -1,0 +1,1077 @@
+// Host engine of the B200-native FEWHA reconstructor (see engine.hpp).
+#include "engine.hpp"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstdint>
+#include <cmath>
+#include <cstring>
+#include <numbers>
+#include <stdexcept>
+#include <type_traits>
+
+#include "daubechies_table.h"
+#include "device.hpp"
+#include "kernels.cuh"
+
+namespace fewha_gpu {
+
+#define CK(x)                                                                                        \
+    do {                                                                                             \
+        cudaError_t e_ = (x);                                                                        \
+        if (e_ != cudaSuccess)                                                                       \
+            throw std::runtime_error(std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " + \
+                                     __FILE__ + ":" + std::to_string(__LINE__));                     \
+    } while (0)
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// Geometry tables (host, fp64, reference expressions)
+// ---------------------------------------------------------------------------
+
+struct Stencil1 {
+    int idx;
+    double f;
+};
+
+// 1-D half of bilinear_stencil (operators.hpp:108-121): u = (p + e/2)/spacing,
+// j0 = min(floor(u), n-2), f = u - j0 (before clamping at 0), idx = max(j0, 0).
+Stencil1 stencil1(int n, double extent, double p) {
+    const double spacing = extent / (n - 1);
+    const double u = (p + extent / 2.0) / spacing;
+    constexpr double eps = 1e-9;
+    if (u < -eps || u > n - 1 + eps) throw std::runtime_error("propagation: evaluation point outside layer grid");
+    const int j0 = std::min(static_cast<int>(std::floor(u)), n - 2);
+    return {std::max(j0, 0), u - j0};
+}
+
+struct Plan {
+    GeoParams gp{};
+    std::vector<int> ti;
+    std::vector<double> td;
+    std::vector<std::uint8_t> masks;
+    std::vector<int> wtiles, ltiles;
+    int maxside = 0;
+};
+
+int push_table(Plan& pl, const std::vector<Stencil1>& t) {
+    const int off = static_cast<int>(pl.ti.size());
+    for (const auto& s : t) {
+        pl.ti.push_back(s.idx);
+        pl.td.push_back(s.f);
+    }
+    return off;
+}
+
+// ranges[I] = [first, last+1) of source nodes whose stencil touches target node I
+int push_ranges(Plan& pl, const std::vector<Stencil1>& t, int n_target) {
+    const int off = static_cast<int>(pl.ti.size());
+    for (int I = 0; I < n_target; ++I) {
+        int lo = static_cast<int>(t.size()), hi = 0;
+        for (int j = 0; j < static_cast<int>(t.size()); ++j) {
+            if (t[j].idx == I || t[j].idx + 1 == I) {
+                lo = std::min(lo, j);
+                hi = std::max(hi, j + 1);
+            }
+        }
+        if (hi <= lo) lo = hi = 0;
+        pl.ti.push_back(lo);
+        pl.ti.push_back(hi);
+        pl.td.push_back(0.0);
+        pl.td.push_back(0.0);
+    }
+    return off;
+}
+
+Plan build_plan(const Geometry& g, int elem_bytes) {
+    Plan pl;
+    GeoParams& gp = pl.gp;
+    const int L = static_cast<int>(g.layers.size()), W = static_cast<int>(g.wfs.size()),
+              M = static_cast<int>(g.dms.size());
+    if (L > kMaxL || W > kMaxW || M > kMaxM)
+        throw ConfigError("invalid geometry: at most 16 layers, 16 wfs and 16 dms are supported on the device");
+    gp.L = L;
+    gp.W = W;
+    gp.M = M;
+    gp.n = static_cast<int>(g.coeff_dim());
+    gp.S = static_cast<int>(g.measurement_dim());
+    gp.Nw = static_cast<int>(g.wavefront_dim());
+    gp.A = static_cast<int>(g.act_dim());
+    gp.iters = g.pcg_iters;
+    gp.closed = g.closed_loop ? 1 : 0;
+    gp.alpha = g.alpha;
+    gp.gain = g.gain;
+    gp.tol = g.pcg_tol;
+    gp.fault = g.fault == "sh_adjoint" ? 1.0 + 1e-6 : 1.0;  // reconstructor.hpp:120
+    gp.filt_off = kDaubechiesOffset[g.wavelet_order - 1];
+    int off = 0;
+    for (int l = 0; l < L; ++l) {
+        if (g.layers[l].order > 7)
+            throw ConfigError("invalid geometry: layer grid_order > 7 exceeds the on-chip transform (see DESIGN.md)");
+        gp.side[l] = g.layers[l].side();
+        gp.lorder[l] = g.layers[l].order;
+        gp.coff[l] = off;
+        off += gp.side[l] * gp.side[l];
+        pl.maxside = std::max(pl.maxside, gp.side[l]);
+    }
+    gp.maxside = pl.maxside;
+    int mo = 0, wo = 0, mk = 0;
+    for (int w = 0; w < W; ++w) {
+        const int ns = g.wfs[w].n_subap;
+        gp.ns[w] = ns;
+        gp.moff[w] = mo;
+        gp.woff[w] = wo;
+        gp.mkoff[w] = mk;
+        gp.inv_var[w] = 1.0 / g.wfs[w].noise_variance;  // operators.hpp:280
+        mo += 2 * ns * ns;
+        wo += (ns + 1) * (ns + 1);
+        mk += ns * ns;
+        pl.masks.insert(pl.masks.end(), g.wfs[w].mask.begin(), g.wfs[w].mask.end());
+    }
+    int ao = 0;
+    for (int m = 0; m < M; ++m) {
+        gp.nact[m] = g.dms[m].n_act;
+        gp.aoff[m] = ao;
+        ao += g.dms[m].n_act * g.dms[m].n_act;
+    }
+
+    // directory slots first, filled below
+    gp.o_pl = 0;
+    pl.ti.assign(static_cast<size_t>(W * L * 4 + W * M * 2 + M + L), 0);
+    pl.td.assign(pl.ti.size(), 0.0);
+    gp.o_pd = W * L * 4;
+    gp.o_fit = gp.o_pd + W * M * 2;
+    gp.o_reg = gp.o_fit + M;
+
+    auto aperture_axis = [&](int w, const Star& s, double h, int n, double extent, bool x_axis) {
+        const int np = g.wfs[w].n_subap + 1;
+        const double d = g.diameter / (np - 1);
+        const double c = s.footprint(h);
+        std::vector<Stencil1> t(static_cast<size_t>(np));
+        for (int j = 0; j < np; ++j) {
+            const double x = -g.diameter / 2.0 + j * d;  // operators.hpp:227-231
+            const double p = c * x + (x_axis ? s.theta_x : s.theta_y) * h;
+            t[j] = stencil1(n, extent, p);
+        }
+        return t;
+    };
+
+    for (int w = 0; w < W; ++w) {
+        for (int l = 0; l < L; ++l) {
+            const auto& lay = g.layers[l];
+            const auto tx = aperture_axis(w, g.stars[w], lay.height, lay.side(), lay.extent, true);
+            const auto ty = aperture_axis(w, g.stars[w], lay.height, lay.side(), lay.extent, false);
+            int* dir = &pl.ti[static_cast<size_t>((w * L + l) * 4)];
+            const int ox = push_table(pl, tx), oy = push_table(pl, ty);
+            const int orr = push_ranges(pl, ty, lay.side()), occ = push_ranges(pl, tx, lay.side());
+            dir = &pl.ti[static_cast<size_t>((w * L + l) * 4)];
+            dir[0] = ox;
+            dir[1] = oy;
+            dir[2] = orr;
+            dir[3] = occ;
+        }
+        for (int m = 0; m < M; ++m) {
+            const auto& dm = g.dms[m];
+            const auto tx = aperture_axis(w, g.stars[w], dm.height, dm.n_act, dm.extent, true);
+            const auto ty = aperture_axis(w, g.stars[w], dm.height, dm.n_act, dm.extent, false);
+            const int ox = push_table(pl, tx), oy = push_table(pl, ty);
+            pl.ti[static_cast<size_t>(gp.o_pd + (w * M + m) * 2)] = ox;
+            pl.ti[static_cast<size_t>(gp.o_pd + (w * M + m) * 2 + 1)] = oy;
+        }
+    }
+    // fitting tables (reconstructor.hpp:294-302): DM m samples layer m
+    for (int m = 0; m < M; ++m) {
+        const auto& dm = g.dms[m];
+        const int side = g.layers[m].side();
+        if (dm.n_act == side) {
+            pl.ti[static_cast<size_t>(gp.o_fit + m)] = -1;
+            continue;
+        }
+        const double da = dm.extent / (dm.n_act - 1);
+        std::vector<Stencil1> t(static_cast<size_t>(dm.n_act));
+        for (int j = 0; j < dm.n_act; ++j) t[j] = stencil1(side, dm.extent, -dm.extent / 2.0 + j * da);
+        pl.ti[static_cast<size_t>(gp.o_fit + m)] = push_table(pl, t);
+    }
+    // alpha * regularizer per (layer, scale) (operators.hpp:307-321)
+    const double kappa0 = 2.0 * std::numbers::pi / g.outer_scale;
+    for (int l = 0; l < L; ++l) {
+        const auto& lay = g.layers[l];
+        pl.ti[static_cast<size_t>(gp.o_reg + l)] = static_cast<int>(pl.td.size());
+        for (int j = 0; j <= lay.order; ++j) {
+            const double kappa = std::ldexp(2.0 * std::numbers::pi / lay.extent, j);
+            const double d = std::pow(kappa * kappa + kappa0 * kappa0, g.spectral_exponent) / lay.strength;
+            pl.td.push_back(g.alpha * d);
+            pl.ti.push_back(0);
+        }
+    }
+
+    // WFS tiles: 16 x 16 nodes
+    gp.wtile = 16;
+    for (int w = 0; w < W; ++w) {
+        const int np = g.wfs[w].n_subap + 1;
+        for (int i0 = 0; i0 < np; i0 += gp.wtile)
+            for (int j0 = 0; j0 < np; j0 += gp.wtile) pl.wtiles.insert(pl.wtiles.end(), {w, i0, j0});
+    }
+    gp.n_wtiles = static_cast<int>(pl.wtiles.size() / 3);
+
+    // layer tiles for the adjoint gather; shrink until the psi block fits.
+    // Per (tile, WFS) the exact source block: union of the per-node ranges.
+    std::vector<int> tr;
+    for (int tp : {32, 16, 8, 4, 2}) {
+        gp.ltile = tp;
+        pl.ltiles.clear();
+        tr.clear();
+        int rows_max = 1, cols_max = 1;
+        for (int l = 0; l < L; ++l) {
+            const int side = gp.side[l];
+            for (int I0 = 0; I0 < side; I0 += tp)
+                for (int J0 = 0; J0 < side; J0 += tp) {
+                    pl.ltiles.insert(pl.ltiles.end(), {l, I0, J0});
+                    const int nI = std::min(tp, side - I0), nJ = std::min(tp, side - J0);
+                    for (int w = 0; w < W; ++w) {
+                        const int* dir = &pl.ti[static_cast<size_t>((w * L + l) * 4)];
+                        auto span = [&](int ranges, int a0, int cnt) {
+                            int lo = INT32_MAX, hi = 0;
+                            for (int a = a0; a < a0 + cnt; ++a) {
+                                const int rl = pl.ti[ranges + 2 * a], rh = pl.ti[ranges + 2 * a + 1];
+                                if (rl < rh) {
+                                    lo = std::min(lo, rl);
+                                    hi = std::max(hi, rh);
+                                }
+                            }
+                            return lo < hi ? std::pair<int, int>{lo, hi} : std::pair<int, int>{0, 0};
+                        };
+                        const auto [ilo, ihi] = span(dir[2], I0, nI);
+                        const auto [jlo, jhi] = span(dir[3], J0, nJ);
+                        const bool hit = ilo < ihi && jlo < jhi;
+                        tr.insert(tr.end(), {hit ? ilo : 0, hit ? ihi : 0, hit ? jlo : 0, hit ? jhi : 0});
+                        if (!hit) continue;
+                        rows_max = std::max(rows_max, ihi - ilo);
+                        cols_max = std::max(cols_max, jhi - jlo);
+                    }
+                }
+        }
+        gp.lt_rows_max = rows_max;
+        gp.lt_cols_max = cols_max;
+        const size_t bytes = static_cast<size_t>(rows_max) * (cols_max + tp) * elem_bytes;
+        if (bytes <= 160 * 1024 && tp * tp <= 256 * 16) break;
+    }
+    gp.o_tr = static_cast<int>(pl.ti.size());
+    pl.ti.insert(pl.ti.end(), tr.begin(), tr.end());
+    pl.td.resize(pl.ti.size(), 0.0);
+    gp.n_ltiles = static_cast<int>(pl.ltiles.size() / 3);
+    return pl;
+}
+
+template <typename T>
+T* dalloc(size_t n) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+    CK(cudaMemset(p, 0, std::max<size_t>(n, 1) * sizeof(T)));
+    return static_cast<T*>(p);
+}
+
+struct DevFree {
+    std::vector<void*> ptrs;
+    void add(void* p) { ptrs.push_back(p); }
+    ~DevFree() {
+        for (void* p : ptrs) cudaFree(p);
+    }
+};
+
+// Per-batch device workspace of one element type.
+template <typename T>
+struct Work {
+    int count = 0;
+    Bufs<T> bf{};
+    T *in = nullptr, *out = nullptr, *a = nullptr;
+    double* meas = nullptr;
+    double* meas2 = nullptr;
+    void alloc(const GeoParams& gp, int cnt, DevFree& fr, bool state) {
+        count = cnt;
+        const size_t n = static_cast<size_t>(gp.n) * cnt;
+        auto A = [&](auto* tag, size_t k) {
+            using U = std::remove_pointer_t<decltype(tag)>;
+            U* p = dalloc<U>(k);
+            fr.add(p);
+            return p;
+        };
+        bf.phi = A((T*)nullptr, n);
+        bf.y = A((T*)nullptr, n);
+        bf.psi = A((T*)nullptr, static_cast<size_t>(gp.Nw) * cnt);
+        meas = A((double*)nullptr, static_cast<size_t>(gp.S) * cnt);
+        meas2 = A((double*)nullptr, static_cast<size_t>(gp.S) * cnt);
+        bf.meas = meas;
+        in = A((T*)nullptr, n);
+        out = A((T*)nullptr, n);
+        a = A((T*)nullptr, static_cast<size_t>(gp.A) * cnt);
+        bf.in = in;
+        bf.out = out;
+        bf.a_out = a;
+        bf.a_prev2 = a;
+        if (state) {
+            bf.c = A((T*)nullptr, n);
+            bf.b = A((T*)nullptr, n);
+            bf.r = A((T*)nullptr, n);
+            bf.p = A((T*)nullptr, n);
+            bf.q = A((T*)nullptr, n);
+            bf.mz = A((T*)nullptr, n);
+            const size_t aa = static_cast<size_t>(gp.A) * cnt;
+            bf.a_prev2 = A((T*)nullptr, aa);
+            bf.a_prev = A((T*)nullptr, aa);
+            bf.a_out = A((T*)nullptr, aa);
+            bf.carry = A((Carry*)nullptr, static_cast<size_t>(gp.iters + 1) * cnt);
+            const size_t np = static_cast<size_t>(gp.iters) * gp.L * cnt;
+            bf.rho_part = A((double*)nullptr, np);
+            bf.mu_part = A((double*)nullptr, np);
+            bf.rho_log = A((double*)nullptr, static_cast<size_t>(gp.iters) * cnt);
+            bf.status = A((int*)nullptr, cnt);
+            bf.nlog = A((int*)nullptr, cnt);
+        }
+    }
+};
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Typed launchers
+// ---------------------------------------------------------------------------
+template <typename T>
+struct Launch {
+    static int layer_threads(int side) { return std::max(128, std::min(1024, side * side / 8)); }
+    static size_t layer_smem(int side) { return static_cast<size_t>(side) * (side + 1) * sizeof(T); }
+    static size_t wfs_smem(const GeoParams& gp) {
+        const int H = gp.wtile + 2, Q = gp.wtile + 1;
+        return static_cast<size_t>(H * H + 2 * Q * Q) * sizeof(T);
+    }
+    static size_t adj_smem(const GeoParams& gp) {
+        return static_cast<size_t>(gp.lt_rows_max) * (gp.lt_cols_max + gp.ltile) * sizeof(T);
+    }
+
+    template <int FLEN>
+    static void set_attrs_flen(const GeoParams& gp) {
+        const int smem = static_cast<int>(layer_smem(gp.maxside));
+        CK(cudaFuncSetAttribute(k_layer_inverse<T, FLEN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        CK(cudaFuncSetAttribute(k_layer_forward<T, FLEN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    }
+    static void set_attrs(const GeoParams& gp, int flen) {
+        switch (flen) {
+            case 2: set_attrs_flen<2>(gp); break;
+            case 4: set_attrs_flen<4>(gp); break;
+            case 6: set_attrs_flen<6>(gp); break;
+            case 8: set_attrs_flen<8>(gp); break;
+            case 10: set_attrs_flen<10>(gp); break;
+            case 12: set_attrs_flen<12>(gp); break;
+            case 14: set_attrs_flen<14>(gp); break;
+            case 16: set_attrs_flen<16>(gp); break;
+            case 18: set_attrs_flen<18>(gp); break;
+            default: set_attrs_flen<20>(gp); break;
+        }
+        CK(cudaFuncSetAttribute(k_wfs<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wfs_smem(gp)));
+        CK(cudaFuncSetAttribute(k_wfs<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wfs_smem(gp)));
+        CK(cudaFuncSetAttribute(k_adjoint<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)adj_smem(gp)));
+    }
+
+    template <int FLEN>
+    static void layer_flen(bool inverse, const GeoParams& gp, const Bufs<T>& bf, int mode, int it, int count,
+                           cudaStream_t st, int fit_term) {
+        const dim3 grid(gp.L, count);
+        const int thr = layer_threads(gp.maxside);
+        const size_t smem = layer_smem(gp.maxside);
+        if (inverse) k_layer_inverse<T, FLEN><<<grid, thr, smem, st>>>(gp, bf, mode, it);
+        else k_layer_forward<T, FLEN><<<grid, thr, smem, st>>>(gp, bf, mode, it, fit_term);
+    }
+    static void layer(int flen, bool inverse, const GeoParams& gp, const Bufs<T>& bf, int mode, int it, int count,
+                      cudaStream_t st, int fit_term = 1) {
+        switch (flen) {
+            case 2: layer_flen<2>(inverse, gp, bf, mode, it, count, st, fit_term); break;
+            case 4: layer_flen<4>(inverse, gp, bf, mode, it, count, st, fit_term); break;
+            case 6: layer_flen<6>(inverse, gp, bf, mode, it, count, st, fit_term); break;
+            case 8: layer_flen<8>(inverse, gp, bf, mode, it, count, st, fit_term); break;
+            case 10: layer_flen<10>(inverse, gp, bf, mode, it, count, st, fit_term); break;
+            case 12: layer_flen<12>(inverse, gp, bf, mode, it, count, st, fit_term); break;
+            case 14: layer_flen<14>(inverse, gp, bf, mode, it, count, st, fit_term); break;
+            case 16: layer_flen<16>(inverse, gp, bf, mode, it, count, st, fit_term); break;
+            case 18: layer_flen<18>(inverse, gp, bf, mode, it, count, st, fit_term); break;
+            default: layer_flen<20>(inverse, gp, bf, mode, it, count, st, fit_term); break;
+        }
+    }
+    static void wfs(bool rhs, const GeoParams& gp, const Bufs<T>& bf, int with_dm, int count, cudaStream_t st) {
+        const dim3 grid(gp.n_wtiles, count);
+        if (rhs) k_wfs<T, true><<<grid, 256, wfs_smem(gp), st>>>(gp, bf, with_dm);
+        else k_wfs<T, false><<<grid, 256, wfs_smem(gp), st>>>(gp, bf, with_dm);
+    }
+    static void adjoint(const GeoParams& gp, const T* psi, T* y, int count, cudaStream_t st) {
+        k_adjoint<T><<<dim3(gp.n_ltiles, count), 256, adj_smem(gp), st>>>(gp, psi, y);
+    }
+    static void fit(const GeoParams& gp, const Bufs<T>& bf, int step, int count, cudaStream_t st) {
+        k_fit_control<T><<<dim3((gp.A + 255) / 256, count), 256, 0, st>>>(gp, bf, step);
+    }
+};
+
+// ---------------------------------------------------------------------------
+// Engine implementation
+// ---------------------------------------------------------------------------
+struct EngineImpl {
+    Geometry g;
+    int precision, batch, device, flen;
+    Plan plan;
+    DevFree fr;
+    GeoParams gp{};      // with device table pointers
+    cudaStream_t stream = nullptr, user_stream = nullptr;
+    bool own_stream = false;
+    cudaGraphExec_t graph = nullptr;
+    bool has_precond = false;
+    std::vector<double> precond;
+    void* jac = nullptr;
+    // state (precision T) -- one of the two is used
+    Work<double> sd, od, pd;  // state / ops / probes (fp64)
+    Work<float> sf, of;        // state / ops (fp32)
+
+    cudaStream_t s() const { return user_stream ? user_stream : stream; }
+
+    template <typename T>
+    Work<T>& state();
+    template <typename T>
+    Work<T>& ops();
+
+    void upload_plan() {
+        int* ti = dalloc<int>(plan.ti.size());
+        double* td = dalloc<double>(plan.td.size());
+        float* tf = dalloc<float>(plan.td.size());
+        std::uint8_t* mk = dalloc<std::uint8_t>(plan.masks.size());
+        int* wt = dalloc<int>(plan.wtiles.size());
+        int* lt = dalloc<int>(plan.ltiles.size());
+        for (void* p : {(void*)ti, (void*)td, (void*)tf, (void*)mk, (void*)wt, (void*)lt}) fr.add(p);
+        std::vector<float> tdf(plan.td.begin(), plan.td.end());
+        CK(cudaMemcpy(ti, plan.ti.data(), plan.ti.size() * sizeof(int), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(td, plan.td.data(), plan.td.size() * sizeof(double), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(tf, tdf.data(), tdf.size() * sizeof(float), cudaMemcpyHostToDevice));
+        if (!plan.masks.empty())
+            CK(cudaMemcpy(mk, plan.masks.data(), plan.masks.size(), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(wt, plan.wtiles.data(), plan.wtiles.size() * sizeof(int), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(lt, plan.ltiles.data(), plan.ltiles.size() * sizeof(int), cudaMemcpyHostToDevice));
+        gp = plan.gp;
+        gp.ti = ti;
+        gp.td = td;
+        gp.tf = tf;
+        gp.masks = mk;
+        gp.wtiles = wt;
+        gp.ltiles = lt;
+    }
+
+    static void upload_filters() {
+        double lo[110], hi[110];
+        float lof[110], hif[110];
+        for (int o = 1; o <= 10; ++o) {
+            const int off = kDaubechiesOffset[o - 1], len = kDaubechiesOffset[o] - off;
+            for (int k = 0; k < len; ++k) {
+                lo[off + k] = kDaubechies[off + k];
+                hi[off + k] = (k % 2 == 0 ? 1.0 : -1.0) * kDaubechies[off + len - 1 - k];
+            }
+        }
+        for (int k = 0; k < 110; ++k) {
+            lof[k] = static_cast<float>(lo[k]);
+            hif[k] = static_cast<float>(hi[k]);
+        }
+        CK(cudaMemcpyToSymbol(c_lo_d, lo, sizeof lo));
+        CK(cudaMemcpyToSymbol(c_hi_d, hi, sizeof hi));
+        CK(cudaMemcpyToSymbol(c_lo_f, lof, sizeof lof));
+        CK(cudaMemcpyToSymbol(c_hi_f, hif, sizeof hif));
+    }
+
+    void invalidate_graph() {
+        if (graph) cudaGraphExecDestroy(graph);
+        graph = nullptr;
+    }
+
+    // ---- one frame of Reconstructor::step on the state workspace ----------
+    // `mark(kind)` runs after every launch (profiling hook; a no-op for capture).
+    template <typename T, typename Mark>
+    void launch_frame(cudaStream_t st, Mark&& mark) {
+        Work<T>& w = state<T>();
+        Bufs<T> bf = w.bf;
+        bf.jac = static_cast<const T*>(jac);
+        const int B = batch;
+        // RHS with the pseudo open-loop term (reconstructor.hpp:316-323)
+        Launch<T>::wfs(true, gp, bf, gp.closed, B, st);
+        mark(kKindWfsRhs);
+        Launch<T>::adjoint(gp, bf.psi, bf.y, B, st);
+        mark(kKindAdjoint);
+        Launch<T>::layer(flen, false, gp, bf, kRhs, 0, B, st);
+        mark(kKindFwdRhs);
+        // fused PCG (pcg.hpp:68-106), the update of iteration k fused into k+1's W^-1
+        for (int it = 0; it < gp.iters; ++it) {
+            Launch<T>::layer(flen, true, gp, bf, kPcg, it, B, st);
+            mark(it == 0 ? kKindInvPcg0 : kKindInvPcg);
+            Launch<T>::wfs(false, gp, bf, 0, B, st);
+            mark(kKindWfs);
+            Launch<T>::adjoint(gp, bf.psi, bf.y, B, st);
+            mark(kKindAdjoint);
+            Launch<T>::layer(flen, false, gp, bf, kPcg, it, B, st);
+            mark(kKindFwdPcg);
+        }
+        // last update + fitting W^-1 c, then fit + control + rotation
+        Launch<T>::layer(flen, true, gp, bf, kFit, 0, B, st);
+        mark(kKindInvFit);
+        Launch<T>::fit(gp, bf, 1, B, st);
+        mark(kKindFit);
+        CK(cudaGetLastError());
+    }
+
+    template <typename T>
+    void launch_frame(cudaStream_t st) {
+        launch_frame<T>(st, [](int) {});
+    }
+
+    // Eager frame with an event after every launch: per-launch device times.
+    template <typename T>
+    int profile_frame(float* ms, int* kinds, int max) {
+        const cudaStream_t st = s();
+        std::vector<cudaEvent_t> ev;
+        std::vector<int> kk;
+        cudaEvent_t e0;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventRecord(e0, st));
+        launch_frame<T>(st, [&](int kind) {
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            CK(cudaEventRecord(e, st));
+            ev.push_back(e);
+            kk.push_back(kind);
+        });
+        CK(cudaEventSynchronize(ev.back()));
+        int n = 0;
+        cudaEvent_t prev = e0;
+        for (size_t i = 0; i < ev.size(); ++i) {
+            float t = 0.f;
+            CK(cudaEventElapsedTime(&t, prev, ev[i]));
+            if (n < max) {
+                ms[n] = t;
+                kinds[n] = kk[i];
+                ++n;
+            }
+            prev = ev[i];
+        }
+        for (auto e : ev) cudaEventDestroy(e);
+        cudaEventDestroy(e0);
+        return n;
+    }
+
+    template <typename T>
+    void ensure_graph() {
+        if (graph) return;
+        cudaGraph_t gr;
+        CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+        launch_frame<T>(stream);
+        CK(cudaStreamEndCapture(stream, &gr));
+        CK(cudaGraphInstantiate(&graph, gr, 0));
+        CK(cudaGraphDestroy(gr));
+    }
+
+    // ---- apply_M on a double workspace (also the preconditioner probes) ----
+    template <typename T>
+    void apply_M_dev(Work<T>& w, int count, cudaStream_t st) {
+        Bufs<T> bf = w.bf;
+        Launch<T>::layer(flen, true, gp, bf, kPlain, 0, count, st);
+        Launch<T>::wfs(false, gp, bf, 0, count, st);
+        Launch<T>::adjoint(gp, bf.psi, bf.y, count, st);
+        Launch<T>::layer(flen, false, gp, bf, kApply, 0, count, st);
+    }
+
+    void build_precond() {
+        CK(cudaSetDevice(device));
+        const size_t n = static_cast<size_t>(gp.n);
+        std::vector<double> diag(n, 0.0);
+        // probe list (operators.hpp:381-417)
+        struct Probe {
+            size_t rep;
+            int l, scale, oi, oj, block;
+        };
+        std::vector<Probe> probes;
+        if (g.precond == Precond::exact) {
+            if (static_cast<long long>(n) > g.dense_cap)
+                throw ConfigError("preconditioner: exact mode needs coefficient dimension <= " +
+                                  std::to_string(g.dense_cap) + ", got " + std::to_string(n));
+            for (size_t k = 0; k < n; ++k) probes.push_back({k, -1, 0, 0, 0, 0});
+        } else {
+            for (int l = 0; l < gp.L; ++l) {
+                const int side = gp.side[l], order = gp.lorder[l];
+                for (int scale = 0; scale <= order; ++scale) {
+                    const int block = scale == 0 ? 1 : 1 << (scale - 1);
+                    for (int orient = scale == 0 ? 0 : 1; orient <= (scale == 0 ? 0 : 3); ++orient) {
+                        const int oi = orient >= 2 ? block : 0;
+                        const int oj = (orient == 1 || orient == 3) ? block : 0;
+                        const size_t rep = gp.coff[l] + static_cast<size_t>(oi + block / 2) * side + (oj + block / 2);
+                        probes.push_back({rep, l, scale, oi, oj, block});
+                    }
+                }
+            }
+        }
+        const int chunk = static_cast<int>(std::min<size_t>(probes.size(), n <= 20000 ? 256 : 64));
+        if (pd.count < chunk) pd.alloc(gp, chunk, fr, false);
+        std::vector<double> probed(probes.size());
+        std::vector<double> one(1, 1.0), got(1);
+        for (size_t p0 = 0; p0 < probes.size(); p0 += chunk) {
+            const int cnt = static_cast<int>(std::min<size_t>(chunk, probes.size() - p0));
+            CK(cudaMemsetAsync(pd.in, 0, sizeof(double) * n * cnt, stream));
+            for (int k = 0; k < cnt; ++k)
+                CK(cudaMemcpyAsync(pd.in + k * n + probes[p0 + k].rep, one.data(), sizeof(double),
+                                   cudaMemcpyHostToDevice, stream));
+            apply_M_dev<double>(pd, cnt, stream);
+            for (int k = 0; k < cnt; ++k)
+                CK(cudaMemcpyAsync(&probed[p0 + k], pd.out + k * n + probes[p0 + k].rep, sizeof(double),
+                                   cudaMemcpyDeviceToHost, stream));
+            CK(cudaStreamSynchronize(stream));
+        }
+        for (size_t k = 0; k < probes.size(); ++k) {
+            const Probe& pr = probes[k];
+            if (pr.l < 0) {
+                diag[pr.rep] = probed[k];
+                continue;
+            }
+            const double alpha_d = plan.td[plan.ti[gp.o_reg + pr.l] + pr.scale];
+            double value;
+            if (g.precond == Precond::balanced) {
+                const double ex = g.balance_exponent;
+                value = std::pow(probed[k], ex) * std::pow(alpha_d, 1.0 - ex);
+            } else {
+                const double t_hat = probed[k] - alpha_d;
+                const double wgt = pr.scale == 0 ? g.coarse_weight : 1.0;
+                value = alpha_d + wgt * t_hat;
+            }
+            const int side = gp.side[pr.l];
+            for (int i = pr.oi; i < pr.oi + pr.block; ++i)
+                for (int j = pr.oj; j < pr.oj + pr.block; ++j) diag[gp.coff[pr.l] + static_cast<size_t>(i) * side + j] = value;
+        }
+        for (double v : diag)
+            if (!(v > 0.0))
+                throw std::runtime_error("preconditioner: non-positive diagonal entry (operator symmetry broken?)");
+        precond = diag;
+        if (precision == 64) {
+            CK(cudaMemcpy(jac, diag.data(), n * sizeof(double), cudaMemcpyHostToDevice));
+        } else {
+            std::vector<float> f(diag.begin(), diag.end());
+            CK(cudaMemcpy(jac, f.data(), n * sizeof(float), cudaMemcpyHostToDevice));
+        }
+        has_precond = true;
+    }
+};
+
+template <>
+Work<double>& EngineImpl::state<double>() { return sd; }
+template <>
+Work<float>& EngineImpl::state<float>() { return sf; }
+template <>
+Work<double>& EngineImpl::ops<double>() { return od; }
+template <>
+Work<float>& EngineImpl::ops<float>() { return of; }
+
+// ---------------------------------------------------------------------------
+
+namespace {
+template <typename T>
+void h2d_conv(T* dst, const double* src, size_t n, cudaStream_t st) {
+    if constexpr (std::is_same_v<T, double>) {
+        CK(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));
+    } else {
+        std::vector<float> tmp(src, src + n);
+        CK(cudaMemcpyAsync(dst, tmp.data(), n * sizeof(float), cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));
+    }
+}
+template <typename T>
+void d2h_conv(double* dst, const T* src, size_t n, cudaStream_t st) {
+    if constexpr (std::is_same_v<T, double>) {
+        CK(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    } else {
+        std::vector<float> tmp(n);
+        CK(cudaMemcpyAsync(tmp.data(), src, n * sizeof(float), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        std::copy(tmp.begin(), tmp.end(), dst);
+    }
+}
+}  // namespace
+
+Engine::Engine(Geometry g, int precision, int batch, int device) : p_(std::make_unique<EngineImpl>()) {
+    if (precision != 64 && precision != 32) throw ArgError("precision must be 64 or 32");
+    if (batch < 1) throw ArgError("batch must be >= 1");
+    auto& P = *p_;
+    P.g = std::move(g);
+    P.precision = precision;
+    P.batch = batch;
+    P.device = device;
+    P.flen = 2 * P.g.wavelet_order;
+    P.plan = build_plan(P.g, precision / 8);
+    P.plan.gp.piston_exact = precision == 32 ? 1 : 0;
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) throw ArgError("device ordinal out of range");
+    CK(cudaSetDevice(device));
+    EngineImpl::upload_filters();
+    P.upload_plan();
+    CK(cudaStreamCreateWithFlags(&P.stream, cudaStreamNonBlocking));
+    P.own_stream = true;
+    if (precision == 64) {
+        Launch<double>::set_attrs(P.gp, P.flen);
+        P.sd.alloc(P.gp, batch, P.fr, true);
+        P.jac = dalloc<double>(P.gp.n);
+    } else {
+        Launch<float>::set_attrs(P.gp, P.flen);
+        P.sf.alloc(P.gp, batch, P.fr, true);
+        P.jac = dalloc<float>(P.gp.n);
+    }
+    Launch<double>::set_attrs(P.gp, P.flen);  // probes always fp64
+    P.fr.add(P.jac);
+    reset();
+}
+
+Engine::~Engine() {
+    if (!p_) return;
+    cudaSetDevice(p_->device);
+    p_->invalidate_graph();
+    if (p_->own_stream && p_->stream) cudaStreamDestroy(p_->stream);
+}
+
+const Geometry& Engine::geometry() const { return p_->g; }
+int Engine::precision() const { return p_->precision; }
+int Engine::batch() const { return p_->batch; }
+bool Engine::has_preconditioner() const { return p_->has_precond; }
+std::vector<double> Engine::preconditioner() const { return p_->precond; }
+
+void Engine::override_loop(int loop_mode, double gain) {
+    auto& P = *p_;
+    if (loop_mode == 0 || loop_mode == 1) {
+        P.g.closed_loop = loop_mode == 0;
+        P.gp.closed = loop_mode == 0 ? 1 : 0;
+    }
+    if (gain >= 0.0) {
+        if (gain > 1.0) throw ConfigError("invalid geometry: gain out of [0,1]");
+        P.g.gain = gain;
+        P.gp.gain = gain;
+    }
+    P.invalidate_graph();
+}
+
+void Engine::build_preconditioner() { p_->build_precond(); }
+
+void Engine::step(const double* slopes, double* coeffs, double* dm, double* rho, int* n_rho) {
+    auto& P = *p_;
+    CK(cudaSetDevice(P.device));
+    if (!P.has_precond) P.build_precond();
+    const size_t B = P.batch, S = P.gp.S, n = P.gp.n, A = P.gp.A, it = P.gp.iters;
+    const cudaStream_t st = P.s();
+    double* meas = P.precision == 64 ? P.sd.meas : P.sf.meas;
+    CK(cudaMemcpyAsync(meas, slopes, B * S * sizeof(double), cudaMemcpyHostToDevice, st));
+    if (P.precision == 64) P.ensure_graph<double>();
+    else P.ensure_graph<float>();
+    CK(cudaGraphLaunch(P.graph, st));
+    std::vector<int> status(B), nl(B);
+    const int* dstat = P.precision == 64 ? P.sd.bf.status : P.sf.bf.status;
+    const int* dnl = P.precision == 64 ? P.sd.bf.nlog : P.sf.bf.nlog;
+    const double* drho = P.precision == 64 ? P.sd.bf.rho_log : P.sf.bf.rho_log;
+    CK(cudaMemcpyAsync(status.data(), dstat, B * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(nl.data(), dnl, B * sizeof(int), cudaMemcpyDeviceToHost, st));
+    if (rho) CK(cudaMemcpyAsync(rho, drho, B * it * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (P.precision == 64) {
+        if (coeffs) CK(cudaMemcpyAsync(coeffs, P.sd.bf.c, B * n * sizeof(double), cudaMemcpyDeviceToHost, st));
+        if (dm) CK(cudaMemcpyAsync(dm, P.sd.bf.a_out, B * A * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    } else {
+        CK(cudaStreamSynchronize(st));
+        if (coeffs) d2h_conv<float>(coeffs, P.sf.bf.c, B * n, st);
+        if (dm) d2h_conv<float>(dm, P.sf.bf.a_out, B * A, st);
+    }
+    if (n_rho) std::copy(nl.begin(), nl.end(), n_rho);
+    for (size_t b = 0; b < B; ++b)
+        if (status[b]) throw std::runtime_error("pcg_solve: non-finite scalar (indefinite operator?)");
+}
+
+void Engine::reset() {
+    auto& P = *p_;
+    CK(cudaSetDevice(P.device));
+    const size_t B = P.batch, n = P.gp.n, A = P.gp.A;
+    auto zero_state = [&](auto& w, size_t es) {
+        for (void* ptr : {(void*)w.bf.c, (void*)w.bf.b, (void*)w.bf.r, (void*)w.bf.p, (void*)w.bf.q, (void*)w.bf.mz})
+            CK(cudaMemset(ptr, 0, B * n * es));
+        for (void* ptr : {(void*)w.bf.a_prev2, (void*)w.bf.a_prev, (void*)w.bf.a_out}) CK(cudaMemset(ptr, 0, B * A * es));
+        std::vector<Carry> c(B * (P.gp.iters + 1));
+        for (auto& x : c) x = Carry{0.0, 0.0, 0.0, 1, 0, 0, 0};  // PcgScalars{} : fresh
+        CK(cudaMemcpy(w.bf.carry, c.data(), c.size() * sizeof(Carry), cudaMemcpyHostToDevice));
+    };
+    if (P.precision == 64) zero_state(P.sd, sizeof(double));
+    else zero_state(P.sf, sizeof(float));
+}
+
+void Engine::get_state(int inst, double* c, double* b, double* r, double* p, double* q, double* sc, double* a_prev2,
+                       double* a_prev) {
+    auto& P = *p_;
+    if (inst < 0 || inst >= P.batch) throw ArgError("instance out of range");
+    CK(cudaSetDevice(P.device));
+    const size_t n = P.gp.n, A = P.gp.A;
+    auto get = [&](auto& w) {
+        using T = std::remove_pointer_t<decltype(w.bf.c)>;
+        const cudaStream_t st = P.s();
+        CK(cudaStreamSynchronize(st));
+        d2h_conv<T>(c, w.bf.c + inst * n, n, st);
+        d2h_conv<T>(b, w.bf.b + inst * n, n, st);
+        d2h_conv<T>(r, w.bf.r + inst * n, n, st);
+        d2h_conv<T>(p, w.bf.p + inst * n, n, st);
+        d2h_conv<T>(q, w.bf.q + inst * n, n, st);
+        d2h_conv<T>(a_prev2, w.bf.a_prev2 + inst * A, A, st);
+        d2h_conv<T>(a_prev, w.bf.a_prev + inst * A, A, st);
+        Carry cr;
+        CK(cudaMemcpy(&cr, w.bf.carry + inst * (P.gp.iters + 1), sizeof(Carry), cudaMemcpyDeviceToHost));
+        sc[0] = cr.rho_old;
+        sc[1] = cr.alpha;
+        sc[2] = cr.fresh ? 1.0 : 0.0;
+    };
+    if (P.precision == 64) get(P.sd);
+    else get(P.sf);
+}
+
+void Engine::set_state(int inst, const double* c, const double* b, const double* r, const double* p, const double* q,
+                       const double* sc, const double* a_prev2, const double* a_prev) {
+    auto& P = *p_;
+    if (inst < 0 || inst >= P.batch) throw ArgError("instance out of range");
+    CK(cudaSetDevice(P.device));
+    const size_t n = P.gp.n, A = P.gp.A;
+    auto set = [&](auto& w) {
+        using T = std::remove_pointer_t<decltype(w.bf.c)>;
+        const cudaStream_t st = P.s();
+        CK(cudaStreamSynchronize(st));
+        h2d_conv<T>(w.bf.c + inst * n, c, n, st);
+        h2d_conv<T>(w.bf.b + inst * n, b, n, st);
+        h2d_conv<T>(w.bf.r + inst * n, r, n, st);
+        h2d_conv<T>(w.bf.p + inst * n, p, n, st);
+        h2d_conv<T>(w.bf.q + inst * n, q, n, st);
+        h2d_conv<T>(w.bf.a_prev2 + inst * A, a_prev2, A, st);
+        h2d_conv<T>(w.bf.a_prev + inst * A, a_prev, A, st);
+        Carry cr{sc[0], sc[1], 0.0, sc[2] != 0.0 ? 1 : 0, 0, 0, 0};
+        CK(cudaMemcpy(w.bf.carry + inst * (P.gp.iters + 1), &cr, sizeof(Carry), cudaMemcpyHostToDevice));
+    };
+    if (P.precision == 64) set(P.sd);
+    else set(P.sf);
+}
+
+void Engine::set_stream(void* stream) {
+    p_->user_stream = static_cast<cudaStream_t>(stream);
+}
+
+void Engine::step_device(const void* d_slopes) {
+    auto& P = *p_;
+    CK(cudaSetDevice(P.device));
+    if (!P.has_precond) P.build_precond();
+    const cudaStream_t st = P.s();
+    double* meas = P.precision == 64 ? P.sd.meas : P.sf.meas;
+    if (d_slopes && d_slopes != meas)
+        CK(cudaMemcpyAsync(meas, d_slopes, sizeof(double) * P.gp.S * P.batch, cudaMemcpyDeviceToDevice, st));
+    if (P.precision == 64) P.ensure_graph<double>();
+    else P.ensure_graph<float>();
+    CK(cudaGraphLaunch(P.graph, st));
+}
+
+void Engine::load_slopes(const void* src, bool on_device) {
+    auto& P = *p_;
+    CK(cudaSetDevice(P.device));
+    double* meas = P.precision == 64 ? P.sd.meas : P.sf.meas;
+    CK(cudaMemcpyAsync(meas, src, sizeof(double) * P.gp.S * P.batch,
+                       on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, P.s()));
+}
+
+void Engine::sync_check() {
+    auto& P = *p_;
+    CK(cudaSetDevice(P.device));
+    const cudaStream_t st = P.s();
+    std::vector<int> status(P.batch);
+    const int* dstat = P.precision == 64 ? P.sd.bf.status : P.sf.bf.status;
+    CK(cudaMemcpyAsync(status.data(), dstat, status.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int s : status)
+        if (s) throw std::runtime_error("pcg_solve: non-finite scalar (indefinite operator?)");
+}
+
+int Engine::launches_per_step() const { return 6 + 4 * p_->gp.iters; }
+
+int Engine::profile_step(float* ms, int* kinds, int max) {
+    auto& P = *p_;
+    CK(cudaSetDevice(P.device));
+    if (!P.has_precond) P.build_precond();
+    return P.precision == 64 ? P.profile_frame<double>(ms, kinds, max) : P.profile_frame<float>(ms, kinds, max);
+}
+
+void Engine::device_buffers(void** slopes, void** coeffs, void** dm, double** rho, int** status, int** n_rho) {
+    auto& P = *p_;
+    auto fill = [&](auto& w) {
+        *slopes = w.meas;
+        *coeffs = w.bf.c;
+        *dm = w.bf.a_out;
+        *rho = w.bf.rho_log;
+        *status = w.bf.status;
+        *n_rho = w.bf.nlog;
+    };
+    if (P.precision == 64) fill(P.sd);
+    else fill(P.sf);
+}
+
+// ---- operator entry points --------------------------------------------------
+namespace {
+template <typename T, typename F>
+void with_ops(EngineImpl& P, int count, F&& f) {
+    if (count < 1) throw ArgError("count must be >= 1");
+    CK(cudaSetDevice(P.device));
+    Work<T>& w = P.ops<T>();
+    if (w.count < count) w.alloc(P.gp, std::max(count, w.count), P.fr, false);
+    f(w);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(P.stream));
+}
+}  // namespace
+
+#define FEWHA_DISPATCH(body)                        \
+    if (p_->precision == 64) {                      \
+        using T = double;                           \
+        body                                        \
+    } else {                                        \
+        using T = float;                            \
+        body                                        \
+    }
+
+void Engine::apply_M(const double* in, double* out, int count) {
+    auto& P = *p_;
+    FEWHA_DISPATCH({
+        with_ops<T>(P, count, [&](Work<T>& w) {
+            const size_t n = static_cast<size_t>(P.gp.n) * count;
+            h2d_conv<T>(w.in, in, n, P.stream);
+            P.apply_M_dev<T>(w, count, P.stream);
+            d2h_conv<T>(out, w.out, n, P.stream);
+        });
+    })
+}
+
+void Engine::build_rhs(const double* meas, double* out, int count) {
+    auto& P = *p_;
+    FEWHA_DISPATCH({
+        with_ops<T>(P, count, [&](Work<T>& w) {
+            CK(cudaMemcpy(w.meas, meas, sizeof(double) * P.gp.S * count, cudaMemcpyHostToDevice));
+            Bufs<T> bf = w.bf;
+            Launch<T>::wfs(true, P.gp, bf, 0, count, P.stream);
+            Launch<T>::adjoint(P.gp, bf.psi, bf.y, count, P.stream);
+            Launch<T>::layer(P.flen, false, P.gp, bf, kPlain, 0, count, P.stream);
+            d2h_conv<T>(out, w.out, static_cast<size_t>(P.gp.n) * count, P.stream);
+        });
+    })
+}
+
+void Engine::add_dm_slopes(const double* a, double* meas, int count) {
+    auto& P = *p_;
+    FEWHA_DISPATCH({
+        with_ops<T>(P, count, [&](Work<T>& w) {
+            h2d_conv<T>(w.a, a, static_cast<size_t>(P.gp.A) * count, P.stream);
+            CK(cudaMemcpy(w.meas, meas, sizeof(double) * P.gp.S * count, cudaMemcpyHostToDevice));
+            const int sub = P.gp.S / 2;
+            k_slopes<T><<<dim3((sub + 255) / 256, count), 256, 0, P.stream>>>(P.gp, nullptr, nullptr, w.a, T(1),
+                                                                               w.meas, w.meas2, count);
+            CK(cudaMemcpyAsync(meas, w.meas2, sizeof(double) * P.gp.S * count, cudaMemcpyDeviceToHost, P.stream));
+        });
+    })
+}
+
+void Engine::forward_slopes(const double* layers, const double* a, double* meas, int count) {
+    auto& P = *p_;
+    FEWHA_DISPATCH({
+        with_ops<T>(P, count, [&](Work<T>& w) {
+            h2d_conv<T>(w.in, layers, static_cast<size_t>(P.gp.n) * count, P.stream);
+            if (a) h2d_conv<T>(w.a, a, static_cast<size_t>(P.gp.A) * count, P.stream);
+            const int sub = P.gp.S / 2;
+            k_slopes<T><<<dim3((sub + 255) / 256, count), 256, 0, P.stream>>>(P.gp, nullptr, w.in, a ? w.a : nullptr,
+                                                                               T(-1), nullptr, w.meas2, count);
+            CK(cudaMemcpyAsync(meas, w.meas2, sizeof(double) * P.gp.S * count, cudaMemcpyDeviceToHost, P.stream));
+        });
+    })
+}
+
+void Engine::fit(const double* c, double* a, int count) {
+    auto& P = *p_;
+    FEWHA_DISPATCH({
+        with_ops<T>(P, count, [&](Work<T>& w) {
+            h2d_conv<T>(w.in, c, static_cast<size_t>(P.gp.n) * count, P.stream);
+            Bufs<T> bf = w.bf;
+            Launch<T>::layer(P.flen, true, P.gp, bf, kPlain, 0, count, P.stream);
+            Launch<T>::fit(P.gp, bf, 0, count, P.stream);
+            d2h_conv<T>(a, w.a, static_cast<size_t>(P.gp.A) * count, P.stream);
+        });
+    })
+}
+
+void Engine::wavelet(int inverse, double* data, int count) {
+    auto& P = *p_;
+    FEWHA_DISPATCH({
+        with_ops<T>(P, count, [&](Work<T>& w) {
+            const size_t n = static_cast<size_t>(P.gp.n) * count;
+            Bufs<T> bf = w.bf;
+            if (inverse) {
+                h2d_conv<T>(w.in, data, n, P.stream);
+                Launch<T>::layer(P.flen, true, P.gp, bf, kPlain, 0, count, P.stream);
+                d2h_conv<T>(data, bf.phi, n, P.stream);
+            } else {
+                h2d_conv<T>(bf.y, data, n, P.stream);
+                Launch<T>::layer(P.flen, false, P.gp, bf, kPlain, 0, count, P.stream, /*fit_term=*/0);
+                d2h_conv<T>(data, w.out, n, P.stream);
+            }
+        });
+    })
+}
+
+void Engine::propagate(const double* layers, double* wf, int count) {
+    auto& P = *p_;
+    FEWHA_DISPATCH({
+        with_ops<T>(P, count, [&](Work<T>& w) {
+            h2d_conv<T>(w.in, layers, static_cast<size_t>(P.gp.n) * count, P.stream);
+            k_propagate<T><<<dim3((P.gp.Nw + 255) / 256, count), 256, 0, P.stream>>>(P.gp, w.in, w.bf.psi, count);
+            d2h_conv<T>(wf, w.bf.psi, static_cast<size_t>(P.gp.Nw) * count, P.stream);
+        });
+    })
+}
+
+void Engine::propagate_transpose(const double* wf, double* layers, int count) {
+    auto& P = *p_;
+    FEWHA_DISPATCH({
+        with_ops<T>(P, count, [&](Work<T>& w) {
+            h2d_conv<T>(w.bf.psi, wf, static_cast<size_t>(P.gp.Nw) * count, P.stream);
+            Launch<T>::adjoint(P.gp, w.bf.psi, w.bf.y, count, P.stream);
+            d2h_conv<T>(layers, w.bf.y, static_cast<size_t>(P.gp.n) * count, P.stream);
+        });
+    })
+}
+
+void Engine::sh(const double* wf, double* meas, int count) {
+    auto& P = *p_;
+    FEWHA_DISPATCH({
+        with_ops<T>(P, count, [&](Work<T>& w) {
+            h2d_conv<T>(w.bf.psi, wf, static_cast<size_t>(P.gp.Nw) * count, P.stream);
+            const int sub = P.gp.S / 2;
+            k_slopes<T><<<dim3((sub + 255) / 256, count), 256, 0, P.stream>>>(P.gp, w.bf.psi, nullptr, nullptr, T(1),
+                                                                               nullptr, w.meas2, count);
+            CK(cudaMemcpyAsync(meas, w.meas2, sizeof(double) * P.gp.S * count, cudaMemcpyDeviceToHost, P.stream));
+        });
+    })
+}
+
+void Engine::sh_transpose(const double* meas, double* wf, int count) {
+    auto& P = *p_;
+    FEWHA_DISPATCH({
+        with_ops<T>(P, count, [&](Work<T>& w) {
+            CK(cudaMemcpy(w.meas, meas, sizeof(double) * P.gp.S * count, cudaMemcpyHostToDevice));
+            k_sh_transpose<T><<<dim3((P.gp.Nw + 255) / 256, count), 256, 0, P.stream>>>(P.gp, w.meas, w.bf.psi, count);
+            d2h_conv<T>(wf, w.bf.psi, static_cast<size_t>(P.gp.Nw) * count, P.stream);
+        });
+    })
+}
+
+}  // namespace fewha_gpu

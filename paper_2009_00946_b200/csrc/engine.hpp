@@ -1,0 +1,64 @@
+// Host-side engine: owns the geometry tables, the device-resident state of
+// `batch` reconstructor instances, and the captured per-frame CUDA graph.
+#pragma once
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "geometry.hpp"
+
+namespace fewha_gpu {
+
+struct EngineImpl;
+
+class Engine {
+public:
+    Engine(Geometry g, int precision, int batch, int device);
+    ~Engine();
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+
+    const Geometry& geometry() const;
+    int precision() const;
+    int batch() const;
+
+    void override_loop(int loop_mode, double gain);
+    void build_preconditioner();
+    bool has_preconditioner() const;
+    std::vector<double> preconditioner() const;
+
+    // Reconstructor::step for all instances; host fp64 buffers (outputs may be null).
+    void step(const double* slopes, double* coeffs, double* dm, double* rho, int* n_rho);
+    void reset();
+    void get_state(int instance, double* c, double* b, double* r, double* p, double* q, double* sc,
+                   double* a_prev2, double* a_prev);
+    void set_state(int instance, const double* c, const double* b, const double* r, const double* p,
+                   const double* q, const double* sc, const double* a_prev2, const double* a_prev);
+
+    // device-resident path
+    void set_stream(void* stream);
+    void step_device(const void* d_slopes);
+    void load_slopes(const void* src, bool on_device);
+    void sync_check();
+    int launches_per_step() const;
+    int profile_step(float* ms, int* kinds, int max);
+    void device_buffers(void** slopes, void** coeffs, void** dm, double** rho, int** status, int** n_rho);
+
+    // operator entry points (count stacked host inputs)
+    void apply_M(const double* in, double* out, int count);
+    void build_rhs(const double* meas, double* out, int count);
+    void add_dm_slopes(const double* a, double* meas, int count);
+    void fit(const double* c, double* a, int count);
+    void wavelet(int inverse, double* data, int count);
+    void propagate(const double* layers, double* wf, int count);
+    void propagate_transpose(const double* wf, double* layers, int count);
+    void sh(const double* wf, double* meas, int count);
+    void sh_transpose(const double* meas, double* wf, int count);
+    void forward_slopes(const double* layers, const double* a, double* meas, int count);
+
+private:
+    std::unique_ptr<EngineImpl> p_;
+};
+
+}  // namespace fewha_gpu
