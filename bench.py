@@ -253,7 +253,8 @@ def run_ours(args):
     F = 16
     stream_host = slope_stream(rec, args.preset, F, seed=1 + rank)
     stream = torch.from_numpy(stream_host).to(dev)
-    st = torch.cuda.current_stream(dev)
+    st = torch.cuda.Stream(dev)  # a real stream: events, flushes and the graph all order on it
+    torch.cuda.set_stream(st)
     rec.set_stream(st.cuda_stream)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     S = d["S"]
