@@ -130,6 +130,10 @@ int fewha_gpu_launches_per_step(fewha_gpu_t h);
  * 7 inv_fit, 8 fit_control).  Advances the state like a step.  Returns the
  * number of launches (< 0 on error). */
 int fewha_gpu_profile_step(fewha_gpu_t h, float* ms, int* kinds, int max);
+/* Profiling: the first call (out == NULL) enables per-phase %globaltimer stamps
+ * of the cluster layer kernels for later fewha_gpu_profile_step frames; a call
+ * with a buffer copies [32 launches][4096 blocks][16 stamps] (ns) out. */
+int fewha_gpu_phase_stamps(fewha_gpu_t h, unsigned long long* out, long long n);
 
 /* --- operator entry points (reconstructor.hpp:141-305, operators.hpp) ------
  * Each applies the operator to `count` stacked inputs (host, fp64). */

@@ -31,7 +31,7 @@ EXPORTS = (
     "fewha_gpu_last_error", "fewha_gpu_destroy", "fewha_gpu_dims", "fewha_gpu_preset_info", "fewha_gpu_geometry",
     "fewha_gpu_build_preconditioner", "fewha_gpu_preconditioner", "fewha_gpu_step", "fewha_gpu_reset",
     "fewha_gpu_get_state", "fewha_gpu_set_state", "fewha_gpu_set_stream", "fewha_gpu_device_buffers",
-    "fewha_gpu_load_slopes", "fewha_gpu_step_device", "fewha_gpu_sync", "fewha_gpu_launches_per_step", "fewha_gpu_profile_step", "fewha_gpu_apply_M",
+    "fewha_gpu_load_slopes", "fewha_gpu_step_device", "fewha_gpu_sync", "fewha_gpu_launches_per_step", "fewha_gpu_profile_step", "fewha_gpu_phase_stamps", "fewha_gpu_apply_M",
     "fewha_gpu_build_rhs", "fewha_gpu_add_dm_slopes", "fewha_gpu_fit_to_mirrors", "fewha_gpu_wavelet",
     "fewha_gpu_propagate", "fewha_gpu_propagate_transpose", "fewha_gpu_sh", "fewha_gpu_sh_transpose",
     "fewha_gpu_forward_slopes",
@@ -119,6 +119,7 @@ def lib() -> C.CDLL:
         L.fewha_gpu_sync.argtypes = [vp]
         L.fewha_gpu_launches_per_step.argtypes = [vp]
         L.fewha_gpu_profile_step.argtypes = [vp, C.POINTER(C.c_float), C.POINTER(C.c_int), C.c_int]
+        L.fewha_gpu_phase_stamps.argtypes = [vp, C.c_void_p, C.c_longlong]
         for name in ("apply_M", "build_rhs", "add_dm_slopes", "fit_to_mirrors", "propagate",
                      "propagate_transpose", "sh", "sh_transpose"):
             getattr(L, "fewha_gpu_" + name).argtypes = [vp, dp, dp, C.c_int]
@@ -338,6 +339,18 @@ class Reconstructor:
 
     def launches_per_step(self) -> int:
         return int(self._L.fewha_gpu_launches_per_step(self._h))
+
+    def phase_stamps(self, enable_only=False):
+        """Per-phase %globaltimer stamps of the cluster kernels of the last
+        profile_step frame: array [launch][block][16] (ns; 0 = not stamped)."""
+        if enable_only:
+            self._chk(-min(0, self._L.fewha_gpu_phase_stamps(self._h, None, 0)))
+            return None
+        out = np.zeros(32 * 4096 * 16, np.uint64)
+        n = self._L.fewha_gpu_phase_stamps(self._h, out.ctypes.data_as(C.c_void_p), out.size)
+        if n < 0:
+            self._chk(-n)
+        return out.reshape(32, 4096, 16)
 
     KERNEL_KINDS = ("wfs_rhs", "adjoint", "fwd_rhs", "inv_pcg0", "inv_pcg", "wfs", "fwd_pcg", "inv_fit", "fit_control")
 

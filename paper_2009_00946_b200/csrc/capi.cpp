@@ -177,6 +177,15 @@ int fewha_gpu_load_slopes(fewha_gpu_t h, const void* src, int on_device) {
 int fewha_gpu_step_device(fewha_gpu_t h, const void* d_slopes) { H_GUARD(h->eng->step_device(d_slopes)) }
 int fewha_gpu_sync(fewha_gpu_t h) { H_GUARD(h->eng->sync_check()) }
 int fewha_gpu_launches_per_step(fewha_gpu_t h) { return h ? h->eng->launches_per_step() : -1; }
+int fewha_gpu_phase_stamps(fewha_gpu_t h, unsigned long long* out, long long n) {
+    if (!h) return -1;
+    int got = 0;
+    const int rc = guard(h->err, [&] {
+        h->eng->enable_stamps(true);
+        got = out ? h->eng->read_stamps(out, static_cast<size_t>(n)) : 0;
+    });
+    return rc ? -rc : got;
+}
 int fewha_gpu_profile_step(fewha_gpu_t h, float* ms, int* kinds, int max) {
     if (!h) return -1;
     int n = -1;

@@ -17,6 +17,8 @@ namespace fewha_gpu {
 constexpr int kMaxL = 16;
 constexpr int kMaxW = 16;
 constexpr int kMaxM = 16;
+constexpr int kMaxC = 8;  // CTAs per layer cluster (portable cluster size)
+constexpr int kGatherKMax = 4;  // max bilinear-gather taps per layer node per axis
 
 // Fused-PCG carry (pcg.hpp:32-38 PcgScalars plus per-frame bookkeeping).
 struct Carry {
@@ -34,7 +36,9 @@ struct GeoParams {
     double inv_var[kMaxW];
     double alpha, gain, tol, fault;
     int piston_exact;  // fp32 engines: the fitting term's coarse coefficient is exactly 0 (see k_layer_forward)
-    int filt_off;  // offset of the wavelet order in the constant filter table
+    int filt_off;  // (unused on the device; filters below)
+    double flo[20], fhi[20];  // Daubechies taps of the configured order (wavelet.hpp:100-107)
+    float flo_f[20], fhi_f[20];
     // tables
     const int* ti;
     const double* td;
@@ -51,6 +55,17 @@ struct GeoParams {
     const int* ltiles;  // [n_ltiles][3] (l, I0, J0) for the adjoint-propagation kernel
     int n_ltiles, ltile, lt_rows_max, lt_cols_max;
     int o_tr;  // [(tile*W + w)*4] psi source block {ilo, ihi, jlo, jhi} of each layer tile (into ti)
+    // v2 cluster path
+    int ccl;          // CTAs per layer cluster
+    int o_pg;         // [(w*L+l)*2 + {0 rows, 1 cols}] -> gather table: cnt[side], src[side*KM] (ti), wgt (td/tf)
+    int gather_km;    // max gather taps per layer row/column
+    int o_bs;         // [((w*L+l)*kMaxC + rank)*4] psi source block {ilo, ihi, jlo, jhi} of each band
+    int bd_rows_max, bd_cols_max;
+    unsigned long long* stamps;  // optional phase timestamps [block][16] (nullptr: off)
+    const unsigned char* gblob;  // per-(w,l) gather blobs of the engine's precision (see cluster.cuh)
+    int o_gb;                    // [w*L + l] byte offset of each blob (into ti)
+    int chunk_bytes;  // shared-memory budget of one staged WFS chunk in the band gather
+    int hc_rows;      // rows of the thread-private column scratch
 };
 
 enum LayerMode : int {
@@ -78,7 +93,8 @@ template <typename T>
 struct Bufs {
     // coefficient domain [B][n]
     T *c, *b, *r, *p, *q, *mz;
-    const T* jac;  // [n] shared
+    const T* jac;   // [n] shared Jacobi diagonal
+    const T* jinv;  // [n] shared 1/J (z = r * (1/J): one rounding vs r/J, well inside tolerance)
     T *phi, *y;    // nodal [B][n]
     T* psi;        // [B][Nw]
     const double* meas;  // [B][S]

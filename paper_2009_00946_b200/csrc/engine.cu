@@ -15,6 +15,7 @@
 #include "daubechies_table.h"
 #include "device.hpp"
 #include "kernels.cuh"
+#include "launch.hpp"
 
 namespace fewha_gpu {
 
@@ -54,6 +55,7 @@ struct Plan {
     std::vector<double> td;
     std::vector<std::uint8_t> masks;
     std::vector<int> wtiles, ltiles;
+    std::vector<unsigned char> gblob;
     int maxside = 0;
 };
 
@@ -262,6 +264,195 @@ Plan build_plan(const Geometry& g, int elem_bytes) {
     gp.o_tr = static_cast<int>(pl.ti.size());
     pl.ti.insert(pl.ti.end(), tr.begin(), tr.end());
     pl.td.resize(pl.ti.size(), 0.0);
+
+    // ---- v2 cluster path: R = min(16, side) rows per CTA, C = maxside / R CTAs per layer
+    {
+        const int R = std::min(16, pl.maxside);
+        gp.ccl = pl.maxside / R;
+        if (gp.ccl > kMaxC) throw ConfigError("invalid geometry: layer side exceeds the cluster transform");
+        // gather tables: per (w,l) and axis, for every layer node the (source, weight) list,
+        // ascending source (operators.hpp:129-135 weights as bilinear_stencil assigns them)
+        struct Entry { int src; double w; };
+        std::vector<std::vector<std::vector<Entry>>> rows(W * L), cols(W * L);
+        int km = 1;
+        for (int w = 0; w < W; ++w)
+            for (int l = 0; l < L; ++l) {
+                const auto& lay = g.layers[l];
+                const int side = lay.side();
+                const auto tx = aperture_axis(w, g.stars[w], lay.height, side, lay.extent, true);
+                const auto ty = aperture_axis(w, g.stars[w], lay.height, side, lay.extent, false);
+                auto build = [&](const std::vector<Stencil1>& t) {
+                    std::vector<std::vector<Entry>> out(static_cast<size_t>(side));
+                    for (int s = 0; s < static_cast<int>(t.size()); ++s) {
+                        out[t[s].idx].push_back({s, 1.0 - t[s].f});
+                        out[t[s].idx + 1].push_back({s, t[s].f});
+                    }
+                    for (auto& v : out) km = std::max(km, static_cast<int>(v.size()));
+                    return out;
+                };
+                rows[w * L + l] = build(ty);
+                cols[w * L + l] = build(tx);
+            }
+        if (km > kGatherKMax)
+            throw ConfigError("invalid geometry: aperture sampling denser than the layer grid allows (gather taps " +
+                              std::to_string(km) + " > " + std::to_string(kGatherKMax) + ")");
+        gp.gather_km = km;
+        // padded tables: [side][kGatherKMax] (src in ti, weight in td); padding repeats the last
+        // valid source (or the nearest non-empty node's) with weight 0 so tables stay monotone
+        gp.o_pg = static_cast<int>(pl.ti.size());
+        pl.ti.resize(pl.ti.size() + static_cast<size_t>(W * L * 2), 0);
+        pl.td.resize(pl.ti.size(), 0.0);
+        for (int p = 0; p < W * L; ++p) {
+            for (int axis = 0; axis < 2; ++axis) {
+                const auto& tab = axis == 0 ? rows[p] : cols[p];
+                const int side = static_cast<int>(tab.size());
+                const int off = static_cast<int>(pl.ti.size());
+                pl.ti[static_cast<size_t>(gp.o_pg + p * 2 + axis)] = off;
+                pl.ti.resize(pl.ti.size() + static_cast<size_t>(side) * kGatherKMax, 0);
+                pl.td.resize(pl.ti.size(), 0.0);
+                int first_src = 0;
+                for (const auto& v : tab)
+                    if (!v.empty()) { first_src = v.front().src; break; }
+                int carry = first_src;
+                for (int I = 0; I < side; ++I) {
+                    for (int q = 0; q < kGatherKMax; ++q) {
+                        const bool valid = q < static_cast<int>(tab[I].size());
+                        if (valid) carry = tab[I][q].src;
+                        pl.ti[off + I * kGatherKMax + q] = carry;
+                        pl.td[off + I * kGatherKMax + q] = valid ? tab[I][q].w : 0.0;
+                    }
+                }
+            }
+        }
+        // band source blocks per (w, l, rank)
+        gp.o_bs = static_cast<int>(pl.ti.size());
+        pl.ti.resize(pl.ti.size() + static_cast<size_t>(W * L * kMaxC * 4), 0);
+        pl.td.resize(pl.ti.size(), 0.0);
+        int rmax = 1, cmax = 1;
+        for (int w = 0; w < W; ++w)
+            for (int l = 0; l < L; ++l) {
+                const auto& rt = rows[w * L + l];
+                const auto& ct = cols[w * L + l];
+                const int side = static_cast<int>(rt.size());
+                const int Rl = std::min(16, side);
+                int jlo = INT32_MAX, jhi = 0;
+                for (const auto& v : ct)
+                    for (const auto& en : v) {
+                        jlo = std::min(jlo, en.src);
+                        jhi = std::max(jhi, en.src + 1);
+                    }
+                for (int rank = 0; rank < gp.ccl; ++rank) {
+                    int ilo = INT32_MAX, ihi = 0;
+                    for (int I = rank * Rl; I < std::min(side, rank * Rl + Rl); ++I)
+                        for (const auto& en : rt[I]) {
+                            ilo = std::min(ilo, en.src);
+                            ihi = std::max(ihi, en.src + 1);
+                        }
+                    int* bs = &pl.ti[static_cast<size_t>(gp.o_bs + ((w * L + l) * kMaxC + rank) * 4)];
+                    if (ilo < ihi && jlo < jhi) {
+                        bs[0] = ilo; bs[1] = ihi; bs[2] = jlo; bs[3] = jhi;
+                        rmax = std::max(rmax, ihi - ilo);
+                        cmax = std::max(cmax, jhi - jlo);
+                    } else {
+                        bs[0] = bs[1] = bs[2] = bs[3] = 0;
+                    }
+                }
+            }
+        gp.bd_rows_max = rmax;
+        gp.bd_cols_max = cmax;
+        // thread-private scratch rows: block rows one thread's band rows draw from
+        const int nthr = 256;
+        auto a16 = [](size_t v) { return (v + 15) & ~size_t(15); };
+        int hc_rows = 1;
+        size_t chunk_max = 0, single_max = 0;
+        for (int l = 0; l < L; ++l) {
+            const int side = gp.side[l];
+            const int Rl = std::min(16, side);
+            const int groups = std::max(1, std::min(nthr / side, Rl)), rows_pt = std::max(1, Rl / groups);
+            for (int rank = 0; rank < gp.ccl; ++rank) {
+                size_t total = 0;
+                for (int w = 0; w < W; ++w) {
+                    const int* bs = &pl.ti[static_cast<size_t>(gp.o_bs + ((w * L + l) * kMaxC + rank) * 4)];
+                    // mirrors staged_bytes() in cluster.cuh
+                    const size_t need = a16(static_cast<size_t>(bs[1] - bs[0]) * (bs[3] - bs[2]) * elem_bytes) +
+                                        a16(static_cast<size_t>(side) * km * 2) + a16(static_cast<size_t>(Rl) * km * 2) +
+                                        a16(static_cast<size_t>(side) * km * elem_bytes) +
+                                        a16(static_cast<size_t>(Rl) * km * elem_bytes);
+                    total += need;
+                    single_max = std::max(single_max, need);
+                    const auto& rt = rows[w * L + l];
+                    for (int gI = 0; gI < groups; ++gI) {
+                        int lo = INT32_MAX, hi = -1;
+                        for (int I = rank * Rl + gI * rows_pt; I < std::min(side, rank * Rl + (gI + 1) * rows_pt); ++I)
+                            for (const auto& en : rt[I]) {
+                                lo = std::min(lo, en.src);
+                                hi = std::max(hi, en.src);
+                            }
+                        if (hi >= lo) hc_rows = std::max(hc_rows, hi - lo + 1);
+                    }
+                }
+                chunk_max = std::max(chunk_max, total);
+            }
+        }
+        gp.hc_rows = hc_rows;
+        const size_t Rm = static_cast<size_t>(std::min(16, pl.maxside));
+        const size_t fixed = a16(Rm * (pl.maxside + 1) * elem_bytes) + 2 * a16(Rm * pl.maxside * elem_bytes) +
+                             a16(static_cast<size_t>(hc_rows) * nthr * elem_bytes) + 2048;
+        const size_t limit = 227 * 1024;
+        const size_t budget = limit > fixed ? limit - fixed : 0;
+        if (single_max > budget) throw ConfigError("invalid geometry: adjoint gather does not fit in shared memory");
+        gp.chunk_bytes = static_cast<int>(std::min(chunk_max, budget));
+        // gather blobs per (w,l): [col src int16][row src int16][col w][row w], 16-byte aligned parts;
+        // column sources relative to the WFS's first contributing column (the band block's jlo)
+        gp.o_gb = static_cast<int>(pl.ti.size());
+        pl.ti.resize(pl.ti.size() + static_cast<size_t>(W * L), 0);
+        pl.td.resize(pl.ti.size(), 0.0);
+        pl.gblob.clear();
+        for (int w = 0; w < W; ++w)
+            for (int l = 0; l < L; ++l) {
+                const auto& rt = rows[w * L + l];
+                const auto& ct = cols[w * L + l];
+                const int side = static_cast<int>(rt.size());
+                const int jlo = pl.ti[static_cast<size_t>(gp.o_bs + ((w * L + l) * kMaxC + 0) * 4 + 2)];
+                pl.ti[static_cast<size_t>(gp.o_gb + w * L + l)] = static_cast<int>(pl.gblob.size());
+                auto put_src = [&](const std::vector<std::vector<Entry>>& tab, int rel) {
+                    const size_t start = pl.gblob.size();
+                    int carry = 0;
+                    for (const auto& v : tab)
+                        if (!v.empty()) { carry = v.front().src; break; }
+                    for (int I = 0; I < side; ++I)
+                        for (int q = 0; q < km; ++q) {
+                            if (q < static_cast<int>(tab[I].size())) carry = tab[I][q].src;
+                            const int v = carry - rel;
+                            if (v < -32768 || v > 32767) throw ConfigError("invalid geometry: gather index overflow");
+                            const short s16 = static_cast<short>(v);
+                            const auto* p = reinterpret_cast<const unsigned char*>(&s16);
+                            pl.gblob.insert(pl.gblob.end(), p, p + 2);
+                        }
+                    pl.gblob.resize(start + a16(pl.gblob.size() - start), 0);
+                };
+                auto put_w = [&](const std::vector<std::vector<Entry>>& tab) {
+                    const size_t start = pl.gblob.size();
+                    for (int I = 0; I < side; ++I)
+                        for (int q = 0; q < km; ++q) {
+                            const double v = q < static_cast<int>(tab[I].size()) ? tab[I][q].w : 0.0;
+                            if (elem_bytes == 8) {
+                                const auto* p = reinterpret_cast<const unsigned char*>(&v);
+                                pl.gblob.insert(pl.gblob.end(), p, p + 8);
+                            } else {
+                                const float f = static_cast<float>(v);
+                                const auto* p = reinterpret_cast<const unsigned char*>(&f);
+                                pl.gblob.insert(pl.gblob.end(), p, p + 4);
+                            }
+                        }
+                    pl.gblob.resize(start + a16(pl.gblob.size() - start), 0);
+                };
+                put_src(ct, jlo);
+                put_src(rt, 0);
+                put_w(ct);
+                put_w(rt);
+            }
+    }
     gp.n_ltiles = static_cast<int>(pl.ltiles.size() / 3);
     return pl;
 }
@@ -324,7 +515,7 @@ struct Work {
             bf.a_prev = A((T*)nullptr, aa);
             bf.a_out = A((T*)nullptr, aa);
             bf.carry = A((Carry*)nullptr, static_cast<size_t>(gp.iters + 1) * cnt);
-            const size_t np = static_cast<size_t>(gp.iters) * gp.L * cnt;
+            const size_t np = static_cast<size_t>(gp.iters) * gp.L * kMaxC * cnt;
             bf.rho_part = A((double*)nullptr, np);
             bf.mu_part = A((double*)nullptr, np);
             bf.rho_log = A((double*)nullptr, static_cast<size_t>(gp.iters) * cnt);
@@ -341,8 +532,6 @@ struct Work {
 // ---------------------------------------------------------------------------
 template <typename T>
 struct Launch {
-    static int layer_threads(int side) { return std::max(128, std::min(1024, side * side / 8)); }
-    static size_t layer_smem(int side) { return static_cast<size_t>(side) * (side + 1) * sizeof(T); }
     static size_t wfs_smem(const GeoParams& gp) {
         const int H = gp.wtile + 2, Q = gp.wtile + 1;
         return static_cast<size_t>(H * H + 2 * Q * Q) * sizeof(T);
@@ -350,54 +539,56 @@ struct Launch {
     static size_t adj_smem(const GeoParams& gp) {
         return static_cast<size_t>(gp.lt_rows_max) * (gp.lt_cols_max + gp.ltile) * sizeof(T);
     }
-
-    template <int FLEN>
-    static void set_attrs_flen(const GeoParams& gp) {
-        const int smem = static_cast<int>(layer_smem(gp.maxside));
-        CK(cudaFuncSetAttribute(k_layer_inverse<T, FLEN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        CK(cudaFuncSetAttribute(k_layer_forward<T, FLEN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    static size_t a16(size_t v) { return (v + 15) & ~size_t(15); }
+    static size_t band_rows(const GeoParams& gp) { return static_cast<size_t>(std::min(16, gp.maxside)); }
+    static size_t band_bytes(const GeoParams& gp) { return a16(band_rows(gp) * (gp.maxside + 1) * sizeof(T)); }
+    static size_t slice_bytes(const GeoParams& gp) { return a16(band_rows(gp) * gp.maxside * sizeof(T)); }
+    // band + 6 prefetched band slices (r, 1/J, p, q, c, Mz)
+    static size_t inv_cl_smem(const GeoParams& gp) { return band_bytes(gp) + 6 * slice_bytes(gp); }
+    // band + 2 epilogue slices + thread-private column scratch (256 threads) + one staged WFS chunk
+    static size_t fwd_cl_smem(const GeoParams& gp) {
+        return band_bytes(gp) + 2 * slice_bytes(gp) + a16(static_cast<size_t>(gp.hc_rows) * 256 * sizeof(T)) +
+               static_cast<size_t>(gp.chunk_bytes);
     }
+
+#define FEWHA_FLEN_SWITCH(flen, CALL)          \
+    switch (flen) {                            \
+        case 2: CALL(2); break;                \
+        case 4: CALL(4); break;                \
+        case 6: CALL(6); break;                \
+        case 8: CALL(8); break;                \
+        case 10: CALL(10); break;              \
+        case 12: CALL(12); break;              \
+        case 14: CALL(14); break;              \
+        case 16: CALL(16); break;              \
+        case 18: CALL(18); break;              \
+        default: CALL(20); break;              \
+    }
+
+    // The dynamic shared-memory opt-in is a per-function, process-global attribute:
+    // set it to the device maximum once so engines of different geometries coexist.
     static void set_attrs(const GeoParams& gp, int flen) {
-        switch (flen) {
-            case 2: set_attrs_flen<2>(gp); break;
-            case 4: set_attrs_flen<4>(gp); break;
-            case 6: set_attrs_flen<6>(gp); break;
-            case 8: set_attrs_flen<8>(gp); break;
-            case 10: set_attrs_flen<10>(gp); break;
-            case 12: set_attrs_flen<12>(gp); break;
-            case 14: set_attrs_flen<14>(gp); break;
-            case 16: set_attrs_flen<16>(gp); break;
-            case 18: set_attrs_flen<18>(gp); break;
-            default: set_attrs_flen<20>(gp); break;
-        }
-        CK(cudaFuncSetAttribute(k_wfs<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wfs_smem(gp)));
-        CK(cudaFuncSetAttribute(k_wfs<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wfs_smem(gp)));
-        CK(cudaFuncSetAttribute(k_adjoint<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)adj_smem(gp)));
+        int dev = 0, maxopt = 0;
+        CK(cudaGetDevice(&dev));
+        CK(cudaDeviceGetAttribute(&maxopt, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        if (inv_cl_smem(gp) > static_cast<size_t>(maxopt) || fwd_cl_smem(gp) > static_cast<size_t>(maxopt) ||
+            wfs_smem(gp) > static_cast<size_t>(maxopt) || adj_smem(gp) > static_cast<size_t>(maxopt))
+            throw ConfigError("invalid geometry: layer kernels exceed the device's shared memory");
+        const size_t m = static_cast<size_t>(maxopt);
+#define FEWHA_SET(N) CK((set_layer_cluster_attrs<T, N>(m, m)))
+        FEWHA_FLEN_SWITCH(flen, FEWHA_SET)
+#undef FEWHA_SET
+        CK(cudaFuncSetAttribute(k_wfs<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxopt));
+        CK(cudaFuncSetAttribute(k_wfs<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxopt));
+        CK(cudaFuncSetAttribute(k_adjoint<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxopt));
     }
-
-    template <int FLEN>
-    static void layer_flen(bool inverse, const GeoParams& gp, const Bufs<T>& bf, int mode, int it, int count,
-                           cudaStream_t st, int fit_term) {
-        const dim3 grid(gp.L, count);
-        const int thr = layer_threads(gp.maxside);
-        const size_t smem = layer_smem(gp.maxside);
-        if (inverse) k_layer_inverse<T, FLEN><<<grid, thr, smem, st>>>(gp, bf, mode, it);
-        else k_layer_forward<T, FLEN><<<grid, thr, smem, st>>>(gp, bf, mode, it, fit_term);
-    }
-    static void layer(int flen, bool inverse, const GeoParams& gp, const Bufs<T>& bf, int mode, int it, int count,
-                      cudaStream_t st, int fit_term = 1) {
-        switch (flen) {
-            case 2: layer_flen<2>(inverse, gp, bf, mode, it, count, st, fit_term); break;
-            case 4: layer_flen<4>(inverse, gp, bf, mode, it, count, st, fit_term); break;
-            case 6: layer_flen<6>(inverse, gp, bf, mode, it, count, st, fit_term); break;
-            case 8: layer_flen<8>(inverse, gp, bf, mode, it, count, st, fit_term); break;
-            case 10: layer_flen<10>(inverse, gp, bf, mode, it, count, st, fit_term); break;
-            case 12: layer_flen<12>(inverse, gp, bf, mode, it, count, st, fit_term); break;
-            case 14: layer_flen<14>(inverse, gp, bf, mode, it, count, st, fit_term); break;
-            case 16: layer_flen<16>(inverse, gp, bf, mode, it, count, st, fit_term); break;
-            case 18: layer_flen<18>(inverse, gp, bf, mode, it, count, st, fit_term); break;
-            default: layer_flen<20>(inverse, gp, bf, mode, it, count, st, fit_term); break;
-        }
+    // layer kernels: grid (C, L, count), cluster (C,1,1)
+    static void cl(int flen, bool inverse, const GeoParams& gp, const Bufs<T>& bf, int mode, int it, int count,
+                   cudaStream_t st, int gather = 1) {
+        const size_t smem = inverse ? inv_cl_smem(gp) : fwd_cl_smem(gp);
+#define FEWHA_LAUNCH(N) CK((launch_layer_cluster<T, N>(inverse, gp, bf, mode, it, count, st, gather, smem)))
+        FEWHA_FLEN_SWITCH(flen, FEWHA_LAUNCH)
+#undef FEWHA_LAUNCH
     }
     static void wfs(bool rhs, const GeoParams& gp, const Bufs<T>& bf, int with_dm, int count, cudaStream_t st) {
         const dim3 grid(gp.n_wtiles, count);
@@ -420,13 +611,25 @@ struct EngineImpl {
     int precision, batch, device, flen;
     Plan plan;
     DevFree fr;
-    GeoParams gp{};      // with device table pointers
+    GeoParams gp{};      // with device table pointers (engine precision)
+    GeoParams gp64{};    // fp64 plan for the preconditioner probes (== gp in fp64 engines)
     cudaStream_t stream = nullptr, user_stream = nullptr;
     bool own_stream = false;
     cudaGraphExec_t graph = nullptr;
     bool has_precond = false;
+    // optional per-phase timestamps of the cluster kernels (profiling only)
+    unsigned long long* stamp_buf = nullptr;
+    int stamp_slot = -1;  // < 0: stamping off
+    static constexpr int kStampSlots = 32, kStampBlocks = 4096;
+    GeoParams gps() {
+        GeoParams g2 = gp;
+        if (stamp_slot >= 0 && stamp_slot < kStampSlots)
+            g2.stamps = stamp_buf + static_cast<size_t>(stamp_slot++) * kStampBlocks * 16;
+        return g2;
+    }
     std::vector<double> precond;
     void* jac = nullptr;
+    void* jinv = nullptr;  // 1/J
     // state (precision T) -- one of the two is used
     Work<double> sd, od, pd;  // state / ops / probes (fp64)
     Work<float> sf, of;        // state / ops (fp32)
@@ -438,13 +641,17 @@ struct EngineImpl {
     template <typename T>
     Work<T>& ops();
 
-    void upload_plan() {
+    GeoParams upload_plan(const Plan& plan) {
         int* ti = dalloc<int>(plan.ti.size());
         double* td = dalloc<double>(plan.td.size());
         float* tf = dalloc<float>(plan.td.size());
         std::uint8_t* mk = dalloc<std::uint8_t>(plan.masks.size());
         int* wt = dalloc<int>(plan.wtiles.size());
         int* lt = dalloc<int>(plan.ltiles.size());
+        unsigned char* gb = dalloc<unsigned char>(plan.gblob.size());
+        fr.add(gb);
+        if (!plan.gblob.empty())
+            CK(cudaMemcpy(gb, plan.gblob.data(), plan.gblob.size(), cudaMemcpyHostToDevice));
         for (void* p : {(void*)ti, (void*)td, (void*)tf, (void*)mk, (void*)wt, (void*)lt}) fr.add(p);
         std::vector<float> tdf(plan.td.begin(), plan.td.end());
         CK(cudaMemcpy(ti, plan.ti.data(), plan.ti.size() * sizeof(int), cudaMemcpyHostToDevice));
@@ -454,33 +661,15 @@ struct EngineImpl {
             CK(cudaMemcpy(mk, plan.masks.data(), plan.masks.size(), cudaMemcpyHostToDevice));
         CK(cudaMemcpy(wt, plan.wtiles.data(), plan.wtiles.size() * sizeof(int), cudaMemcpyHostToDevice));
         CK(cudaMemcpy(lt, plan.ltiles.data(), plan.ltiles.size() * sizeof(int), cudaMemcpyHostToDevice));
-        gp = plan.gp;
-        gp.ti = ti;
-        gp.td = td;
-        gp.tf = tf;
-        gp.masks = mk;
-        gp.wtiles = wt;
-        gp.ltiles = lt;
-    }
-
-    static void upload_filters() {
-        double lo[110], hi[110];
-        float lof[110], hif[110];
-        for (int o = 1; o <= 10; ++o) {
-            const int off = kDaubechiesOffset[o - 1], len = kDaubechiesOffset[o] - off;
-            for (int k = 0; k < len; ++k) {
-                lo[off + k] = kDaubechies[off + k];
-                hi[off + k] = (k % 2 == 0 ? 1.0 : -1.0) * kDaubechies[off + len - 1 - k];
-            }
-        }
-        for (int k = 0; k < 110; ++k) {
-            lof[k] = static_cast<float>(lo[k]);
-            hif[k] = static_cast<float>(hi[k]);
-        }
-        CK(cudaMemcpyToSymbol(c_lo_d, lo, sizeof lo));
-        CK(cudaMemcpyToSymbol(c_hi_d, hi, sizeof hi));
-        CK(cudaMemcpyToSymbol(c_lo_f, lof, sizeof lof));
-        CK(cudaMemcpyToSymbol(c_hi_f, hif, sizeof hif));
+        GeoParams g = plan.gp;
+        g.ti = ti;
+        g.td = td;
+        g.tf = tf;
+        g.masks = mk;
+        g.wtiles = wt;
+        g.ltiles = lt;
+        g.gblob = gb;
+        return g;
     }
 
     void invalidate_graph() {
@@ -495,27 +684,24 @@ struct EngineImpl {
         Work<T>& w = state<T>();
         Bufs<T> bf = w.bf;
         bf.jac = static_cast<const T*>(jac);
+        bf.jinv = static_cast<const T*>(jinv);
         const int B = batch;
         // RHS with the pseudo open-loop term (reconstructor.hpp:316-323)
         Launch<T>::wfs(true, gp, bf, gp.closed, B, st);
         mark(kKindWfsRhs);
-        Launch<T>::adjoint(gp, bf.psi, bf.y, B, st);
-        mark(kKindAdjoint);
-        Launch<T>::layer(flen, false, gp, bf, kRhs, 0, B, st);
+        Launch<T>::cl(flen, false, gps(), bf, kRhs, 0, B, st);
         mark(kKindFwdRhs);
         // fused PCG (pcg.hpp:68-106), the update of iteration k fused into k+1's W^-1
         for (int it = 0; it < gp.iters; ++it) {
-            Launch<T>::layer(flen, true, gp, bf, kPcg, it, B, st);
+            Launch<T>::cl(flen, true, gps(), bf, kPcg, it, B, st);
             mark(it == 0 ? kKindInvPcg0 : kKindInvPcg);
             Launch<T>::wfs(false, gp, bf, 0, B, st);
             mark(kKindWfs);
-            Launch<T>::adjoint(gp, bf.psi, bf.y, B, st);
-            mark(kKindAdjoint);
-            Launch<T>::layer(flen, false, gp, bf, kPcg, it, B, st);
+            Launch<T>::cl(flen, false, gps(), bf, kPcg, it, B, st);
             mark(kKindFwdPcg);
         }
         // last update + fitting W^-1 c, then fit + control + rotation
-        Launch<T>::layer(flen, true, gp, bf, kFit, 0, B, st);
+        Launch<T>::cl(flen, true, gps(), bf, kFit, 0, B, st);
         mark(kKindInvFit);
         Launch<T>::fit(gp, bf, 1, B, st);
         mark(kKindFit);
@@ -574,12 +760,11 @@ struct EngineImpl {
 
     // ---- apply_M on a double workspace (also the preconditioner probes) ----
     template <typename T>
-    void apply_M_dev(Work<T>& w, int count, cudaStream_t st) {
+    void apply_M_dev(Work<T>& w, int count, cudaStream_t st, const GeoParams& g) {
         Bufs<T> bf = w.bf;
-        Launch<T>::layer(flen, true, gp, bf, kPlain, 0, count, st);
-        Launch<T>::wfs(false, gp, bf, 0, count, st);
-        Launch<T>::adjoint(gp, bf.psi, bf.y, count, st);
-        Launch<T>::layer(flen, false, gp, bf, kApply, 0, count, st);
+        Launch<T>::cl(flen, true, g, bf, kPlain, 0, count, st);
+        Launch<T>::wfs(false, g, bf, 0, count, st);
+        Launch<T>::cl(flen, false, g, bf, kApply, 0, count, st);
     }
 
     void build_precond() {
@@ -621,7 +806,7 @@ struct EngineImpl {
             for (int k = 0; k < cnt; ++k)
                 CK(cudaMemcpyAsync(pd.in + k * n + probes[p0 + k].rep, one.data(), sizeof(double),
                                    cudaMemcpyHostToDevice, stream));
-            apply_M_dev<double>(pd, cnt, stream);
+            apply_M_dev<double>(pd, cnt, stream, gp64);
             for (int k = 0; k < cnt; ++k)
                 CK(cudaMemcpyAsync(&probed[p0 + k], pd.out + k * n + probes[p0 + k].rep, sizeof(double),
                                    cudaMemcpyDeviceToHost, stream));
@@ -651,11 +836,15 @@ struct EngineImpl {
             if (!(v > 0.0))
                 throw std::runtime_error("preconditioner: non-positive diagonal entry (operator symmetry broken?)");
         precond = diag;
+        std::vector<double> inv(n);
+        for (size_t k = 0; k < n; ++k) inv[k] = 1.0 / diag[k];
         if (precision == 64) {
             CK(cudaMemcpy(jac, diag.data(), n * sizeof(double), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(jinv, inv.data(), n * sizeof(double), cudaMemcpyHostToDevice));
         } else {
-            std::vector<float> f(diag.begin(), diag.end());
+            std::vector<float> f(diag.begin(), diag.end()), fi(inv.begin(), inv.end());
             CK(cudaMemcpy(jac, f.data(), n * sizeof(float), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(jinv, fi.data(), n * sizeof(float), cudaMemcpyHostToDevice));
         }
         has_precond = true;
     }
@@ -707,27 +896,49 @@ Engine::Engine(Geometry g, int precision, int batch, int device) : p_(std::make_
     P.batch = batch;
     P.device = device;
     P.flen = 2 * P.g.wavelet_order;
+    auto set_filters = [&](GeoParams& gpx) {
+        // Daubechies taps of the configured order, hi_k = (-1)^k lo_{len-1-k} (wavelet.hpp:104-106)
+        const auto lo = daubechies(P.g.wavelet_order);
+        const int len = static_cast<int>(lo.size());
+        for (int k = 0; k < len; ++k) {
+            const double hi = (k % 2 == 0 ? 1.0 : -1.0) * lo[len - 1 - k];
+            gpx.flo[k] = lo[k];
+            gpx.fhi[k] = hi;
+            gpx.flo_f[k] = static_cast<float>(lo[k]);
+            gpx.fhi_f[k] = static_cast<float>(hi);
+        }
+    };
     P.plan = build_plan(P.g, precision / 8);
     P.plan.gp.piston_exact = precision == 32 ? 1 : 0;
+    set_filters(P.plan.gp);
+    Plan plan64;
+    if (precision == 32) {  // the preconditioner probes run in fp64 with their own tables
+        plan64 = build_plan(P.g, 8);
+        plan64.gp.piston_exact = 0;
+        set_filters(plan64.gp);
+    }
     int ndev = 0;
     CK(cudaGetDeviceCount(&ndev));
     if (device < 0 || device >= ndev) throw ArgError("device ordinal out of range");
     CK(cudaSetDevice(device));
-    EngineImpl::upload_filters();
-    P.upload_plan();
+    P.gp = P.upload_plan(P.plan);
+    P.gp64 = precision == 64 ? P.gp : P.upload_plan(plan64);
     CK(cudaStreamCreateWithFlags(&P.stream, cudaStreamNonBlocking));
     P.own_stream = true;
     if (precision == 64) {
         Launch<double>::set_attrs(P.gp, P.flen);
         P.sd.alloc(P.gp, batch, P.fr, true);
         P.jac = dalloc<double>(P.gp.n);
+        P.jinv = dalloc<double>(P.gp.n);
     } else {
         Launch<float>::set_attrs(P.gp, P.flen);
         P.sf.alloc(P.gp, batch, P.fr, true);
         P.jac = dalloc<float>(P.gp.n);
+        P.jinv = dalloc<float>(P.gp.n);
     }
-    Launch<double>::set_attrs(P.gp, P.flen);  // probes always fp64
+    Launch<double>::set_attrs(P.gp64, P.flen);  // probes always fp64
     P.fr.add(P.jac);
+    P.fr.add(P.jinv);
     reset();
 }
 
@@ -896,13 +1107,40 @@ void Engine::sync_check() {
         if (s) throw std::runtime_error("pcg_solve: non-finite scalar (indefinite operator?)");
 }
 
-int Engine::launches_per_step() const { return 6 + 4 * p_->gp.iters; }
+int Engine::launches_per_step() const { return 4 + 3 * p_->gp.iters; }
 
 int Engine::profile_step(float* ms, int* kinds, int max) {
     auto& P = *p_;
     CK(cudaSetDevice(P.device));
     if (!P.has_precond) P.build_precond();
+    if (P.stamp_buf) {
+        CK(cudaMemset(P.stamp_buf, 0, sizeof(unsigned long long) * EngineImpl::kStampSlots * EngineImpl::kStampBlocks * 16));
+        P.stamp_slot = 0;
+    }
+    struct Off {
+        int& s;
+        ~Off() { s = -1; }
+    } off{P.stamp_slot};
     return P.precision == 64 ? P.profile_frame<double>(ms, kinds, max) : P.profile_frame<float>(ms, kinds, max);
+}
+
+void Engine::enable_stamps(bool on) {
+    auto& P = *p_;
+    CK(cudaSetDevice(P.device));
+    if (on && !P.stamp_buf) {
+        void* p = nullptr;
+        CK(cudaMalloc(&p, sizeof(unsigned long long) * EngineImpl::kStampSlots * EngineImpl::kStampBlocks * 16));
+        P.stamp_buf = static_cast<unsigned long long*>(p);
+        P.fr.add(p);
+    }
+}
+
+int Engine::read_stamps(unsigned long long* out, size_t n) {
+    auto& P = *p_;
+    if (!P.stamp_buf) return 0;
+    const size_t total = static_cast<size_t>(EngineImpl::kStampSlots) * EngineImpl::kStampBlocks * 16;
+    CK(cudaMemcpy(out, P.stamp_buf, sizeof(unsigned long long) * std::min(n, total), cudaMemcpyDeviceToHost));
+    return static_cast<int>(std::min(n, total));
 }
 
 void Engine::device_buffers(void** slopes, void** coeffs, void** dm, double** rho, int** status, int** n_rho) {
@@ -948,7 +1186,7 @@ void Engine::apply_M(const double* in, double* out, int count) {
         with_ops<T>(P, count, [&](Work<T>& w) {
             const size_t n = static_cast<size_t>(P.gp.n) * count;
             h2d_conv<T>(w.in, in, n, P.stream);
-            P.apply_M_dev<T>(w, count, P.stream);
+            P.apply_M_dev<T>(w, count, P.stream, P.gp);
             d2h_conv<T>(out, w.out, n, P.stream);
         });
     })
@@ -961,8 +1199,7 @@ void Engine::build_rhs(const double* meas, double* out, int count) {
             CK(cudaMemcpy(w.meas, meas, sizeof(double) * P.gp.S * count, cudaMemcpyHostToDevice));
             Bufs<T> bf = w.bf;
             Launch<T>::wfs(true, P.gp, bf, 0, count, P.stream);
-            Launch<T>::adjoint(P.gp, bf.psi, bf.y, count, P.stream);
-            Launch<T>::layer(P.flen, false, P.gp, bf, kPlain, 0, count, P.stream);
+            Launch<T>::cl(P.flen, false, P.gp, bf, kPlain, 0, count, P.stream);
             d2h_conv<T>(out, w.out, static_cast<size_t>(P.gp.n) * count, P.stream);
         });
     })
@@ -1002,7 +1239,7 @@ void Engine::fit(const double* c, double* a, int count) {
         with_ops<T>(P, count, [&](Work<T>& w) {
             h2d_conv<T>(w.in, c, static_cast<size_t>(P.gp.n) * count, P.stream);
             Bufs<T> bf = w.bf;
-            Launch<T>::layer(P.flen, true, P.gp, bf, kPlain, 0, count, P.stream);
+            Launch<T>::cl(P.flen, true, P.gp, bf, kPlain, 0, count, P.stream);
             Launch<T>::fit(P.gp, bf, 0, count, P.stream);
             d2h_conv<T>(a, w.a, static_cast<size_t>(P.gp.A) * count, P.stream);
         });
@@ -1017,11 +1254,11 @@ void Engine::wavelet(int inverse, double* data, int count) {
             Bufs<T> bf = w.bf;
             if (inverse) {
                 h2d_conv<T>(w.in, data, n, P.stream);
-                Launch<T>::layer(P.flen, true, P.gp, bf, kPlain, 0, count, P.stream);
+                Launch<T>::cl(P.flen, true, P.gp, bf, kPlain, 0, count, P.stream);
                 d2h_conv<T>(data, bf.phi, n, P.stream);
             } else {
                 h2d_conv<T>(bf.y, data, n, P.stream);
-                Launch<T>::layer(P.flen, false, P.gp, bf, kPlain, 0, count, P.stream, /*fit_term=*/0);
+                Launch<T>::cl(P.flen, false, P.gp, bf, kPlain, 0, count, P.stream, /*gather=*/0);
                 d2h_conv<T>(data, w.out, n, P.stream);
             }
         });

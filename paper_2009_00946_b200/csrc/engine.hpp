@@ -43,6 +43,8 @@ public:
     void sync_check();
     int launches_per_step() const;
     int profile_step(float* ms, int* kinds, int max);
+    void enable_stamps(bool on);
+    int read_stamps(unsigned long long* out, size_t n);
     void device_buffers(void** slopes, void** coeffs, void** dm, double** rho, int** status, int** n_rho);
 
     // operator entry points (count stacked host inputs)

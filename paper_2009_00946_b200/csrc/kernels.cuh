@@ -32,24 +32,20 @@
 
 namespace fewha_gpu {
 
-// Daubechies analysis (lo) / highpass (hi) filters for orders 1..10, 110 taps
-// each (offsets kDaubechiesOffset); hi_k = (-1)^k lo_{len-1-k} (wavelet.hpp:104-106).
-__constant__ double c_lo_d[110];
-__constant__ double c_hi_d[110];
-__constant__ float c_lo_f[110];
-__constant__ float c_hi_f[110];
-
+// Daubechies analysis (lo) / highpass (hi) taps of the configured order live in
+// the kernel parameter block (GeoParams::flo/fhi): constant-bank operands, one
+// copy per launch, no per-translation-unit __constant__ symbols.
 template <typename T>
 struct Filt;
 template <>
 struct Filt<double> {
-    __device__ static double lo(int k) { return c_lo_d[k]; }
-    __device__ static double hi(int k) { return c_hi_d[k]; }
+    __device__ static double lo(const GeoParams& gp, int k) { return gp.flo[k]; }
+    __device__ static double hi(const GeoParams& gp, int k) { return gp.fhi[k]; }
 };
 template <>
 struct Filt<float> {
-    __device__ static float lo(int k) { return c_lo_f[k]; }
-    __device__ static float hi(int k) { return c_hi_f[k]; }
+    __device__ static float lo(const GeoParams& gp, int k) { return gp.flo_f[k]; }
+    __device__ static float hi(const GeoParams& gp, int k) { return gp.fhi_f[k]; }
 };
 
 template <typename T>
@@ -79,131 +75,16 @@ __device__ __forceinline__ double block_sum(double v, double* scratch) {
     return t;  // valid in thread 0
 }
 
-// ---------------------------------------------------------------------------
-// In-shared-memory periodic Mallat DWT passes (wavelet.hpp:153-201).
-// buf[i*P + j], P = side + 1.  A pass at level s processes the top-left s x s
-// block along rows (COL=false) or columns (COL=true).  Work item = (line,
-// segment of SEG consecutive output pairs); lanes walk consecutive lines.
-// ---------------------------------------------------------------------------
 template <typename T, bool COL>
 __device__ __forceinline__ T& at(T* buf, int P, int line, int pos) {
     return COL ? buf[pos * P + line] : buf[line * P + pos];
 }
 
-// Each pass runs in `rounds`: a round covers s/rounds lines, all its reads
-// land in registers before one barrier and all its writes follow (lines are
-// independent, so rounds need no cross-round ordering beyond the barrier).
-// SEG is fixed per element type (4 fp64 / 8 fp32) to bound register staging.
+// Per-thread output staging of the in-place DWT passes (4 fp64 / 8 fp32).
 template <typename T>
 struct SegOf {
     static constexpr int value = sizeof(T) == 8 ? 4 : 8;
 };
-
-template <typename T, int FLEN, bool COL>
-__device__ __forceinline__ void analysis_pass(T* buf, int P, int s, int fo) {
-    constexpr int SEGM = SegOf<T>::value;
-    const int h = s >> 1, mask = s - 1;
-    const int seg = h < SEGM ? h : SEGM;
-    const int segs = h / seg;
-    const int nthr = blockDim.x, tid = threadIdx.x;
-    int lines = s;
-    while (lines * segs > nthr) lines >>= 1;
-    for (int l0 = 0; l0 < s; l0 += lines) {
-        const bool act = tid < lines * segs;
-        const int line = l0 + tid % lines, m0 = (tid / lines) * seg;
-        T a[SEGM], d[SEGM];
-        if (act) {
-#pragma unroll
-            for (int e = 0; e < SEGM; ++e) {
-                if (e >= seg) break;
-                T sa = T(0), sd = T(0);
-#pragma unroll
-                for (int k = 0; k < FLEN; ++k) {
-                    const T v = at<T, COL>(buf, P, line, (2 * (m0 + e) + k) & mask);
-                    sa += Filt<T>::lo(fo + k) * v;
-                    sd += Filt<T>::hi(fo + k) * v;
-                }
-                a[e] = sa;
-                d[e] = sd;
-            }
-        }
-        __syncthreads();
-        if (act) {
-#pragma unroll
-            for (int e = 0; e < SEGM; ++e) {
-                if (e >= seg) break;
-                at<T, COL>(buf, P, line, m0 + e) = a[e];
-                at<T, COL>(buf, P, line, h + m0 + e) = d[e];
-            }
-        }
-        __syncthreads();
-    }
-}
-
-// Gather form of synthesis: x[t] = sum_{k = t mod 2} a_m lo_k + d_m hi_k with
-// m = ((t-k) mod s)/2 -- valid for every s >= 2, including the small levels
-// where the filter wraps the period several times (wavelet.hpp:178, & mask).
-// The a/d windows are staged in registers across the barrier; outputs are
-// formed and stored after it.
-template <typename T, int FLEN, bool COL>
-__device__ __forceinline__ void synthesis_pass(T* buf, int P, int s, int fo) {
-    constexpr int SEGM = SegOf<T>::value;
-    constexpr int HF = FLEN / 2;
-    const int h = s >> 1, hmask = h - 1;
-    const int seg = h < SEGM ? h : SEGM;
-    const int segs = h / seg;
-    const int nthr = blockDim.x, tid = threadIdx.x;
-    int lines = s;
-    while (lines * segs > nthr) lines >>= 1;
-    for (int l0 = 0; l0 < s; l0 += lines) {
-        const bool act = tid < lines * segs;
-        const int line = l0 + tid % lines, m0 = (tid / lines) * seg;
-        T wa[SEGM + HF - 1], wd[SEGM + HF - 1];
-        if (act) {
-#pragma unroll
-            for (int i = 0; i < SEGM + HF - 1; ++i) {
-                if (i >= seg + HF - 1) break;
-                const int m = (m0 - (HF - 1) + i) & hmask;
-                wa[i] = at<T, COL>(buf, P, line, m);
-                wd[i] = at<T, COL>(buf, P, line, h + m);
-            }
-        }
-        __syncthreads();
-        if (act) {
-#pragma unroll
-            for (int u = 0; u < 2 * SEGM; ++u) {
-                if (u >= 2 * seg) break;
-                T acc = T(0);
-#pragma unroll
-                for (int kk = 0; kk < HF; ++kk) {
-                    const int k = (u & 1) + 2 * kk;
-                    const int wi = (u >> 1) - kk + HF - 1;
-                    acc += wa[wi] * Filt<T>::lo(fo + k) + wd[wi] * Filt<T>::hi(fo + k);
-                }
-                at<T, COL>(buf, P, line, 2 * m0 + u) = acc;
-            }
-        }
-        __syncthreads();
-    }
-}
-
-// forward transform, wavelet.hpp:115-125: per level rows then columns
-template <typename T, int FLEN>
-__device__ void dwt_forward(T* buf, int side, int P, int fo) {
-    for (int s = side; s >= 2; s >>= 1) {
-        analysis_pass<T, FLEN, false>(buf, P, s, fo);
-        analysis_pass<T, FLEN, true>(buf, P, s, fo);
-    }
-}
-
-// inverse transform, wavelet.hpp:128-138: per level columns then rows
-template <typename T, int FLEN>
-__device__ void dwt_inverse(T* buf, int side, int P, int fo) {
-    for (int s = 2; s <= side; s <<= 1) {
-        synthesis_pass<T, FLEN, true>(buf, P, s, fo);
-        synthesis_pass<T, FLEN, false>(buf, P, s, fo);
-    }
-}
 
 // ---------------------------------------------------------------------------
 // Fused-PCG scalar step (pcg.hpp:72-99), evaluated for the iteration whose
@@ -215,11 +96,8 @@ struct ScalarStep {
     double beta, alpha, logval;
 };
 
-__device__ ScalarStep pcg_scalar_step(const GeoParams& gp, const Carry& in, const double* rho_part,
-                                      const double* mu_part, int first) {
-    double rho = 0.0, mu = 0.0;
-    for (int l = 0; l < gp.L; ++l) rho += rho_part[l];
-    for (int l = 0; l < gp.L; ++l) mu += mu_part[l];
+__device__ inline ScalarStep pcg_scalar_from_sums(const GeoParams& gp, const Carry& in, double rho, double mu,
+                                                   int first) {
     ScalarStep r;
     r.out = in;
     r.apply = 0;
@@ -262,145 +140,7 @@ __device__ ScalarStep pcg_scalar_step(const GeoParams& gp, const Carry& in, cons
     return r;
 }
 
-// ---------------------------------------------------------------------------
-// Phase A: one CTA per (layer, instance).
-//   kPlain: phi = W^-1 in
-//   kPcg  : [apply iteration it-1's update] z = r/J; rho partial; phi = W^-1 z
-//   kFit  : [apply the last iteration's update]       phi = W^-1 c
-// ---------------------------------------------------------------------------
-template <typename T, int FLEN>
-__global__ void __launch_bounds__(1024, 1) k_layer_inverse(const GeoParams gp, const Bufs<T> bf, int mode, int it) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    T* buf = reinterpret_cast<T*>(smem_raw);
-    __shared__ double s_red[32];
-    __shared__ double s_beta, s_alpha;
-    __shared__ int s_apply;
-    const int l = blockIdx.x, b = blockIdx.y;
-    const int side = gp.side[l], P = side + 1, ne = side * side;
-    const size_t base = static_cast<size_t>(b) * gp.n + gp.coff[l];
-    const int nthr = blockDim.x, tid = threadIdx.x;
 
-    if (mode == kPlain) {
-        for (int e = tid; e < ne; e += nthr) buf[(e / side) * P + (e % side)] = bf.in[base + e];
-    } else {
-        const int upd = mode == kFit ? gp.iters : it;  // carry slot being produced
-        if (upd > 0) {
-            if (tid == 0) {
-                const int ci = b * (gp.iters + 1) + upd - 1;
-                const size_t pi = (static_cast<size_t>(b) * gp.iters + (upd - 1)) * gp.L;
-                const ScalarStep st =
-                    pcg_scalar_step(gp, bf.carry[ci], bf.rho_part + pi, bf.mu_part + pi, upd - 1 == 0);
-                s_apply = st.apply;
-                s_beta = st.beta;
-                s_alpha = st.alpha;
-                if (l == 0) {
-                    Carry o = st.out;
-                    if (st.log) bf.rho_log[static_cast<size_t>(b) * gp.iters + o.nlog++] = st.logval;
-                    bf.carry[ci + 1] = o;
-                }
-            }
-            __syncthreads();
-        } else if (tid == 0) {
-            s_apply = 0;
-            s_beta = 0.0;
-            s_alpha = 0.0;
-        }
-        __syncthreads();
-        const bool apply = s_apply != 0;
-        const T beta = static_cast<T>(s_beta), alpha = static_cast<T>(s_alpha);
-        double racc = 0.0;
-        for (int e = tid; e < ne; e += nthr) {
-            const size_t g = base + e;
-            const T jv = bf.jac[gp.coff[l] + e];
-            T rr = bf.r[g];
-            T cc = T(0);
-            if (apply) {  // pcg.hpp:101-104
-                const T zo = rr / jv;
-                const T pn = zo + beta * bf.p[g];
-                const T qn = bf.mz[g] + beta * bf.q[g];
-                cc = bf.c[g] + alpha * pn;
-                rr = rr - alpha * qn;
-                bf.p[g] = pn;
-                bf.q[g] = qn;
-                bf.c[g] = cc;
-                bf.r[g] = rr;
-            }
-            T v;
-            if (mode == kPcg) {
-                v = rr / jv;
-                racc += static_cast<double>(rr) * static_cast<double>(v);
-            } else {
-                v = apply ? cc : bf.c[g];
-            }
-            buf[(e / side) * P + (e % side)] = v;
-        }
-        if (mode == kPcg) {
-            const double t = block_sum(racc, s_red);
-            if (tid == 0) bf.rho_part[(static_cast<size_t>(b) * gp.iters + it) * gp.L + l] = t;
-        }
-    }
-    __syncthreads();
-    dwt_inverse<T, FLEN>(buf, side, P, gp.filt_off);
-    for (int e = tid; e < ne; e += nthr) bf.phi[base + e] = buf[(e / side) * P + (e % side)];
-}
-
-// ---------------------------------------------------------------------------
-// Phase C2: one CTA per (layer, instance): W y then the mode's epilogue.
-//   kPlain: out = W y                       (build_rhs / wavelet forward)
-//   kApply: out = W y + alpha D in          (apply_M, operators.hpp:324-332)
-//   kPcg  : s = W y + alpha D z, z = r/J; mu partial
-//   kRhs  : b1 = W y; r += b1 - b; b = b1   (reconstructor.hpp:321-323)
-// ---------------------------------------------------------------------------
-//
-// fit_term = 1 when y = sum_w P^T Gamma^T(...) (every caller except the bare
-// wavelet operator).  Its coarse (scale-0) coefficient is then exactly zero in
-// real arithmetic: the bilinear weights of every aperture node sum to one and
-// each subaperture's Gamma^T stencil (-x-y, x-y, -x+y, x+y; operators.hpp:
-// 182-185) sums to zero, so sum(y) = 0 and the periodic Daubechies coarse
-// coefficient is sum(y)/2^J.  The reference evaluates it as cancellation noise
-// (~1e-16 relative in fp64, measured 8e-11 of ||c|| after the 1/(alpha d_0)
-// amplification); an fp32 evaluation would inflate that noise to ~1e-2 of
-// ||c||, so fp32 engines (gp.piston_exact) use the exact value.
-template <typename T, int FLEN>
-__global__ void __launch_bounds__(1024, 1) k_layer_forward(const GeoParams gp, const Bufs<T> bf, int mode, int it,
-                                                           int fit_term) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    T* buf = reinterpret_cast<T*>(smem_raw);
-    __shared__ double s_red[32];
-    const int l = blockIdx.x, b = blockIdx.y;
-    const int side = gp.side[l], P = side + 1, ne = side * side;
-    const size_t base = static_cast<size_t>(b) * gp.n + gp.coff[l];
-    const int nthr = blockDim.x, tid = threadIdx.x;
-    for (int e = tid; e < ne; e += nthr) buf[(e / side) * P + (e % side)] = bf.y[base + e];
-    __syncthreads();
-    dwt_forward<T, FLEN>(buf, side, P, gp.filt_off);
-    const double* ad = gp.td + gp.ti[gp.o_reg + l];  // alpha * d_{l, scale}
-    double macc = 0.0;
-    for (int e = tid; e < ne; e += nthr) {
-        const int i = e / side, j = e % side;
-        const size_t g = base + e;
-        const T wy = (fit_term && gp.piston_exact && e == 0) ? T(0) : buf[i * P + j];
-        if (mode == kPlain) {
-            bf.out[g] = wy;
-        } else if (mode == kApply) {
-            const T adv = static_cast<T>(ad[bit_width(static_cast<unsigned>(max(i, j)))]);
-            bf.out[g] = wy + adv * bf.in[g];
-        } else if (mode == kPcg) {
-            const T adv = static_cast<T>(ad[bit_width(static_cast<unsigned>(max(i, j)))]);
-            const T z = bf.r[g] / bf.jac[gp.coff[l] + e];
-            const T s = wy + adv * z;
-            bf.mz[g] = s;
-            macc += static_cast<double>(s) * static_cast<double>(z);
-        } else {  // kRhs
-            bf.r[g] += wy - bf.b[g];
-            bf.b[g] = wy;
-        }
-    }
-    if (mode == kPcg) {
-        const double t = block_sum(macc, s_red);
-        if (tid == 0) bf.mu_part[(static_cast<size_t>(b) * gp.iters + it) * gp.L + l] = t;
-    }
-}
 
 // ---------------------------------------------------------------------------
 // Bilinear stencil pieces (operators.hpp:108-121): separable tables per

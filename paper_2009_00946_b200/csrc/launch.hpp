@@ -1,0 +1,21 @@
+// Launchers of the filter-length-templated cluster kernels, instantiated one
+// filter length per translation unit (layer_flen.cu, -DFEWHA_FLEN=N) so the
+// build parallelises.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+
+#include "device.hpp"
+
+namespace fewha_gpu {
+
+template <typename T, int FLEN>
+cudaError_t launch_layer_cluster(bool inverse, const GeoParams& gp, const Bufs<T>& bf, int mode, int it, int count,
+                                 cudaStream_t st, int gather, size_t smem);
+
+template <typename T, int FLEN>
+cudaError_t set_layer_cluster_attrs(size_t smem_inv, size_t smem_fwd);
+
+}  // namespace fewha_gpu

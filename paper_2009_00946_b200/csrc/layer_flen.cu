@@ -1,0 +1,46 @@
+// One filter length of the cluster layer kernels (compiled with -DFEWHA_FLEN=N).
+#include "cluster.cuh"
+#include "launch.hpp"
+
+#ifndef FEWHA_FLEN
+#error "compile with -DFEWHA_FLEN=<2|4|...|20>"
+#endif
+
+namespace fewha_gpu {
+
+template <typename T, int FLEN>
+cudaError_t launch_layer_cluster(bool inverse, const GeoParams& gp, const Bufs<T>& bf, int mode, int it, int count,
+                                 cudaStream_t st, int gather, size_t smem) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(gp.ccl, gp.L, count);
+    cfg.blockDim = dim3(256, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = gp.ccl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (inverse) return cudaLaunchKernelEx(&cfg, k_inv_cluster<T, FLEN>, gp, bf, mode, it);
+    return cudaLaunchKernelEx(&cfg, k_fwd_cluster<T, FLEN>, gp, bf, mode, it, gather);
+}
+
+template <typename T, int FLEN>
+cudaError_t set_layer_cluster_attrs(size_t smem_inv, size_t smem_fwd) {
+    cudaError_t e = cudaFuncSetAttribute(k_inv_cluster<T, FLEN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem_inv));
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_fwd_cluster<T, FLEN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem_fwd));
+}
+
+#define FEWHA_INST(T)                                                                                          \
+    template cudaError_t launch_layer_cluster<T, FEWHA_FLEN>(bool, const GeoParams&, const Bufs<T>&, int, int, int, \
+                                                             cudaStream_t, int, size_t);                        \
+    template cudaError_t set_layer_cluster_attrs<T, FEWHA_FLEN>(size_t, size_t);
+FEWHA_INST(double)
+FEWHA_INST(float)
+
+}  // namespace fewha_gpu
