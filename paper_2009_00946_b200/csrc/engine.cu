@@ -578,9 +578,17 @@ struct Launch {
 #define FEWHA_SET(N) CK((set_layer_cluster_attrs<T, N>(m, m)))
         FEWHA_FLEN_SWITCH(flen, FEWHA_SET)
 #undef FEWHA_SET
-        CK(cudaFuncSetAttribute(k_wfs<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxopt));
-        CK(cudaFuncSetAttribute(k_wfs<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxopt));
-        CK(cudaFuncSetAttribute(k_adjoint<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxopt));
+        auto opt_in = [&](auto kernel, size_t need) {
+            cudaFuncAttributes fa{};
+            CK(cudaFuncGetAttributes(&fa, kernel));
+            if (need + fa.sharedSizeBytes > m)
+                throw ConfigError("invalid geometry: layer kernels exceed the device's shared memory");
+            CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(m - fa.sharedSizeBytes)));
+        };
+        opt_in(k_wfs<T, false>, wfs_smem(gp));
+        opt_in(k_wfs<T, true>, wfs_smem(gp));
+        opt_in(k_adjoint<T>, adj_smem(gp));
     }
     // layer kernels: grid (C, L, count), cluster (C,1,1)
     static void cl(int flen, bool inverse, const GeoParams& gp, const Bufs<T>& bf, int mode, int it, int count,

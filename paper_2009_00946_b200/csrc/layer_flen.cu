@@ -27,13 +27,21 @@ cudaError_t launch_layer_cluster(bool inverse, const GeoParams& gp, const Bufs<T
     return cudaLaunchKernelEx(&cfg, k_fwd_cluster<T, FLEN>, gp, bf, mode, it, gather);
 }
 
+// Opt in to the device maximum minus each kernel's static shared memory.
+template <typename K>
+static cudaError_t opt_in_max(K kernel, size_t maxopt) {
+    cudaFuncAttributes fa{};
+    cudaError_t e = cudaFuncGetAttributes(&fa, kernel);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(maxopt - fa.sharedSizeBytes));
+}
+
 template <typename T, int FLEN>
 cudaError_t set_layer_cluster_attrs(size_t smem_inv, size_t smem_fwd) {
-    cudaError_t e = cudaFuncSetAttribute(k_inv_cluster<T, FLEN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem_inv));
+    cudaError_t e = opt_in_max(k_inv_cluster<T, FLEN>, smem_inv);
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_fwd_cluster<T, FLEN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(smem_fwd));
+    return opt_in_max(k_fwd_cluster<T, FLEN>, smem_fwd);
 }
 
 #define FEWHA_INST(T)                                                                                          \
