@@ -187,6 +187,7 @@ __device__ __forceinline__ void fwd_columns_cluster(const Band<T>& bd, int s, co
     T out[2][SEG];
     int jj[2], oo[2];
     cl.sync();  // row pass results of every rank visible
+    if (s == gp.maxside) stamp(gp, 4);
 #pragma unroll
     for (int rep = 0; rep < 2; ++rep) {
         const int it = tid + rep * nthr;
@@ -213,7 +214,9 @@ __device__ __forceinline__ void fwd_columns_cluster(const Band<T>& bd, int s, co
             out[rep][e] = acc;
         }
     }
+    if (s == gp.maxside) stamp(gp, 5);
     cl.sync();  // every rank done reading before anyone overwrites
+    if (s == gp.maxside) stamp(gp, 8);
 #pragma unroll
     for (int rep = 0; rep < 2; ++rep) {
         const int it = tid + rep * nthr;
@@ -288,7 +291,9 @@ __device__ void cluster_dwt_forward(const Band<T>& bd, int side, const GeoParams
     int s = side;
     for (; s >= 2 * bd.R; s >>= 1) {
         if (bd.rank < (s >> bd.rsh)) analysis_lines<T, FLEN, false>(bd.loc, bd.P, s, bd.R, gp);
+        if (s == side) stamp(gp, 3);
         fwd_columns_cluster<T, FLEN>(bd, s, gp, cl);
+        if (s == side) stamp(gp, 6);
     }
     stamp(gp, 7);
     if (bd.rank == 0) {
@@ -386,22 +391,24 @@ __device__ __forceinline__ void gather_contract(const T* blk, int nr, int nc, co
 // [row src R*KM short][col w side*KM T][row w R*KM T], each 16-byte aligned
 __device__ __forceinline__ int align16(int v) { return (v + 15) & ~15; }
 
+// psi block staged as the contiguous full rows [ilo, ihi) of the WFS grid
+// (np columns), fetched from the 16-byte aligned address at or below its start.
 template <typename T>
-__device__ __forceinline__ int staged_bytes(const WDesc& d, int side, int R, int KM) {
-    return align16((d.ihi - d.ilo) * (d.jhi - d.jlo) * static_cast<int>(sizeof(T))) + align16(side * KM * 2) +
+__device__ __forceinline__ int staged_bytes(const WDesc& d, int side, int R, int KM, int np) {
+    return align16((d.ihi - d.ilo) * np * static_cast<int>(sizeof(T)) + 16) + align16(side * KM * 2) +
            align16(R * KM * 2) + align16(side * KM * static_cast<int>(sizeof(T))) +
            align16(R * KM * static_cast<int>(sizeof(T)));
 }
 
 template <typename T>
 __device__ void gather_band(const GeoParams& gp, const T* __restrict__ psi_b, int l, const Band<T>& bd, bool owner,
-                            T* hc, unsigned char* stage, WDesc* desc) {
+                            T* hc, unsigned char* stage, WDesc* desc, Bulk& bulk) {
     const int side = gp.side[l];
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int KM = gp.gather_km;
     const int groups = min(nthr / side, bd.R);  // threads per layer column
     const int rows_pt = bd.R / groups;          // band rows per thread
-    const int J = tid % side, grp = tid / side;
+    const int J = tid & (side - 1), grp = tid >> ilog2(side);
     const int i0 = grp * rows_pt;
     const bool worker = owner && grp < groups;
     T out[kRowsPerThreadMax];
@@ -419,61 +426,62 @@ __device__ void gather_band(const GeoParams& gp, const T* __restrict__ psi_b, in
         desc[w] = d;
     }
     __syncthreads();
+    stamp(gp, 12);
     const unsigned char* blob = gp.gblob;
     int w0 = 0;
     while (w0 < gp.W) {
         int w1 = w0, used = 0;
         while (w1 < gp.W) {
-            const int need = staged_bytes<T>(desc[w1], side, bd.R, KM);
+            const int need = staged_bytes<T>(desc[w1], side, bd.R, KM, gp.ns[w1] + 1);
             if (w1 > w0 && used + need > gp.chunk_bytes) break;
             used += need;
             ++w1;
         }
-        // ---- stage the chunk (asynchronous copies only) ----
-        {
+        // ---- stage the chunk: thread 0 issues TMA bulk copies, everyone waits ----
+        if (tid == 0) {
+            bulk.begin();
             int off = 0;
             for (int w = w0; w < w1; ++w) {
                 const WDesc d = desc[w];
-                const int nr = d.ihi - d.ilo, nc = d.jhi - d.jlo;
+                const int nr = d.ihi - d.ilo, np = gp.ns[w] + 1;
                 unsigned char* p = stage + off;
-                off += staged_bytes<T>(d, side, bd.R, KM);
+                off += staged_bytes<T>(d, side, bd.R, KM, np);
                 if (nr <= 0) continue;
-                T* blk = reinterpret_cast<T*>(p);
-                const T* psi = psi_b + gp.woff[w];
-                const int np = gp.ns[w] + 1;
-                for (int idx = tid; idx < nr * nc; idx += nthr) {
-                    const int r = idx / nc, cc = idx - r * nc;
-                    cp_async_elem(blk + idx, psi + (d.ilo + r) * np + d.jlo + cc);
-                }
-                p += align16(nr * nc * static_cast<int>(sizeof(T)));
+                const T* src = psi_b + gp.woff[w] + d.ilo * np;
+                const uintptr_t a = reinterpret_cast<uintptr_t>(src);
+                const unsigned shift = static_cast<unsigned>(a & 15u);
+                bulk.copy(p, reinterpret_cast<const void*>(a - shift), shift + nr * np * static_cast<unsigned>(sizeof(T)));
+                p += align16(nr * np * static_cast<int>(sizeof(T)) + 16);
                 const unsigned char* g = blob + d.blob;  // [col src][row src][col w][row w]
                 const int cs_b = side * KM * 2, cw_b = side * KM * static_cast<int>(sizeof(T));
                 const int g_rs = align16(cs_b), g_cw = g_rs + align16(cs_b), g_rw = g_cw + align16(cw_b);
                 const int r0 = bd.rank * bd.R;
-                cp_async_bytes(p, g, cs_b);
+                bulk.copy(p, g, cs_b);
                 p += align16(cs_b);
-                cp_async_bytes(p, g + g_rs + r0 * KM * 2, bd.R * KM * 2);
+                bulk.copy(p, g + g_rs + r0 * KM * 2, bd.R * KM * 2);
                 p += align16(bd.R * KM * 2);
-                cp_async_bytes(p, g + g_cw, cw_b);
+                bulk.copy(p, g + g_cw, cw_b);
                 p += align16(cw_b);
-                cp_async_bytes(p, g + g_rw + r0 * KM * static_cast<int>(sizeof(T)),
-                               bd.R * KM * static_cast<int>(sizeof(T)));
+                bulk.copy(p, g + g_rw + r0 * KM * static_cast<int>(sizeof(T)), bd.R * KM * static_cast<int>(sizeof(T)));
             }
+            bulk.commit();
         }
-        cp_async_wait_all();
-        __syncthreads();
+        stamp(gp, 13);
+        bulk.wait();
         stamp(gp, 1);
         // ---- contract ----
         if (worker) {
             int off = 0;
             for (int w = w0; w < w1; ++w) {
                 const WDesc d = desc[w];
-                const int nr = d.ihi - d.ilo, nc = d.jhi - d.jlo;
+                const int nr = d.ihi - d.ilo, np = gp.ns[w] + 1;
                 const unsigned char* p = stage + off;
-                off += staged_bytes<T>(d, side, bd.R, KM);
+                off += staged_bytes<T>(d, side, bd.R, KM, np);
                 if (nr <= 0) continue;
-                const T* blk = reinterpret_cast<const T*>(p);
-                p += align16(nr * nc * static_cast<int>(sizeof(T)));
+                const unsigned shift =
+                    static_cast<unsigned>(reinterpret_cast<uintptr_t>(psi_b + gp.woff[w] + d.ilo * np) & 15u);
+                const T* blk = reinterpret_cast<const T*>(p + shift) + d.jlo;  // (r, c) at blk[r*np + c]
+                p += align16(nr * np * static_cast<int>(sizeof(T)) + 16);
                 const short* cs = reinterpret_cast<const short*>(p);
                 p += align16(side * KM * 2);
                 const short* rs = reinterpret_cast<const short*>(p);
@@ -481,9 +489,9 @@ __device__ void gather_band(const GeoParams& gp, const T* __restrict__ psi_b, in
                 const T* cw = reinterpret_cast<const T*>(p);
                 p += align16(side * KM * static_cast<int>(sizeof(T)));
                 const T* rw = reinterpret_cast<const T*>(p);
-                if (KM == 2) gather_contract<T, 2>(blk, nr, nc, cs, cw, rs, rw, d.ilo, J, i0, rows_pt, hc, nthr, tid, out);
-                else if (KM == 3) gather_contract<T, 3>(blk, nr, nc, cs, cw, rs, rw, d.ilo, J, i0, rows_pt, hc, nthr, tid, out);
-                else gather_contract<T, 4>(blk, nr, nc, cs, cw, rs, rw, d.ilo, J, i0, rows_pt, hc, nthr, tid, out);
+                if (KM == 2) gather_contract<T, 2>(blk, nr, np, cs, cw, rs, rw, d.ilo, J, i0, rows_pt, hc, nthr, tid, out);
+                else if (KM == 3) gather_contract<T, 3>(blk, nr, np, cs, cw, rs, rw, d.ilo, J, i0, rows_pt, hc, nthr, tid, out);
+                else gather_contract<T, 4>(blk, nr, np, cs, cw, rs, rw, d.ilo, J, i0, rows_pt, hc, nthr, tid, out);
             }
         }
         __syncthreads();  // chunk consumed before the next one is staged
@@ -524,14 +532,13 @@ __device__ __forceinline__ void warp_dot_sums(const double* rho_part, const doub
 // Shared memory: band | prefetched band slices of r, 1/J, p, q, c, Mz.
 // ---------------------------------------------------------------------------
 template <typename T, int FLEN>
-__global__ void __launch_bounds__(256) k_inv_cluster(const GeoParams gp, const Bufs<T> bf, int mode, int it) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    cg::cluster_group cl = cg::this_cluster();
+__device__ __forceinline__ void inv_phase(const GeoParams& gp, const Bufs<T>& bf, int mode, int it, unsigned char* smem_raw, int l,
+                          int b, cg::cluster_group& cl) {
     __shared__ double s_red[32];
     __shared__ double s_beta, s_alpha;
     __shared__ int s_apply;
-    const int l = blockIdx.y, b = blockIdx.z;
     const int side = gp.side[l];
+    const int lsd = ilog2(side);
     Band<T> bd = make_band<T>(reinterpret_cast<T*>(smem_raw), side, cl);
     const int C = static_cast<int>(cl.num_blocks());
     const bool owner = (bd.rank << bd.rsh) < side;  // holds rows of this layer
@@ -548,17 +555,29 @@ __global__ void __launch_bounds__(256) k_inv_cluster(const GeoParams gp, const B
     T *sr = pre, *sj = pre + ne, *sp = pre + 2 * ne, *sq = pre + 3 * ne, *sc = pre + 4 * ne, *sm = pre + 5 * ne;
     const int upd = mode == kFit ? gp.iters : it;
     const bool may_update = mode != kPlain && upd > 0;
-    if (mode == kPlain) {
-        cp_async_bytes(sr, bf.in + base, nb);
-    } else {
-        cp_async_bytes(sr, bf.r + base, nb);
-        cp_async_bytes(sj, bf.jinv + jbase, nb);
-        cp_async_bytes(sc, bf.c + base, nb);
-        if (may_update) {
-            cp_async_bytes(sp, bf.p + base, nb);
-            cp_async_bytes(sq, bf.q + base, nb);
-            cp_async_bytes(sm, bf.mz + base, nb);
+    __shared__ unsigned long long s_mbar;
+    Bulk bulk{&s_mbar, 0};
+    bulk.init();
+    if (tid == 0) {  // band slices by TMA bulk copy (16 KiB each at J=7 fp64)
+        bulk.begin();
+        if (nb > 0 && mode != kPlain) bulk.copy(sj, bf.jinv + jbase, nb);  // constant: before the wait
+    }
+    pdl_wait();  // the predecessor's outputs (r, c, p, q, Mz, dot partials) are complete
+    if (tid == 0) {
+        if (nb > 0) {
+            if (mode == kPlain) {
+                bulk.copy(sr, bf.in + base, nb);
+            } else {
+                bulk.copy(sr, bf.r + base, nb);
+                bulk.copy(sc, bf.c + base, nb);
+                if (may_update) {
+                    bulk.copy(sp, bf.p + base, nb);
+                    bulk.copy(sq, bf.q + base, nb);
+                    bulk.copy(sm, bf.mz + base, nb);
+                }
+            }
         }
+        bulk.commit();
     }
     if (mode != kPlain && tid < 32) {
         // scalar recurrences of the iteration whose dots are complete (warp 0)
@@ -583,11 +602,11 @@ __global__ void __launch_bounds__(256) k_inv_cluster(const GeoParams gp, const B
             s_alpha = st.alpha;
         }
     }
-    cp_async_wait_all();
+    bulk.wait();
     __syncthreads();
     stamp(gp, 1);
     if (mode == kPlain) {
-        for (int e = tid; e < ne; e += nthr) bd.loc[(e / side) * bd.P + (e % side)] = sr[e];
+        for (int e = tid; e < ne; e += nthr) bd.loc[(e >> lsd) * bd.P + (e & (side - 1))] = sr[e];
     } else {
         const bool apply = s_apply != 0;
         const T beta = static_cast<T>(s_beta), alpha = static_cast<T>(s_alpha);
@@ -616,7 +635,7 @@ __global__ void __launch_bounds__(256) k_inv_cluster(const GeoParams gp, const B
             } else {
                 v = cc;
             }
-            bd.loc[(e / side) * bd.P + (e % side)] = v;
+            bd.loc[(e >> lsd) * bd.P + (e & (side - 1))] = v;
         }
         if (mode == kPcg) {
             const double t = block_sum(racc, s_red);
@@ -629,7 +648,15 @@ __global__ void __launch_bounds__(256) k_inv_cluster(const GeoParams gp, const B
     cluster_dwt_inverse<T, FLEN>(bd, side, gp, cl);
     __syncthreads();
     stamp(gp, 9);
-    for (int e = tid; e < ne; e += nthr) bf.phi[base + e] = bd.loc[(e / side) * bd.P + (e % side)];
+    for (int e = tid; e < ne; e += nthr) bf.phi[base + e] = bd.loc[(e >> lsd) * bd.P + (e & (side - 1))];
+}
+
+template <typename T, int FLEN>
+__global__ void __launch_bounds__(256) k_inv_cluster(const GeoParams gp, const Bufs<T> bf, int mode, int it) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cg::cluster_group cl = cg::this_cluster();
+    pdl_launch_dependents();
+    inv_phase<T, FLEN>(gp, bf, mode, it, smem_raw, blockIdx.y, blockIdx.z, cl);
     cl.sync();  // no rank exits while its shared memory may still be read
     stamp(gp, 11);
 }
@@ -651,14 +678,12 @@ __global__ void __launch_bounds__(256) k_inv_cluster(const GeoParams gp, const B
 // (gp.piston_exact) use the exact value.
 // ---------------------------------------------------------------------------
 template <typename T, int FLEN>
-__global__ void __launch_bounds__(256) k_fwd_cluster(const GeoParams gp, const Bufs<T> bf, int mode, int it,
-                                                      int gather) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    cg::cluster_group cl = cg::this_cluster();
+__device__ __forceinline__ void fwd_phase(const GeoParams& gp, const Bufs<T>& bf, int mode, int it, int gather,
+                          unsigned char* smem_raw, int l, int b, cg::cluster_group& cl) {
     __shared__ double s_red[32];
     __shared__ WDesc s_desc[kMaxW];
-    const int l = blockIdx.y, b = blockIdx.z;
     const int side = gp.side[l];
+    const int lsd = ilog2(side);
     T* band = reinterpret_cast<T*>(smem_raw);
     Band<T> bd = make_band<T>(band, side, cl);
     const int C = static_cast<int>(cl.num_blocks());
@@ -676,36 +701,50 @@ __global__ void __launch_bounds__(256) k_fwd_cluster(const GeoParams gp, const B
     T* hc = reinterpret_cast<T*>(smem_raw + band_b + 2 * slice_b);
     unsigned char* stage = smem_raw + band_b + 2 * slice_b + align16(gp.hc_rows * nthr * static_cast<int>(sizeof(T)));
     const int nb = ne * static_cast<int>(sizeof(T));
-    // epilogue operands, requested now, consumed after the transform
-    if (mode == kApply) {
-        cp_async_bytes(e0, bf.in + base, nb);
-    } else if (mode == kPcg) {
-        cp_async_bytes(e0, bf.r + base, nb);
-        cp_async_bytes(e1, bf.jinv + jbase, nb);
-    } else if (mode == kRhs) {
-        cp_async_bytes(e0, bf.r + base, nb);
-        cp_async_bytes(e1, bf.b + base, nb);
+    __shared__ unsigned long long s_mbar[2];
+    Bulk epi{&s_mbar[0], 0}, stg{&s_mbar[1], 0};
+    epi.init();
+    stg.init();
+    pdl_wait();  // psi / y / r / b of the predecessor kernels are complete
+    // epilogue operands by TMA bulk copy, requested now, consumed after the transform
+    if (tid == 0) {
+        epi.begin();
+        if (nb > 0) {
+            if (mode == kApply) {
+                epi.copy(e0, bf.in + base, nb);
+            } else if (mode == kPcg) {
+                epi.copy(e0, bf.r + base, nb);
+                epi.copy(e1, bf.jinv + jbase, nb);
+            } else if (mode == kRhs) {
+                epi.copy(e0, bf.r + base, nb);
+                epi.copy(e1, bf.b + base, nb);
+            }
+        }
+        epi.commit();
     }
     if (!gather) {
-        cp_async_bytes(hc, bf.y + base, nb);
-        cp_async_wait_all();
-        __syncthreads();
-        for (int e = tid; e < ne; e += nthr) bd.loc[(e / side) * bd.P + (e % side)] = hc[e];
+        if (tid == 0) {
+            stg.begin();
+            if (nb > 0) stg.copy(hc, bf.y + base, nb);
+            stg.commit();
+        }
+        stg.wait();
+        for (int e = tid; e < ne; e += nthr) bd.loc[(e >> lsd) * bd.P + (e & (side - 1))] = hc[e];
     } else {
-        gather_band<T>(gp, bf.psi + static_cast<size_t>(b) * gp.Nw, l, bd, owner, hc, stage, s_desc);
+        gather_band<T>(gp, bf.psi + static_cast<size_t>(b) * gp.Nw, l, bd, owner, hc, stage, s_desc, stg);
     }
-    cp_async_wait_all();
     __syncthreads();
     stamp(gp, 2);
     cluster_dwt_forward<T, FLEN>(bd, side, gp, cl);
     __syncthreads();
     stamp(gp, 9);
+    epi.wait();
     const double* ad = gp.td + gp.ti[gp.o_reg + l];
     double macc = 0.0;
     for (int e = tid; e < ne; e += nthr) {
-        const int i = r0 + e / side, j = e % side;
+        const int i = r0 + (e >> lsd), j = e & (side - 1);
         const size_t g = base + e;
-        const T wy = (gather && gp.piston_exact && i == 0 && j == 0) ? T(0) : bd.loc[(e / side) * bd.P + j];
+        const T wy = (gather && gp.piston_exact && i == 0 && j == 0) ? T(0) : bd.loc[(e >> lsd) * bd.P + j];
         if (mode == kPlain) {
             bf.out[g] = wy;
         } else if (mode == kApply) {
@@ -728,6 +767,15 @@ __global__ void __launch_bounds__(256) k_fwd_cluster(const GeoParams gp, const B
             bf.mu_part[(static_cast<size_t>(b) * gp.iters + it) * (gp.L * C) + l * C + bd.rank] = t;
     }
     stamp(gp, 10);
+}
+
+template <typename T, int FLEN>
+__global__ void __launch_bounds__(256) k_fwd_cluster(const GeoParams gp, const Bufs<T> bf, int mode, int it,
+                                                      int gather) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cg::cluster_group cl = cg::this_cluster();
+    pdl_launch_dependents();
+    fwd_phase<T, FLEN>(gp, bf, mode, it, gather, smem_raw, blockIdx.y, blockIdx.z, cl);
     cl.sync();
     stamp(gp, 11);
 }

@@ -50,8 +50,12 @@ struct GeoParams {
     int o_fit;  // [m] fit table (n_act entries) or -1 for identity
     int o_reg;  // [l] offset into td of d_{l,0..J}
     // tiles
-    const int* wtiles;  // [n_wtiles][3] (w, i0, j0) for the per-WFS kernels
+    const int* wtiles;  // [n_wtiles][3] (w, i0, j0) for the per-WFS kernels (host bookkeeping)
     int n_wtiles, wtile;
+    int wt_first[kMaxW + 1];  // first tile of each WFS (prefix), tiles row-major per WFS
+    int wt_cols[kMaxW];       // tiles per row of WFS w
+    const unsigned char* tblob;  // per-tile stencil tables [tile][screen][axis][H] idx, then weights
+    int tt_stride_l, tt_stride_d, tt_off_d;  // byte stride per tile (layer / DM screens), DM base
     const int* ltiles;  // [n_ltiles][3] (l, I0, J0) for the adjoint-propagation kernel
     int n_ltiles, ltile, lt_rows_max, lt_cols_max;
     int o_tr;  // [(tile*W + w)*4] psi source block {ilo, ihi, jlo, jhi} of each layer tile (into ti)
@@ -62,6 +66,7 @@ struct GeoParams {
     int o_bs;         // [((w*L+l)*kMaxC + rank)*4] psi source block {ilo, ihi, jlo, jhi} of each band
     int bd_rows_max, bd_cols_max;
     unsigned long long* stamps;  // optional phase timestamps [block][16] (nullptr: off)
+    unsigned long long* fstamps; // optional frame-kernel phase timestamps [block][32]
     const unsigned char* gblob;  // per-(w,l) gather blobs of the engine's precision (see cluster.cuh)
     int o_gb;                    // [w*L + l] byte offset of each blob (into ti)
     int chunk_bytes;  // shared-memory budget of one staged WFS chunk in the band gather
@@ -87,6 +92,7 @@ enum KernelKind : int {
     kKindFwdPcg = 6,   // k_layer_forward kPcg: s = W y + alpha D z, mu
     kKindInvFit = 7,   // k_layer_inverse kFit: last update + W^-1 c
     kKindFit = 8,      // k_fit_control
+    kKindFrame = 9,    // k_frame: the whole step as one persistent cooperative launch
 };
 
 template <typename T>

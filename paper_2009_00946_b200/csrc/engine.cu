@@ -7,6 +7,7 @@
 #include <climits>
 #include <cstdint>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numbers>
 #include <stdexcept>
@@ -55,7 +56,7 @@ struct Plan {
     std::vector<double> td;
     std::vector<std::uint8_t> masks;
     std::vector<int> wtiles, ltiles;
-    std::vector<unsigned char> gblob;
+    std::vector<unsigned char> gblob, tblob;
     int maxside = 0;
 };
 
@@ -211,13 +212,55 @@ Plan build_plan(const Geometry& g, int elem_bytes) {
     }
 
     // WFS tiles: 16 x 16 nodes
-    gp.wtile = 16;
+    gp.wtile = kWfsTile;
     for (int w = 0; w < W; ++w) {
         const int np = g.wfs[w].n_subap + 1;
+        gp.wt_first[w] = static_cast<int>(pl.wtiles.size() / 3);
+        gp.wt_cols[w] = (np + gp.wtile - 1) / gp.wtile;
         for (int i0 = 0; i0 < np; i0 += gp.wtile)
             for (int j0 = 0; j0 < np; j0 += gp.wtile) pl.wtiles.insert(pl.wtiles.end(), {w, i0, j0});
     }
     gp.n_wtiles = static_cast<int>(pl.wtiles.size() / 3);
+    gp.wt_first[W] = gp.n_wtiles;
+    // per-tile stencil tables of the tile's halo rows/columns for every screen, in the
+    // shared-memory layout of wfs_tile (kernels.cuh): [screen][axis][H] idx | [screen][axis][H] weight
+    {
+        constexpr int H = kWfsTile + 2;
+        auto a16 = [](size_t v) { return (v + 15) & ~size_t(15); };
+        auto build = [&](int NS, bool dms) {
+            const size_t ib = a16(static_cast<size_t>(NS) * 2 * H * sizeof(int));
+            const size_t stride = ib + a16(static_cast<size_t>(NS) * 2 * H * elem_bytes);
+            const size_t base = pl.tblob.size();
+            pl.tblob.resize(base + stride * gp.n_wtiles, 0);
+            for (int t = 0; t < gp.n_wtiles; ++t) {
+                const int w = pl.wtiles[3 * t], i0 = pl.wtiles[3 * t + 1], j0 = pl.wtiles[3 * t + 2];
+                const int np = g.wfs[w].n_subap + 1;
+                unsigned char* p = pl.tblob.data() + base + stride * t;
+                for (int sc = 0; sc < NS; ++sc)
+                    for (int axis = 0; axis < 2; ++axis) {
+                        const int off = dms ? pl.ti[static_cast<size_t>(gp.o_pd + (w * M + sc) * 2 + axis)]
+                                            : pl.ti[static_cast<size_t>(gp.o_pl + (w * L + sc) * 4 + axis)];
+                        for (int kk = 0; kk < H; ++kk) {
+                            const int node = std::min(std::max((axis ? i0 : j0) - 1 + kk, 0), np - 1);
+                            const int q = (sc * 2 + axis) * H + kk;
+                            std::memcpy(p + q * sizeof(int), &pl.ti[static_cast<size_t>(off + node)], sizeof(int));
+                            const double wv = pl.td[static_cast<size_t>(off + node)];
+                            if (elem_bytes == 8) std::memcpy(p + ib + q * 8, &wv, 8);
+                            else {
+                                const float f = static_cast<float>(wv);
+                                std::memcpy(p + ib + q * 4, &f, 4);
+                            }
+                        }
+                    }
+            }
+            return std::pair<size_t, size_t>{base, stride};
+        };
+        const auto tl = build(L, false);
+        const auto td_ = build(M, true);
+        gp.tt_stride_l = static_cast<int>(tl.second);
+        gp.tt_stride_d = static_cast<int>(td_.second);
+        gp.tt_off_d = static_cast<int>(td_.first);
+    }
 
     // layer tiles for the adjoint gather; shrink until the psi block fits.
     // Per (tile, WFS) the exact source block: union of the per-node ranges.
@@ -374,7 +417,7 @@ Plan build_plan(const Geometry& g, int elem_bytes) {
                 for (int w = 0; w < W; ++w) {
                     const int* bs = &pl.ti[static_cast<size_t>(gp.o_bs + ((w * L + l) * kMaxC + rank) * 4)];
                     // mirrors staged_bytes() in cluster.cuh
-                    const size_t need = a16(static_cast<size_t>(bs[1] - bs[0]) * (bs[3] - bs[2]) * elem_bytes) +
+                    const size_t need = a16(static_cast<size_t>(bs[1] - bs[0]) * (g.wfs[w].n_subap + 1) * elem_bytes + 16) +
                                         a16(static_cast<size_t>(side) * km * 2) + a16(static_cast<size_t>(Rl) * km * 2) +
                                         a16(static_cast<size_t>(side) * km * elem_bytes) +
                                         a16(static_cast<size_t>(Rl) * km * elem_bytes);
@@ -492,7 +535,7 @@ struct Work {
         };
         bf.phi = A((T*)nullptr, n);
         bf.y = A((T*)nullptr, n);
-        bf.psi = A((T*)nullptr, static_cast<size_t>(gp.Nw) * cnt);
+        bf.psi = A((T*)nullptr, static_cast<size_t>(gp.Nw) * cnt + 16);  // bulk copies may read 16 B past rows
         meas = A((double*)nullptr, static_cast<size_t>(gp.S) * cnt);
         meas2 = A((double*)nullptr, static_cast<size_t>(gp.S) * cnt);
         bf.meas = meas;
@@ -530,12 +573,19 @@ struct Work {
 // ---------------------------------------------------------------------------
 // Typed launchers
 // ---------------------------------------------------------------------------
+// Programmatic dependent launch between the frame's kernels: opt-in
+// (FEWHA_PDL=1) -- measured neutral-to-negative on the ELT frame.
+inline bool pdl_enabled() {
+    static const bool on = [] {
+        const char* v = std::getenv("FEWHA_PDL");
+        return v && v[0] == '1';
+    }();
+    return on;
+}
+
 template <typename T>
 struct Launch {
-    static size_t wfs_smem(const GeoParams& gp) {
-        const int H = gp.wtile + 2, Q = gp.wtile + 1;
-        return static_cast<size_t>(H * H + 2 * Q * Q) * sizeof(T);
-    }
+    static size_t wfs_smem(const GeoParams& gp) { return wfs_tile_smem<T>(std::max(gp.L, gp.M)); }
     static size_t adj_smem(const GeoParams& gp) {
         return static_cast<size_t>(gp.lt_rows_max) * (gp.lt_cols_max + gp.ltile) * sizeof(T);
     }
@@ -598,16 +648,33 @@ struct Launch {
         FEWHA_FLEN_SWITCH(flen, FEWHA_LAUNCH)
 #undef FEWHA_LAUNCH
     }
+    // programmatic dependent launch config (the kernels call griddepcontrol)
+    static cudaLaunchConfig_t pdl_cfg(dim3 grid, size_t smem, cudaStream_t st, cudaLaunchAttribute* attr,
+                                      int threads = 256) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(threads, 1, 1);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cfg;
+    }
     static void wfs(bool rhs, const GeoParams& gp, const Bufs<T>& bf, int with_dm, int count, cudaStream_t st) {
-        const dim3 grid(gp.n_wtiles, count);
-        if (rhs) k_wfs<T, true><<<grid, 256, wfs_smem(gp), st>>>(gp, bf, with_dm);
-        else k_wfs<T, false><<<grid, 256, wfs_smem(gp), st>>>(gp, bf, with_dm);
+        cudaLaunchAttribute attr[1];
+        cudaLaunchConfig_t cfg = pdl_cfg(dim3(gp.n_wtiles, count), wfs_smem(gp), st, attr, 512);
+        if (rhs) CK(cudaLaunchKernelEx(&cfg, k_wfs<T, true>, gp, bf, with_dm));
+        else CK(cudaLaunchKernelEx(&cfg, k_wfs<T, false>, gp, bf, with_dm));
     }
     static void adjoint(const GeoParams& gp, const T* psi, T* y, int count, cudaStream_t st) {
         k_adjoint<T><<<dim3(gp.n_ltiles, count), 256, adj_smem(gp), st>>>(gp, psi, y);
     }
     static void fit(const GeoParams& gp, const Bufs<T>& bf, int step, int count, cudaStream_t st) {
-        k_fit_control<T><<<dim3((gp.A + 255) / 256, count), 256, 0, st>>>(gp, bf, step);
+        cudaLaunchAttribute attr[1];
+        cudaLaunchConfig_t cfg = pdl_cfg(dim3((gp.A + 255) / 256, count), 0, st, attr);
+        CK(cudaLaunchKernelEx(&cfg, k_fit_control<T>, gp, bf, step));
     }
 };
 
@@ -625,14 +692,18 @@ struct EngineImpl {
     bool own_stream = false;
     cudaGraphExec_t graph = nullptr;
     bool has_precond = false;
+    bool persistent = false;         // single-instance frames as one cooperative launch (frame.cuh)
+    unsigned int* bar = nullptr;     // its grid-barrier counter
     // optional per-phase timestamps of the cluster kernels (profiling only)
     unsigned long long* stamp_buf = nullptr;
     int stamp_slot = -1;  // < 0: stamping off
     static constexpr int kStampSlots = 32, kStampBlocks = 4096;
     GeoParams gps() {
         GeoParams g2 = gp;
-        if (stamp_slot >= 0 && stamp_slot < kStampSlots)
-            g2.stamps = stamp_buf + static_cast<size_t>(stamp_slot++) * kStampBlocks * 16;
+        if (stamp_slot >= 0 && stamp_slot < kStampSlots) {
+            if (persistent) g2.fstamps = stamp_buf;  // [block][32] in the first slots
+            else g2.stamps = stamp_buf + static_cast<size_t>(stamp_slot++) * kStampBlocks * 16;
+        }
         return g2;
     }
     std::vector<double> precond;
@@ -658,6 +729,10 @@ struct EngineImpl {
         int* lt = dalloc<int>(plan.ltiles.size());
         unsigned char* gb = dalloc<unsigned char>(plan.gblob.size());
         fr.add(gb);
+        unsigned char* tb = dalloc<unsigned char>(plan.tblob.size());
+        fr.add(tb);
+        if (!plan.tblob.empty())
+            CK(cudaMemcpy(tb, plan.tblob.data(), plan.tblob.size(), cudaMemcpyHostToDevice));
         if (!plan.gblob.empty())
             CK(cudaMemcpy(gb, plan.gblob.data(), plan.gblob.size(), cudaMemcpyHostToDevice));
         for (void* p : {(void*)ti, (void*)td, (void*)tf, (void*)mk, (void*)wt, (void*)lt}) fr.add(p);
@@ -677,6 +752,7 @@ struct EngineImpl {
         g.wtiles = wt;
         g.ltiles = lt;
         g.gblob = gb;
+        g.tblob = tb;
         return g;
     }
 
@@ -694,8 +770,17 @@ struct EngineImpl {
         bf.jac = static_cast<const T*>(jac);
         bf.jinv = static_cast<const T*>(jinv);
         const int B = batch;
+        if (persistent) {
+            const size_t smem = std::max(Launch<T>::fwd_cl_smem(gp), Launch<T>::inv_cl_smem(gp));
+#define FEWHA_PF(N) CK((launch_frame_persistent<T, N>(gps(), bf, bar, st, smem)))
+            FEWHA_FLEN_SWITCH(flen, FEWHA_PF)
+#undef FEWHA_PF
+            mark(kKindFrame);
+            CK(cudaGetLastError());
+            return;
+        }
         // RHS with the pseudo open-loop term (reconstructor.hpp:316-323)
-        Launch<T>::wfs(true, gp, bf, gp.closed, B, st);
+        Launch<T>::wfs(true, gps(), bf, gp.closed, B, st);
         mark(kKindWfsRhs);
         Launch<T>::cl(flen, false, gps(), bf, kRhs, 0, B, st);
         mark(kKindFwdRhs);
@@ -703,7 +788,7 @@ struct EngineImpl {
         for (int it = 0; it < gp.iters; ++it) {
             Launch<T>::cl(flen, true, gps(), bf, kPcg, it, B, st);
             mark(it == 0 ? kKindInvPcg0 : kKindInvPcg);
-            Launch<T>::wfs(false, gp, bf, 0, B, st);
+            Launch<T>::wfs(false, gps(), bf, 0, B, st);
             mark(kKindWfs);
             Launch<T>::cl(flen, false, gps(), bf, kPcg, it, B, st);
             mark(kKindFwdPcg);
@@ -945,6 +1030,30 @@ Engine::Engine(Geometry g, int precision, int batch, int device) : p_(std::make_
         P.jinv = dalloc<float>(P.gp.n);
     }
     Launch<double>::set_attrs(P.gp64, P.flen);  // probes always fp64
+    {
+        const char* env = std::getenv("FEWHA_PERSISTENT");
+        // opt-in until its phases outrun the launch gaps they remove
+        const bool allow = batch == 1 && env && env[0] == '1';
+        int ok = 0;
+        if (allow) {
+            if (precision == 64) {
+                const size_t smem = std::max(Launch<double>::fwd_cl_smem(P.gp), Launch<double>::inv_cl_smem(P.gp));
+#define FEWHA_FIT(N) CK((frame_persistent_fits<double, N>(P.gp, smem, &ok)))
+                FEWHA_FLEN_SWITCH(P.flen, FEWHA_FIT)
+#undef FEWHA_FIT
+            } else {
+                const size_t smem = std::max(Launch<float>::fwd_cl_smem(P.gp), Launch<float>::inv_cl_smem(P.gp));
+#define FEWHA_FIT(N) CK((frame_persistent_fits<float, N>(P.gp, smem, &ok)))
+                FEWHA_FLEN_SWITCH(P.flen, FEWHA_FIT)
+#undef FEWHA_FIT
+            }
+        }
+        if (ok) {
+            P.bar = dalloc<unsigned int>(1);
+            P.fr.add(P.bar);
+            P.persistent = true;
+        }
+    }
     P.fr.add(P.jac);
     P.fr.add(P.jinv);
     reset();
@@ -1115,7 +1224,7 @@ void Engine::sync_check() {
         if (s) throw std::runtime_error("pcg_solve: non-finite scalar (indefinite operator?)");
 }
 
-int Engine::launches_per_step() const { return 4 + 3 * p_->gp.iters; }
+int Engine::launches_per_step() const { return p_->persistent ? 1 : 4 + 3 * p_->gp.iters; }
 
 int Engine::profile_step(float* ms, int* kinds, int max) {
     auto& P = *p_;

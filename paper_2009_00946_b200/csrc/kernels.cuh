@@ -48,6 +48,71 @@ struct Filt<float> {
     __device__ static float hi(const GeoParams& gp, int k) { return gp.fhi_f[k]; }
 };
 
+// ---- TMA 1-D bulk copies (cp.async.bulk) completing on an mbarrier --------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* m, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(m)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* m, unsigned bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* m) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(m)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* m, unsigned parity) {
+    asm volatile(
+        "{\n.reg .pred P;\nWAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+        "@!P bra WAIT_%=;\n}\n" ::"r"(smem_u32(m)),
+        "r"(parity)
+        : "memory");
+}
+// dst, src 16-byte aligned; bytes a multiple of 16 (callers round up inside padded buffers)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* m) {
+    mbar_expect_tx(m, bytes);
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(m))
+                 : "memory");
+}
+__device__ __forceinline__ unsigned round16(unsigned v) { return (v + 15u) & ~15u; }
+
+// A single-use-per-phase bulk loader: thread 0 issues, everyone waits.
+struct Bulk {
+    unsigned long long* mbar;
+    unsigned phase;
+    __device__ __forceinline__ void init() {
+        if (threadIdx.x == 0) {
+            mbar_init(mbar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        }
+        __syncthreads();
+        phase = 0;
+    }
+    // thread 0 only
+    __device__ __forceinline__ void begin() {
+        asm volatile("fence.proxy.async.global;\n" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    }
+    __device__ __forceinline__ void copy(void* dst, const void* src, unsigned bytes) { bulk_g2s(dst, src, round16(bytes), mbar); }
+    __device__ __forceinline__ void commit() { mbar_arrive(mbar); }
+    // all threads
+    __device__ __forceinline__ void wait() {
+        mbar_wait(mbar, phase);
+        phase ^= 1u;
+    }
+};
+
+// ---- programmatic dependent launch -------------------------------------------
+// Every frame kernel lets its successor launch at once (launch_dependents) and
+// waits for its predecessor's results only where it first reads them
+// (griddepcontrol.wait): launch latency and constant-table prefetches overlap
+// the previous kernel's tail.  Both are no-ops for non-programmatic launches.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
 template <typename T>
 __device__ __forceinline__ const T* weights(const GeoParams& gp);
 template <>
@@ -187,35 +252,117 @@ __device__ __forceinline__ T prop_dms(const GeoParams& gp, const T* dms, int w, 
 //   rhs=true : psi = fault * Gamma^T C^-1 (s + [closed] Gamma P_dm a_prev2)
 //              (add_dm_slopes :259-280 + build_rhs stage 1 :221-231)
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ void wstamp(const GeoParams& gp, int k) {
+    if (gp.stamps == nullptr || threadIdx.x != 0) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const unsigned blk = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    gp.stamps[blk * 16 + k] = t;
+}
+
+constexpr int kWfsTile = 16;  // WFS node tile side (compile-time: index math by constants)
+
+// Shared memory of one WFS tile: stencil tables of the tile's halo rows and
+// columns for every screen, then the wavefront, then the two slope grids.
+template <typename T>
+__host__ __device__ constexpr size_t wfs_tile_table_bytes(int screens) {
+    constexpr int H = kWfsTile + 2;
+    return ((static_cast<size_t>(screens) * 2 * H * sizeof(int) + 15) & ~size_t(15)) +
+           ((static_cast<size_t>(screens) * 2 * H * sizeof(T) + 15) & ~size_t(15));
+}
+template <typename T>
+__host__ __device__ constexpr size_t wfs_tile_smem(int screens) {
+    constexpr int H = kWfsTile + 2, Q = kWfsTile + 1;
+    return wfs_tile_table_bytes<T>(screens) + static_cast<size_t>(H * H + 2 * Q * Q) * sizeof(T);
+}
+
 template <typename T, bool RHS>
-__global__ void __launch_bounds__(256) k_wfs(const GeoParams gp, const Bufs<T> bf, int with_dm) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int TS = gp.wtile, H = TS + 2, Q = TS + 1;
-    T* ph = reinterpret_cast<T*>(smem_raw);
-    T* sx = ph + H * H;
-    T* sy = sx + Q * Q;
-    const int tile = blockIdx.x, b = blockIdx.y;
-    const int w = gp.wtiles[3 * tile], i0 = gp.wtiles[3 * tile + 1], j0 = gp.wtiles[3 * tile + 2];
+__device__ __forceinline__ void wfs_tile(const GeoParams& gp, const Bufs<T>& bf, int with_dm, int tile, int b,
+                                         unsigned char* smem_raw) {
+    constexpr int TS = kWfsTile, H = TS + 2, Q = TS + 1;
+    int w = 0;
+    while (w + 1 < gp.W && tile >= gp.wt_first[w + 1]) ++w;
+    const int local = tile - gp.wt_first[w], trow = local / gp.wt_cols[w];
+    const int i0 = trow * TS, j0 = (local - trow * gp.wt_cols[w]) * TS;
     const int ns = gp.ns[w], np = ns + 1;
     const int tid = threadIdx.x, nthr = blockDim.x;
-
-    // 1. wavefront on the tile + 1-node halo
+    const bool screens_on = !RHS || with_dm;
+    const int NS = RHS ? gp.M : gp.L;  // screens: DMs for the RHS, layers otherwise
+    // stencil tables of the halo rows/columns: [screen][axis][H] (index), then weights
+    const int ib = (NS * 2 * H * static_cast<int>(sizeof(int)) + 15) & ~15;
+    int* tix = reinterpret_cast<int*>(smem_raw);
+    T* tw = reinterpret_cast<T*>(smem_raw + ib);
+    T* ph = tw + NS * 2 * H;
+    T* sx = ph + H * H;
+    T* sy = sx + Q * Q;
+    __shared__ unsigned long long s_mbar;
+    wstamp(gp, 0);
+    if (screens_on) {
+        // prebuilt per-tile tables (constant): fetched by one TMA bulk copy before
+        // waiting on the predecessor kernel
+        if (tid == 0) {
+            mbar_init(&s_mbar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // smem reused by a persistent caller
+            const int stride = RHS ? gp.tt_stride_d : gp.tt_stride_l;
+            const unsigned char* src = gp.tblob + (RHS ? gp.tt_off_d : 0) + static_cast<size_t>(tile) * stride;
+            bulk_g2s(smem_raw, src, static_cast<unsigned>(stride), &s_mbar);
+            mbar_arrive(&s_mbar);
+        }
+        __syncthreads();
+        pdl_wait();
+        mbar_wait(&s_mbar, 0);
+    } else {
+        pdl_wait();
+    }
+    __syncthreads();
+    wstamp(gp, 1);
+    // 1. wavefront on the tile + 1-node halo (propagate_point, operators.hpp:204-213)
+    const T* src = RHS ? bf.a_prev2 + static_cast<size_t>(b) * gp.A : bf.phi + static_cast<size_t>(b) * gp.n;
     for (int idx = tid; idx < H * H; idx += nthr) {
-        const int i = i0 - 1 + idx / H, j = j0 - 1 + idx % H;
+        const int a = idx / H, c = idx - a * H;
+        const int i = i0 - 1 + a, j = j0 - 1 + c;
         T v = T(0);
-        if (i >= 0 && i < np && j >= 0 && j < np) {
-            if (!RHS) v = prop_layers<T>(gp, bf.phi + static_cast<size_t>(b) * gp.n, w, i, j);
-            else if (with_dm) v = prop_dms<T>(gp, bf.a_prev2 + static_cast<size_t>(b) * gp.A, w, i, j);
+        if (screens_on && i >= 0 && i < np && j >= 0 && j < np) {
+            // screens in unrolled groups of G: a group's 4G loads are in flight together
+            // (padding screens of the last group read a valid node with weight 0)
+            constexpr int G = 9;
+            for (int s0 = 0; s0 < NS; s0 += G) {
+                T q00[G], q01[G], q10[G], q11[G], fy[G], fx[G];
+#pragma unroll
+                for (int u = 0; u < G; ++u) {
+                    const int sc = min(s0 + u, NS - 1);
+                    const int* tx = tix + sc * 2 * H;
+                    const T* wx = tw + sc * 2 * H;
+                    const int stride = RHS ? gp.nact[sc] : gp.side[sc];
+                    const T* r0 = src + (RHS ? gp.aoff[sc] : gp.coff[sc]) + tx[H + a] * stride + tx[c];
+                    q00[u] = r0[0];
+                    q01[u] = r0[1];
+                    q10[u] = r0[stride];
+                    q11[u] = r0[stride + 1];
+                    fy[u] = s0 + u < NS ? wx[H + a] : T(0);
+                    fx[u] = wx[c];
+                }
+#pragma unroll
+                for (int u = 0; u < G; ++u) {
+                    if (s0 + u >= NS) break;
+                    // bilinear(): w00 v00 + w01 v01 + w10 v10 + w11 v11 (operators.hpp:125-126)
+                    const T w00 = (T(1) - fy[u]) * (T(1) - fx[u]), w01 = (T(1) - fy[u]) * fx[u];
+                    const T w10 = fy[u] * (T(1) - fx[u]), w11 = fy[u] * fx[u];
+                    v += w00 * q00[u] + w01 * q01[u] + w10 * q10[u] + w11 * q11[u];
+                }
+            }
         }
         ph[idx] = v;
     }
     __syncthreads();
+    wstamp(gp, 2);
     // 2. weighted half-slopes on the (TS+1)^2 subapertures touching the tile
     const T iv = static_cast<T>(gp.inv_var[w]);
     const std::uint8_t* mask = gp.masks + gp.mkoff[w];
     const double* meas = bf.meas + static_cast<size_t>(b) * gp.S + gp.moff[w];
     for (int idx = tid; idx < Q * Q; idx += nthr) {
-        const int a = idx / Q, c = idx % Q;
+        const int a = idx / Q, c = idx - a * Q;
         const int i = i0 - 1 + a, j = j0 - 1 + c;
         T x = T(0), y = T(0);
         if (i >= 0 && i < ns && j >= 0 && j < ns && mask[i * ns + j]) {
@@ -236,11 +383,12 @@ __global__ void __launch_bounds__(256) k_wfs(const GeoParams gp, const Bufs<T> b
         sy[idx] = y;
     }
     __syncthreads();
+    wstamp(gp, 3);
     // 3. adjoint slopes: gather of the 4 neighbouring subapertures in the
     //    reference's scatter order (operators.hpp:176-187)
     T* psi = bf.psi + static_cast<size_t>(b) * gp.Nw + gp.woff[w];
     for (int idx = tid; idx < TS * TS; idx += nthr) {
-        const int a = idx / TS, c = idx % TS;
+        const int a = idx / TS, c = idx - a * TS;
         const int i = i0 + a, j = j0 + c;
         if (i >= np || j >= np) continue;
         T v = sx[a * Q + c] + sy[a * Q + c];
@@ -250,6 +398,14 @@ __global__ void __launch_bounds__(256) k_wfs(const GeoParams gp, const Bufs<T> b
         if (gp.fault != 1.0) v *= static_cast<T>(gp.fault);
         psi[i * np + j] = v;
     }
+    wstamp(gp, 4);
+}
+
+template <typename T, bool RHS>
+__global__ void __launch_bounds__(512, 2) k_wfs(const GeoParams gp, const Bufs<T> bf, int with_dm) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    pdl_launch_dependents();
+    wfs_tile<T, RHS>(gp, bf, with_dm, blockIdx.x, blockIdx.y, smem_raw);
 }
 
 // ---------------------------------------------------------------------------
@@ -332,21 +488,20 @@ __global__ void __launch_bounds__(256) k_adjoint(const GeoParams gp, const T* __
 //   step=0: out = a~ (fit_to_mirrors operator)
 // ---------------------------------------------------------------------------
 template <typename T>
-__global__ void __launch_bounds__(256) k_fit_control(const GeoParams gp, const Bufs<T> bf, int step) {
-    const int b = blockIdx.y;
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (step && blockIdx.x == 0 && threadIdx.x == 0) {
-        // frame epilogue: publish status, seed the next frame's carry slot 0
-        Carry c = bf.carry[b * (gp.iters + 1) + gp.iters];
-        bf.status[b] = c.err;
-        bf.nlog[b] = c.nlog;
-        c.done = 0;
-        c.err = 0;
-        c.nlog = 0;
-        c.rho_entry = 0.0;
-        bf.carry[b * (gp.iters + 1)] = c;
-    }
-    if (k >= gp.A) return;
+__device__ __forceinline__ void frame_epilogue(const GeoParams& gp, const Bufs<T>& bf, int b) {
+    // publish status, seed the next frame's carry slot 0
+    Carry c = bf.carry[b * (gp.iters + 1) + gp.iters];
+    bf.status[b] = c.err;
+    bf.nlog[b] = c.nlog;
+    c.done = 0;
+    c.err = 0;
+    c.nlog = 0;
+    c.rho_entry = 0.0;
+    bf.carry[b * (gp.iters + 1)] = c;
+}
+
+template <typename T>
+__device__ void fit_actuator(const GeoParams& gp, const Bufs<T>& bf, int step, int k, int b) {
     int m = 0;
     while (m + 1 < gp.M && k >= gp.aoff[m + 1]) ++m;
     const int idx = k - gp.aoff[m], na = gp.nact[m];
@@ -371,6 +526,16 @@ __global__ void __launch_bounds__(256) k_fit_control(const GeoParams gp, const B
     bf.a_prev2[g] = a0;
     bf.a_prev[g] = an;
     bf.a_out[g] = an;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_fit_control(const GeoParams gp, const Bufs<T> bf, int step) {
+    pdl_launch_dependents();
+    pdl_wait();
+    const int b = blockIdx.y;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (step && blockIdx.x == 0 && threadIdx.x == 0) frame_epilogue(gp, bf, b);
+    if (k < gp.A) fit_actuator(gp, bf, step, k, b);
 }
 
 // ---------------------------------------------------------------------------

@@ -18,4 +18,11 @@ cudaError_t launch_layer_cluster(bool inverse, const GeoParams& gp, const Bufs<T
 template <typename T, int FLEN>
 cudaError_t set_layer_cluster_attrs(size_t smem_inv, size_t smem_fwd);
 
+template <typename T, int FLEN>
+cudaError_t launch_frame_persistent(const GeoParams& gp, const Bufs<T>& bf, unsigned int* bar, cudaStream_t st,
+                                    size_t smem);
+
+template <typename T, int FLEN>
+cudaError_t frame_persistent_fits(const GeoParams& gp, size_t smem, int* ok);
+
 }  // namespace fewha_gpu
