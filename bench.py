@@ -2,13 +2,15 @@
 """Benchmark of the FEWHA reconstruction frame (Reconstructor::step) on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--precision 64|32] [--preset presets/elt_mcao84.json]
+                    [--precision 64|32] [--preset presets/elt_mcao84_3dm.json]
 
 Workload (BASELINE.json metric "per-frame reconstruction latency p50/p99 (ms)
-and recon/sec vs memory roofline"): ELT MCAO-84 -- 39 m, 6 LGS 84x84 + 3 NGS,
-9 layers of 128^2 (J=7), closed loop, 4 warm-started PCG iterations, fp64 --
-in its reference-runnable L=M=9 form (presets/elt_mcao84.json; the 3-DM
-fitting is SURVEY.md 8f "next").  One step = one frame of one instance.
+and recon/sec vs memory roofline", config 3): ELT MCAO-84 -- 39 m, 6 LGS 84x84
++ 3 NGS, 9 layers of 128^2 (J=7), 3 DMs (81^2, 48^2, 54^2), closed loop, 4
+warm-started PCG iterations, fp64 (presets/elt_mcao84_3dm.json; the 3-DM
+fitting is the projection extension).  One step = one frame of one
+instance.  The reference supports only L = M, so its CPU arm runs the L = M
+shadow of the same preset (same layers, WFS and PCG; 9 identity-fitted DMs).
 
   value      reconstructions/s over all ranks, slopes resident in HBM, timed with
              CUDA events around each frame's graph launch; L2 flushed (256 MiB
@@ -44,7 +46,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "per-frame reconstruction latency p50/p99 (ms) and recon/sec vs memory roofline"
 UNIT = "recon/s"
-DEFAULT_PRESET = os.path.join(ROOT, "presets", "elt_mcao84.json")
+DEFAULT_PRESET = os.path.join(ROOT, "presets", "elt_mcao84_3dm.json")
 L2_FLUSH_BYTES = 256 << 20
 
 
@@ -183,11 +185,25 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def reference_preset(preset):
+    """The reference accepts only L = M: for a projection-fitting preset return
+    its L = M shadow (same layers, WFS, solver; one DM per layer)."""
+    j = load_json(preset)
+    if j.get("fitting", "identity") != "projection":
+        return preset
+    j.pop("fitting", None)
+    j["dms"] = [{"n_act": 1 << l["grid_order"], "conjugation_height": l["height"]} for l in j["layers"]]
+    path = os.path.join("/tmp", "fewha_ref_shadow_" + os.path.basename(preset))
+    with open(path, "w") as f:
+        json.dump(j, f)
+    return path
+
+
 def cpu_reference_time(preset, stream, frames, threads):
     """Reference solver (oracle/_ref) on this host: per-frame wall times (us)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     from oracle import RefOracle  # noqa: E402
-    r = RefOracle(preset, threads=threads)
+    r = RefOracle(reference_preset(preset), threads=threads)
     r.build_preconditioner()
     r.time_steps(stream[:2], 2)  # warm-up frames
     us = r.time_steps(stream, frames)
@@ -207,7 +223,7 @@ def run_reference(args):
     threads = os.cpu_count() or 1
     rng = np.random.default_rng(7)
     # reference-side slope stream: the reference's own synthesis (bench.hpp:144-154 pattern)
-    r = RefOracle(args.preset, threads=threads)
+    r = RefOracle(reference_preset(args.preset), threads=threads)
     stream = np.stack([r.synthesize(1, k) for k in range(4)])
     r.build_preconditioner()
     r.time_steps(stream, max(args.warmup, 1))
@@ -219,7 +235,8 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(float(np.mean(ms)), 4),
         "p50_ms": round(float(np.percentile(ms, 50)), 4), "p99_ms": round(float(np.percentile(ms, 99)), 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "ELT MCAO-84 (L=M=9) single-instance frame, reference CPU solver",
+        "config": {"workload": "ELT MCAO-84 single-instance frame, reference CPU solver "
+                               "(L=M shadow of the 3-DM preset: the reference supports only L=M)",
                    "preset": os.path.relpath(args.preset, ROOT), "threads": r.threads},
         "cpu_baseline": {"value": round(val, 3), "unit": UNIT, "cores": r.threads, "kind": "reference",
                          "sample": f"{args.steps} frames of Reconstructor::step after {max(args.warmup,1)} warm-up, "
@@ -380,7 +397,7 @@ def run_ours(args):
             us, thr = cpu_reference_time(args.preset, stream_host, frames, threads)
             cms = us / 1000.0
             cpu = {"value": round(1000.0 / float(np.mean(cms)), 3), "unit": UNIT, "cores": thr, "kind": "reference",
-                   "sample": f"{frames} frames of the reference Reconstructor::step (oracle/_ref) on this slope stream, "
+                   "sample": f"{frames} frames of the reference Reconstructor::step (oracle/_ref, L=M shadow preset) on this slope stream, "
                              f"{thr} pool threads (min(max(L,W), nproc)), {os.cpu_count()} host cpus; "
                              f"p50 {np.percentile(cms, 50):.2f} ms p99 {np.percentile(cms, 99):.2f} ms"}
 
@@ -392,8 +409,8 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": round(total_ms / K, 5), "p50_ms": round(p50, 5),
             "p99_ms": round(p99, 5), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64" if args.precision == 64 else "f32", "data": "synthetic",
-            "config": {"workload": "ELT MCAO-84 (L=M=9 reference-runnable form), 1 instance/rank, closed loop, "
-                                   "4 PCG iters, frame latency",
+            "config": {"workload": "ELT MCAO-84 (BASELINE config 3: 84x84 SH, 6 LGS + 3 NGS, 9 layers, 3 DMs), "
+                                   "1 instance/rank, closed loop, 4 PCG iters, single-frame latency",
                        "preset": os.path.relpath(args.preset, ROOT), "n_coeff": d["n"], "n_slopes": S,
                        "n_act": d["A"], "l2": "flushed (256 MiB write) before every timed frame",
                        "parallelism": f"replicas x{world}"},

@@ -23,6 +23,8 @@ struct orc {
     double *noise_variance, *theta_x, *theta_y, *star_height, *layer_height, *layer_extent, *layer_strength,
         *dm_height, *dm_extent;
     unsigned char* masks; /* concatenated n_s^2 per WFS */
+    int* dm_group;        /* projection fitting: layer bitmask per DM */
+    double *dm_tx, *dm_ty;
     size_t *mask_off, *meas_off, *wf_off, *coeff_off, *act_off;
     int* side;
     size_t n, S, Nw, A;
@@ -451,6 +453,30 @@ int orc_add_dm_slopes(orc_t* h, const double* a, double* meas) {
 
 /* ---- reconstructor.hpp:284-305 fit_to_mirrors ----------------------------- */
 int orc_fit(orc_t* h, const double* c, double* a) {
+    if (h->cfg.projection) { /* L != M extension */
+        memcpy(h->layer_work, c, sizeof(double) * h->n);
+        orc_wavelet(h, 1, h->layer_work);
+        for (int m = 0; m < h->cfg.n_dms; ++m) {
+            const int na = h->n_act[m];
+            const double e = h->dm_extent[m], da = e / (na - 1);
+            double* out = a + h->act_off[m];
+            for (int i = 0; i < na; ++i)
+                for (int j = 0; j < na; ++j) {
+                    const double px = -e / 2.0 + j * da, py = -e / 2.0 + i * da;
+                    double acc = 0.0;
+                    for (int l = 0; l < h->cfg.n_layers; ++l) {
+                        if (!(h->dm_group[m] >> l & 1)) continue;
+                        double v;
+                        if (sample(h, h->layer_work + h->coeff_off[l], h->side[l], h->layer_extent[l],
+                                   px + h->dm_tx[m] * h->layer_height[l], py + h->dm_ty[m] * h->layer_height[l], &v))
+                            return 1;
+                        acc += v;
+                    }
+                    out[(size_t)i * na + j] = acc;
+                }
+        }
+        return 0;
+    }
     for (int l = 0; l < h->cfg.n_layers; ++l) {
         const int side = h->side[l];
         double* grid = h->layer_work + h->coeff_off[l];
@@ -731,7 +757,7 @@ orc_t* orc_create(const orc_config* cfg, char* err, int errlen, int* code) {
         *code = 2;
         return NULL;
     }
-    if (cfg->n_dms != cfg->n_layers) { /* geometry.hpp:294-296 */
+    if (!cfg->projection && cfg->n_dms != cfg->n_layers) { /* geometry.hpp:294-296 */
         snprintf(err, (size_t)errlen,
                  "invalid geometry: dm count %d != layer count %d (only the L = M identity-fitting mode is supported)",
                  cfg->n_dms, cfg->n_layers);
@@ -762,7 +788,41 @@ orc_t* orc_create(const orc_config* cfg, char* err, int errlen, int* code) {
 
     for (int l = 0; l < L; ++l)
         if (h->layer_extent[l] <= 0.0) h->layer_extent[l] = layer_extent_derived(h, l);
-    for (int m = 0; m < M; ++m) h->dm_extent[m] = h->layer_extent[m]; /* geometry.hpp:374 */
+    h->dm_group = calloc((size_t)(M > 0 ? M : 1), sizeof(int));
+    h->dm_tx = calloc((size_t)(M > 0 ? M : 1), sizeof(double));
+    h->dm_ty = calloc((size_t)(M > 0 ? M : 1), sizeof(double));
+    if (!cfg->projection) {
+        for (int m = 0; m < M; ++m) h->dm_extent[m] = h->layer_extent[m]; /* geometry.hpp:374 */
+    } else {
+        int any = 0;
+        for (int m = 0; m < M; ++m) {
+            h->dm_group[m] = cfg->dm_layer_mask ? cfg->dm_layer_mask[m] : 0;
+            h->dm_tx[m] = cfg->dm_theta_x ? cfg->dm_theta_x[m] : 0.0;
+            h->dm_ty[m] = cfg->dm_theta_y ? cfg->dm_theta_y[m] : 0.0;
+            any |= h->dm_group[m];
+        }
+        if (!any) /* each layer to the DM of nearest conjugation height (ties: lower index) */
+            for (int l = 0; l < L; ++l) {
+                int best = 0;
+                for (int m = 1; m < M; ++m)
+                    if (fabs(h->dm_height[m] - h->layer_height[l]) < fabs(h->dm_height[best] - h->layer_height[l])) best = m;
+                h->dm_group[best] |= 1 << l;
+            }
+        for (int m = 0; m < M; ++m) {
+            if (cfg->dm_extent_in && cfg->dm_extent_in[m] > 0.0) {
+                h->dm_extent[m] = cfg->dm_extent_in[m];
+                continue;
+            }
+            double e = INFINITY;
+            const double t = fabs(h->dm_tx[m]) > fabs(h->dm_ty[m]) ? fabs(h->dm_tx[m]) : fabs(h->dm_ty[m]);
+            for (int l = 0; l < L; ++l)
+                if (h->dm_group[m] >> l & 1) {
+                    const double v = h->layer_extent[l] - 2.0 * t * h->layer_height[l];
+                    if (v < e) e = v;
+                }
+            h->dm_extent[m] = (e > 0.0 && isfinite(e)) ? e : cfg->diameter;
+        }
+    }
 
     h->mask_off = malloc(sizeof(size_t) * (size_t)(W + 1));
     h->meas_off = malloc(sizeof(size_t) * (size_t)(W + 1));
@@ -833,7 +893,7 @@ void orc_destroy(orc_t* h) {
     void* ptrs[] = {h->n_subap, h->star_is_lgs, h->layer_order, h->n_act, h->noise_variance, h->theta_x,
                     h->theta_y, h->star_height, h->layer_height, h->layer_extent, h->layer_strength, h->dm_height,
                     h->dm_extent, h->masks, h->mask_off, h->meas_off, h->wf_off, h->coeff_off, h->act_off,
-                    h->side, h->reg, h->precond, h->c, h->b, h->r, h->p, h->q, h->a_prev2, h->a_prev,
+                    h->side, h->reg, h->precond, h->dm_group, h->dm_tx, h->dm_ty, h->c, h->b, h->r, h->p, h->q, h->a_prev2, h->a_prev,
                     h->layer_work, h->wf_work, h->meas_work, h->b1, h->z, h->s, h->tmp};
     for (size_t i = 0; i < sizeof ptrs / sizeof ptrs[0]; ++i) free(ptrs[i]);
     free(h);

@@ -50,6 +50,16 @@ typedef struct {
     int fault_sh_adjoint;
     int loop_closed;
     double gain;
+    /* L != M extension (not in the reference; "fitting": "projection"): per DM a
+     * science direction, a layer-group bitmask (0 = default nearest-height
+     * grouping) and an extent (<= 0 = derived).  The DM shape is
+     * sum_{l in group} bilinear(phi_l; x + theta*h_l), x on the actuator grid,
+     * built from the reference's bilinear_sample (operators.hpp:123-127). */
+    int projection;
+    const double* dm_theta_x;
+    const double* dm_theta_y;
+    const int* dm_layer_mask;
+    const double* dm_extent_in;
 } orc_config;
 
 typedef struct orc orc_t;

@@ -77,6 +77,20 @@ def load_preset(path_or_dict) -> dict:
         g["theta_x"].append(float(tx))
         g["theta_y"].append(float(ty))
         g["star_height"].append(float(s["height"]) if lgs else math.inf)
+    # L != M projection-fitting extension (not in the reference)
+    g["projection"] = 1 if j.get("fitting", "identity") == "projection" else 0
+    g["dm_theta_x"], g["dm_theta_y"], g["dm_layer_mask"], g["dm_extent_in"] = [], [], [], []
+    for d in j["dms"]:
+        if "direction_rad" in d:
+            tx, ty = d["direction_rad"]
+        elif "direction_arcsec" in d:
+            tx, ty = (v * ARCSEC for v in d["direction_arcsec"])
+        else:
+            tx = ty = 0.0
+        g["dm_theta_x"].append(float(tx))
+        g["dm_theta_y"].append(float(ty))
+        g["dm_layer_mask"].append(sum(1 << int(l) for l in d.get("layers", [])))
+        g["dm_extent_in"].append(float(d.get("extent", 0.0)))
     sol = j["solver"]
     g.update(
         pcg_max_iter=int(sol["pcg_max_iter"]),
@@ -108,6 +122,8 @@ class _Cfg(C.Structure):
         ("precond_mode", C.c_int), ("precond_coarse_weight", C.c_double),
         ("precond_balance_exponent", C.c_double), ("dense_size_cap", C.c_longlong),
         ("fault_sh_adjoint", C.c_int), ("loop_closed", C.c_int), ("gain", C.c_double),
+        ("projection", C.c_int), ("dm_theta_x", _dp), ("dm_theta_y", _dp), ("dm_layer_mask", _ip),
+        ("dm_extent_in", _dp),
     ]
 
 
@@ -256,6 +272,8 @@ class Oracle(_Base):
             g["pcg_tolerance"], g["alpha"], g["wavelet_order"], g["outer_scale"], g["spectral_exponent"],
             g["precond_mode"], g["precond_coarse_weight"], g["precond_balance_exponent"], g["dense_size_cap"],
             g["fault_sh_adjoint"], g["loop_closed"], g["gain"],
+            g["projection"], arr("dm_theta_x", C.c_double), arr("dm_theta_y", C.c_double),
+            arr("dm_layer_mask", C.c_int), arr("dm_extent_in", C.c_double),
         )
         err = C.create_string_buffer(512)
         code = C.c_int(0)

@@ -177,6 +177,12 @@ int fewha_gpu_load_slopes(fewha_gpu_t h, const void* src, int on_device) {
 int fewha_gpu_step_device(fewha_gpu_t h, const void* d_slopes) { H_GUARD(h->eng->step_device(d_slopes)) }
 int fewha_gpu_sync(fewha_gpu_t h) { H_GUARD(h->eng->sync_check()) }
 int fewha_gpu_launches_per_step(fewha_gpu_t h) { return h ? h->eng->launches_per_step() : -1; }
+float fewha_gpu_debug_bench_dwt(fewha_gpu_t h, int variant, int inverse, int reps, int threads) {
+    float ms = -1.f;
+    if (!h) return ms;
+    guard(h->err, [&] { ms = h->eng->bench_dwt(variant, inverse, reps, threads); });
+    return ms;
+}
 int fewha_gpu_phase_stamps(fewha_gpu_t h, unsigned long long* out, long long n) {
     if (!h) return -1;
     int got = 0;

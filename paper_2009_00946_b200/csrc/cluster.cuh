@@ -85,6 +85,7 @@ __device__ __forceinline__ int ilog2(int v) { return 31 - __clz(v); }
 template <typename T, int FLEN, bool COL>
 __device__ __forceinline__ void analysis_lines(T* buf, int P, int s, int nlines, const GeoParams& gp) {
     constexpr int SEGM = SegOf<T>::value;
+    constexpr int WIN = 2 * SEGM + FLEN - 2;
     const int h = s >> 1, mask = s - 1;
     const int seg = h < SEGM ? h : SEGM;
     const int segs = h / seg;
@@ -97,15 +98,20 @@ __device__ __forceinline__ void analysis_lines(T* buf, int P, int s, int nlines,
         const int line = l0 + (tid & (lines - 1)), m0 = (tid >> lsh) * seg;
         T a[SEGM], d[SEGM];
         if (act) {
+            T win[WIN];  // sliding window: 2*seg+FLEN-2 reads for seg output pairs
+#pragma unroll
+            for (int q = 0; q < WIN; ++q) {
+                if (q >= 2 * seg + FLEN - 2) break;
+                win[q] = at<T, COL>(buf, P, line, (2 * m0 + q) & mask);
+            }
 #pragma unroll
             for (int e = 0; e < SEGM; ++e) {
                 if (e >= seg) break;
                 T sa = T(0), sd = T(0);
 #pragma unroll
                 for (int k = 0; k < FLEN; ++k) {
-                    const T v = at<T, COL>(buf, P, line, (2 * (m0 + e) + k) & mask);
-                    sa += Filt<T>::lo(gp, k) * v;
-                    sd += Filt<T>::hi(gp, k) * v;
+                    sa += Filt<T>::lo(gp, k) * win[2 * e + k];
+                    sd += Filt<T>::hi(gp, k) * win[2 * e + k];
                 }
                 a[e] = sa;
                 d[e] = sd;

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <climits>
 #include <cstdint>
 #include <cmath>
@@ -185,18 +186,39 @@ Plan build_plan(const Geometry& g, int elem_bytes) {
             pl.ti[static_cast<size_t>(gp.o_pd + (w * M + m) * 2 + 1)] = oy;
         }
     }
-    // fitting tables (reconstructor.hpp:294-302): DM m samples layer m
+    // fitting tables.  Reference L = M pairing (reconstructor.hpp:294-302): DM m
+    // samples layer m on its own extent -- identity copy when n_act = 2^J (-1).
+    // Projection fitting (L != M extension): DM m sums its layer group at the
+    // actuator positions shifted by theta_m * h_l.  Block: [cnt, (l, ox, oy) x cnt].
     for (int m = 0; m < M; ++m) {
         const auto& dm = g.dms[m];
-        const int side = g.layers[m].side();
-        if (dm.n_act == side) {
+        std::vector<int> group = g.projection ? dm.layers : std::vector<int>{m};
+        if (!g.projection && dm.n_act == g.layers[m].side()) {
             pl.ti[static_cast<size_t>(gp.o_fit + m)] = -1;
             continue;
         }
         const double da = dm.extent / (dm.n_act - 1);
-        std::vector<Stencil1> t(static_cast<size_t>(dm.n_act));
-        for (int j = 0; j < dm.n_act; ++j) t[j] = stencil1(side, dm.extent, -dm.extent / 2.0 + j * da);
-        pl.ti[static_cast<size_t>(gp.o_fit + m)] = push_table(pl, t);
+        std::vector<std::array<int, 3>> entries;
+        for (int l : group) {
+            const auto& lay = g.layers[static_cast<size_t>(l)];
+            const int side = lay.side();
+            // reference path: bilinear_sample(grid, dm.extent, ...) -- the DM extent is the layer's
+            const double e_grid = g.projection ? lay.extent : dm.extent;
+            std::vector<Stencil1> tx(static_cast<size_t>(dm.n_act)), ty(static_cast<size_t>(dm.n_act));
+            for (int j = 0; j < dm.n_act; ++j) {
+                const double p = -dm.extent / 2.0 + j * da;
+                tx[j] = stencil1(side, e_grid, g.projection ? p + dm.theta_x * lay.height : p);
+                ty[j] = stencil1(side, e_grid, g.projection ? p + dm.theta_y * lay.height : p);
+            }
+            const int ox = push_table(pl, tx);
+            const int oy = g.projection ? push_table(pl, ty) : ox;
+            entries.push_back({l, ox, oy});
+        }
+        const int off = static_cast<int>(pl.ti.size());
+        pl.ti.push_back(static_cast<int>(entries.size()));
+        for (const auto& en : entries) pl.ti.insert(pl.ti.end(), en.begin(), en.end());
+        pl.td.resize(pl.ti.size(), 0.0);
+        pl.ti[static_cast<size_t>(gp.o_fit + m)] = off;
     }
     // alpha * regularizer per (layer, scale) (operators.hpp:307-321)
     const double kappa0 = 2.0 * std::numbers::pi / g.outer_scale;
@@ -1033,7 +1055,7 @@ Engine::Engine(Geometry g, int precision, int batch, int device) : p_(std::make_
     {
         const char* env = std::getenv("FEWHA_PERSISTENT");
         // opt-in until its phases outrun the launch gaps they remove
-        const bool allow = batch == 1 && env && env[0] == '1';
+        const bool allow = batch == 1 && env && env[0] == '1' && !P.g.projection;
         int ok = 0;
         if (allow) {
             if (precision == 64) {
@@ -1239,6 +1261,42 @@ int Engine::profile_step(float* ms, int* kinds, int max) {
         ~Off() { s = -1; }
     } off{P.stamp_slot};
     return P.precision == 64 ? P.profile_frame<double>(ms, kinds, max) : P.profile_frame<float>(ms, kinds, max);
+}
+
+// Micro-benchmark of one layer transform kernel: single-CTA (variant 1, `threads`)
+// or cluster-distributed (variant 0).  Returns mean ms per launch over `reps`.
+float Engine::bench_dwt(int variant, int inverse, int reps, int threads) {
+    auto& P = *p_;
+    CK(cudaSetDevice(P.device));
+    float ms = 0.f;
+    auto run = [&](auto& w) {
+        using T = std::remove_pointer_t<decltype(w.in)>;
+        if (w.count < 1) w.alloc(P.gp, 1, P.fr, false);
+        Bufs<T> bf = w.bf;
+        auto once = [&] {
+            if (variant == 1) {
+#define FEWHA_DS(N) CK((launch_dwt_single<T, N>(P.gp, inverse ? w.in : bf.y, inverse ? bf.phi : w.out, inverse, 1, threads, P.stream)))
+                FEWHA_FLEN_SWITCH(P.flen, FEWHA_DS)
+#undef FEWHA_DS
+            } else {
+                Launch<T>::cl(P.flen, inverse != 0, P.gp, bf, kPlain, 0, 1, P.stream, 0);
+            }
+        };
+        for (int i = 0; i < 3; ++i) once();
+        cudaEvent_t a, b;
+        CK(cudaEventCreate(&a));
+        CK(cudaEventCreate(&b));
+        CK(cudaEventRecord(a, P.stream));
+        for (int i = 0; i < reps; ++i) once();
+        CK(cudaEventRecord(b, P.stream));
+        CK(cudaEventSynchronize(b));
+        CK(cudaEventElapsedTime(&ms, a, b));
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+    };
+    if (P.precision == 64) run(P.od);
+    else run(P.of);
+    return ms / reps;
 }
 
 void Engine::enable_stamps(bool on) {

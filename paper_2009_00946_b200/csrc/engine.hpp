@@ -44,6 +44,7 @@ public:
     int launches_per_step() const;
     int profile_step(float* ms, int* kinds, int max);
     void enable_stamps(bool on);
+    float bench_dwt(int variant, int inverse, int reps, int threads);
     int read_stamps(unsigned long long* out, size_t n);
     void device_buffers(void** slopes, void** coeffs, void** dm, double** rho, int** status, int** n_rho);
 

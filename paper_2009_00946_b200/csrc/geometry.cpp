@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <fstream>
+#include <limits>
 #include <numbers>
 #include <sstream>
 
@@ -112,10 +113,27 @@ Geometry from_json(const json& j) {
         l.extent = opt(jl, "extent", 0.0);
         g.layers.push_back(l);
     }
+    // Extension (not in the reference): "fitting": "projection" enables L != M with
+    // per-DM layer groups and science directions; absent, the reference's L = M
+    // identity pairing and its validation apply unchanged.
+    if (j.contains("fitting")) {
+        const auto f = j.at("fitting").get<std::string>();
+        if (f != "projection" && f != "identity") throw ConfigError("config: fitting must be 'identity' or 'projection'");
+        g.projection = f == "projection";
+    }
     for (const auto& jd : j.at("dms")) {
         Dm d;
         d.n_act = need<int>(jd, "n_act", "dms");
         d.height = need<double>(jd, "conjugation_height", "dms");
+        if (g.projection) {
+            if (jd.contains("direction_rad") || jd.contains("direction_arcsec"))
+                std::tie(d.theta_x, d.theta_y) = direction(jd, "dms");
+            if (jd.contains("layers")) d.layers = jd.at("layers").get<std::vector<int>>();
+            if (jd.contains("extent")) {
+                d.extent = jd.at("extent").get<double>();
+                d.extent_given = true;
+            }
+        }
         g.dms.push_back(d);
     }
     const json& sol = j.at("solver");
@@ -258,9 +276,15 @@ void validate(const Geometry& g) {
     if (g.stars.size() != g.wfs.size())
         fail("guide star count " + std::to_string(g.stars.size()) + " != wfs count " + std::to_string(g.wfs.size()));
     if (g.layers.empty()) fail("layer list is empty");
-    if (g.dms.size() != g.layers.size())
+    if (!g.projection && g.dms.size() != g.layers.size())
         fail("dm count " + std::to_string(g.dms.size()) + " != layer count " + std::to_string(g.layers.size()) +
              " (only the L = M identity-fitting mode is supported)");
+    if (g.projection) {
+        if (g.dms.empty()) fail("dm list is empty");
+        for (const auto& d : g.dms)
+            for (int l : d.layers)
+                if (l < 0 || l >= static_cast<int>(g.layers.size())) fail("dm layer index out of range");
+    }
     for (const auto& w : g.wfs) {
         if (w.n_subap < 1) fail("wfs n_subap must be >= 1");
         if (!(w.noise_variance > 0.0)) fail("wfs noise_variance must be > 0");
@@ -316,7 +340,37 @@ void finalize(Geometry& g) {
     validate(g);
     for (size_t l = 0; l < g.layers.size(); ++l)
         if (g.layers[l].extent <= 0.0) g.layers[l].extent = derived_extent(g, static_cast<int>(l));
-    for (size_t m = 0; m < g.dms.size(); ++m) g.dms[m].extent = g.layers[m].extent;  // geometry.hpp:374
+    if (!g.projection) {
+        for (size_t m = 0; m < g.dms.size(); ++m) g.dms[m].extent = g.layers[m].extent;  // geometry.hpp:374
+    } else {
+        bool any_explicit = false;
+        for (const auto& d : g.dms) any_explicit = any_explicit || !d.layers.empty();
+        if (!any_explicit) {  // default groups: each layer to the DM of nearest conjugation height
+            for (size_t l = 0; l < g.layers.size(); ++l) {
+                size_t best = 0;
+                for (size_t m = 1; m < g.dms.size(); ++m)
+                    if (std::abs(g.dms[m].height - g.layers[l].height) < std::abs(g.dms[best].height - g.layers[l].height))
+                        best = m;
+                g.dms[best].layers.push_back(static_cast<int>(l));
+            }
+        }
+        // DM extent: the largest centred square every sampled layer point stays inside
+        // (layer extent minus the direction offset theta*h_l on each side)
+        for (auto& d : g.dms) {
+            if (d.extent_given) continue;
+            double e = std::numeric_limits<double>::infinity();
+            for (int l : d.layers) {
+                const auto& lay = g.layers[static_cast<size_t>(l)];
+                const double shift = std::max(std::abs(d.theta_x), std::abs(d.theta_y)) * lay.height;
+                e = std::min(e, lay.extent - 2.0 * shift);
+            }
+            if (!(e > 0.0) || !std::isfinite(e)) {
+                // DM without layers: span the telescope aperture
+                e = g.diameter;
+            }
+            d.extent = e;
+        }
+    }
     for (size_t w = 0; w < g.wfs.size(); ++w) {
         const int n = g.wfs[w].n_subap;
         auto& mask = g.wfs[w].mask;

@@ -49,7 +49,12 @@ struct Layer {
 struct Dm {
     int n_act = 0;
     double height = 0;
-    double extent = 0;  // derived
+    double extent = 0;  // derived (or given, projection fitting only)
+    // projection fitting (L != M extension): the DM shape is
+    // sum_{l in layers} phi_l(x + theta * h_l) on the actuator grid
+    double theta_x = 0, theta_y = 0;
+    std::vector<int> layers;
+    bool extent_given = false;
 };
 
 struct Geometry {
@@ -68,6 +73,7 @@ struct Geometry {
     long long dense_cap = 20000;
     std::string fault;
     bool closed_loop = true;
+    bool projection = false;  // "fitting": "projection" (L != M allowed); false = reference L = M pairing
     double gain = 0.4;
     // evaluation / simulation blocks are validated but not used on the path
     int eval_n_per_side = 5;

@@ -506,15 +506,19 @@ __device__ void fit_actuator(const GeoParams& gp, const Bufs<T>& bf, int step, i
     while (m + 1 < gp.M && k >= gp.aoff[m + 1]) ++m;
     const int idx = k - gp.aoff[m], na = gp.nact[m];
     const int i = idx / na, j = idx % na;
-    const int side = gp.side[m];
-    const T* ph = bf.phi + static_cast<size_t>(b) * gp.n + gp.coff[m];
+    const T* phi_b = bf.phi + static_cast<size_t>(b) * gp.n;
     const int ofit = gp.ti[gp.o_fit + m];
     T at;
-    if (ofit < 0) {
-        at = ph[i * side + j];
-    } else {
+    if (ofit < 0) {  // identity pairing, n_act = 2^J (reconstructor.hpp:304-307)
+        at = phi_b[gp.coff[m] + i * gp.side[m] + j];
+    } else {  // bilinear resampling of each layer of the DM's group (ascending layer order)
         const T* tw = weights<T>(gp);
-        at = bilinear<T>(ph, side, gp.ti[ofit + i], gp.ti[ofit + j], tw[ofit + i], tw[ofit + j]);
+        const int cnt = gp.ti[ofit];
+        at = T(0);
+        for (int q = 0; q < cnt; ++q) {
+            const int l = gp.ti[ofit + 1 + 3 * q], ox = gp.ti[ofit + 2 + 3 * q], oy = gp.ti[ofit + 3 + 3 * q];
+            at += bilinear<T>(phi_b + gp.coff[l], gp.side[l], gp.ti[oy + i], gp.ti[ox + j], tw[oy + i], tw[ox + j]);
+        }
     }
     const size_t g = static_cast<size_t>(b) * gp.A + k;
     if (!step) {

@@ -25,4 +25,8 @@ cudaError_t launch_frame_persistent(const GeoParams& gp, const Bufs<T>& bf, unsi
 template <typename T, int FLEN>
 cudaError_t frame_persistent_fits(const GeoParams& gp, size_t smem, int* ok);
 
+template <typename T, int FLEN>
+cudaError_t launch_dwt_single(const GeoParams& gp, const T* in, T* out, int inverse, int count, int threads,
+                              cudaStream_t st);
+
 }  // namespace fewha_gpu

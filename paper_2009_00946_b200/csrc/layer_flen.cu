@@ -3,6 +3,7 @@
 
 #include "cluster.cuh"
 #include "frame.cuh"
+#include "single.cuh"
 #include "launch.hpp"
 
 #ifndef FEWHA_FLEN
@@ -107,13 +108,24 @@ cudaError_t frame_persistent_fits(const GeoParams& gp, size_t smem, int* ok) {
     }
 }
 
+template <typename T, int FLEN>
+cudaError_t launch_dwt_single(const GeoParams& gp, const T* in, T* out, int inverse, int count, int threads,
+                              cudaStream_t st) {
+    const size_t smem = static_cast<size_t>(gp.maxside) * (gp.maxside + 1) * sizeof(T);
+    cudaError_t e = opt_in_max(k_dwt_single<T, FLEN>, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    k_dwt_single<T, FLEN><<<dim3(gp.L, count), threads, smem, st>>>(gp, in, out, inverse);
+    return cudaGetLastError();
+}
+
 #define FEWHA_INST(T)                                                                                          \
     template cudaError_t launch_layer_cluster<T, FEWHA_FLEN>(bool, const GeoParams&, const Bufs<T>&, int, int, int, \
                                                              cudaStream_t, int, size_t);                        \
     template cudaError_t set_layer_cluster_attrs<T, FEWHA_FLEN>(size_t, size_t);                                   \
     template cudaError_t launch_frame_persistent<T, FEWHA_FLEN>(const GeoParams&, const Bufs<T>&, unsigned int*,   \
                                                                 cudaStream_t, size_t);                             \
-    template cudaError_t frame_persistent_fits<T, FEWHA_FLEN>(const GeoParams&, size_t, int*);
+    template cudaError_t frame_persistent_fits<T, FEWHA_FLEN>(const GeoParams&, size_t, int*);                     \
+    template cudaError_t launch_dwt_single<T, FEWHA_FLEN>(const GeoParams&, const T*, T*, int, int, int, cudaStream_t);
 FEWHA_INST(double)
 FEWHA_INST(float)
 

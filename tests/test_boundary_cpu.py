@@ -47,7 +47,8 @@ def test_library_is_sm100a():
     assert arches == {"100a"}, arches
 
 
-@pytest.mark.parametrize("name", ["mini", "small_mcao", "elt_mcao84", "maory9"])
+@pytest.mark.parametrize("name", ["mini", "small_mcao", "elt_mcao84", "maory9", "small_mcao_2dm", "elt_ltao84",
+                                  "elt_mcao84_3dm", "elt_moao84"])
 def test_host_geometry_matches_oracle_bitwise(name):
     dims, ext, dext, masks = fg.preset_info(preset(name + ".json"))
     o = Oracle(preset(name + ".json"))

@@ -285,3 +285,27 @@ def test_tolerance_exit_matches_oracle(tmp_path):
     # 25 CG iterations on the 128-unknown mini system amplify rounding ~1e11x
     assert rel_err(g.last_rho, rho_o) <= 1e-3
     assert g.last_rho[-1] <= 1e-8 * g.last_rho[0]
+
+
+# ---- L != M projection fitting (BASELINE configs 1-4) -------------------------
+
+@pytest.mark.parametrize("name", ["small_mcao_2dm", "elt_ltao84", "elt_mcao84_3dm", "elt_moao84"])
+def test_lnem_loop_vs_oracle(name, precision):
+    """Closed loop (open for MOAO) on the L != M presets: c, the DM commands and
+    rho against the oracle's projection fitting."""
+    o = Oracle(preset(name + ".json"))
+    o.build_preconditioner()
+    g = fg.Reconstructor(preset(name + ".json"), precision=precision)
+    x = np.random.default_rng(8).standard_normal(o.dims.n)
+    assert rel_err(g.fit(x), o.fit(x)) <= OP_TOL[precision]
+    layers = smooth_layers(o, 4)
+    tol = STEP_TOL[precision]
+    frames = 3 if name.startswith("elt") else 6
+    for k in range(frames):
+        st = o.get_state()
+        s = noisy_slopes(o, layers, 50 + k, st["a_prev2"] if o.g["loop_closed"] else None)
+        c_o, a_o, rho_o = o.step(s)
+        a_g = g.step(s)
+        assert rel_err(g.coeffs(), c_o) <= tol, ("c", k)
+        assert rel_err(a_g, a_o) <= tol, ("a", k)
+        assert rel_err(g.last_rho, rho_o) <= (tol if precision == 64 else 1e-3), ("rho", k)

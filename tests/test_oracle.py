@@ -176,3 +176,48 @@ def test_mini_noiseless_is_chaotic():
         errs.append(rel_err(c1, c2))
     assert max(errs[:2]) < 1e-10
     assert errs[2] > 1e-9 and errs[5] > 1e-4
+
+
+# ---- L != M projection fitting (extension; not in the reference) -------------
+
+LNEM = ["small_mcao_2dm", "elt_ltao84", "elt_mcao84_3dm", "elt_moao84"]
+
+
+def shadow_preset(name, tmp_path):
+    """The reference-runnable L = M shadow of an L != M preset: same layers,
+    one DM per layer, no projection fitting."""
+    import json
+    j = json.load(open(preset(name + ".json")))
+    j.pop("fitting", None)
+    j["dms"] = [{"n_act": 1 << l["grid_order"], "conjugation_height": l["height"]} for l in j["layers"]]
+    p = tmp_path / f"{name}_shadow.json"
+    p.write_text(json.dumps(j))
+    return str(p)
+
+
+@ref_only
+@pytest.mark.parametrize("name", ["small_mcao_2dm", "elt_ltao84"])
+def test_lnem_layer_part_pinned_to_reference_shadow(name, tmp_path):
+    """In open loop c, b, r and rho do not depend on the DM list
+    (reconstructor.hpp:317, :333), so the L != M oracle's layer solution must
+    equal the unmodified reference run on the L = M shadow, bitwise."""
+    o = Oracle(preset(name + ".json"), loop_mode="open")
+    r = RefOracle(shadow_preset(name, tmp_path), threads=1, loop_mode="open")
+    rng = np.random.default_rng(21)
+    for _ in range(2):
+        m = rng.standard_normal(o.dims.S)
+        co, _, ro = o.step(m)
+        cr, _, rr = r.step(m)
+        assert rel_err(co, cr) <= TOL and rel_err(ro, rr) <= TOL
+
+
+def test_lnem_projection_restates_reference_sampling():
+    """The projection fit of a one-layer group with theta = 0 and the layer's own
+    extent is the reference's identity/bilinear fitting (reconstructor.hpp:294-302)."""
+    import json
+    j = load_preset(preset("small_mcao.json"))
+    jp = dict(j, projection=1, dm_layer_mask=[1, 2, 4], dm_theta_x=[0.0] * 3, dm_theta_y=[0.0] * 3,
+              dm_extent_in=[0.0] * 3)
+    o_ref, o_proj = Oracle(j), Oracle(jp)
+    x = np.random.default_rng(2).standard_normal(o_ref.dims.n)
+    assert rel_err(o_proj.fit(x), o_ref.fit(x)) == 0.0

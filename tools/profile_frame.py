@@ -18,7 +18,7 @@ sys.path.insert(0, ROOT)
 import paper_2009_00946_b200 as fg  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--preset", default=os.path.join(ROOT, "presets", "elt_mcao84.json"))
+ap.add_argument("--preset", default=os.path.join(ROOT, "presets", "elt_mcao84_3dm.json"))
 ap.add_argument("--precision", type=int, default=64)
 ap.add_argument("--frames", type=int, default=2)
 ap.add_argument("--batch", type=int, default=1)
