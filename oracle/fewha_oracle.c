@@ -466,6 +466,12 @@ int orc_fit(orc_t* h, const double* c, double* a) {
                     double acc = 0.0;
                     for (int l = 0; l < h->cfg.n_layers; ++l) {
                         if (!(h->dm_group[m] >> l & 1)) continue;
+                        { /* projected point off this layer's grid: zero contribution */
+                            const double ex = h->layer_extent[l], sp = ex / (h->side[l] - 1);
+                            const double u = (px + h->dm_tx[m] * h->layer_height[l] + ex / 2.0) / sp;
+                            const double t = (py + h->dm_ty[m] * h->layer_height[l] + ex / 2.0) / sp;
+                            if (u < -1e-9 || u > h->side[l] - 1 + 1e-9 || t < -1e-9 || t > h->side[l] - 1 + 1e-9) continue;
+                        }
                         double v;
                         if (sample(h, h->layer_work + h->coeff_off[l], h->side[l], h->layer_extent[l],
                                    px + h->dm_tx[m] * h->layer_height[l], py + h->dm_ty[m] * h->layer_height[l], &v))
@@ -813,14 +819,14 @@ orc_t* orc_create(const orc_config* cfg, char* err, int errlen, int* code) {
                 h->dm_extent[m] = cfg->dm_extent_in[m];
                 continue;
             }
-            double e = INFINITY;
-            const double t = fabs(h->dm_tx[m]) > fabs(h->dm_ty[m]) ? fabs(h->dm_tx[m]) : fabs(h->dm_ty[m]);
-            for (int l = 0; l < L; ++l)
-                if (h->dm_group[m] >> l & 1) {
-                    const double v = h->layer_extent[l] - 2.0 * t * h->layer_height[l];
-                    if (v < e) e = v;
-                }
-            h->dm_extent[m] = (e > 0.0 && isfinite(e)) ? e : cfg->diameter;
+            /* the layer_extent rule (geometry.hpp:256-275) at the DM height, n_act nodes */
+            double side = 0.0;
+            for (int w = 0; w < cfg->n_wfs; ++w) {
+                const double s = footprint(h, w, h->dm_height[m]) * cfg->diameter +
+                                 2.0 * hypot(h->theta_x[w], h->theta_y[w]) * h->dm_height[m];
+                if (s > side) side = s;
+            }
+            h->dm_extent[m] = side + 2.0 * side / (h->n_act[m] - 1);
         }
     }
 

@@ -205,10 +205,18 @@ Plan build_plan(const Geometry& g, int elem_bytes) {
             // reference path: bilinear_sample(grid, dm.extent, ...) -- the DM extent is the layer's
             const double e_grid = g.projection ? lay.extent : dm.extent;
             std::vector<Stencil1> tx(static_cast<size_t>(dm.n_act)), ty(static_cast<size_t>(dm.n_act));
+            // projection: points off the layer grid contribute zero (index -1)
+            auto st = [&](double p) {
+                if (g.projection) {
+                    const double u = (p + e_grid / 2.0) / (e_grid / (side - 1));
+                    if (u < -1e-9 || u > side - 1 + 1e-9) return Stencil1{-1, 0.0};
+                }
+                return stencil1(side, e_grid, p);
+            };
             for (int j = 0; j < dm.n_act; ++j) {
                 const double p = -dm.extent / 2.0 + j * da;
-                tx[j] = stencil1(side, e_grid, g.projection ? p + dm.theta_x * lay.height : p);
-                ty[j] = stencil1(side, e_grid, g.projection ? p + dm.theta_y * lay.height : p);
+                tx[j] = st(g.projection ? p + dm.theta_x * lay.height : p);
+                ty[j] = st(g.projection ? p + dm.theta_y * lay.height : p);
             }
             const int ox = push_table(pl, tx);
             const int oy = g.projection ? push_table(pl, ty) : ox;

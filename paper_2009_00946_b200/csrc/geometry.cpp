@@ -354,21 +354,16 @@ void finalize(Geometry& g) {
                 g.dms[best].layers.push_back(static_cast<int>(l));
             }
         }
-        // DM extent: the largest centred square every sampled layer point stays inside
-        // (layer extent minus the direction offset theta*h_l on each side)
+        // DM extent: the reference's layer-extent rule (geometry.hpp:256-275) applied at
+        // the DM's conjugation height with its actuator count, so every WFS beam through
+        // the DM stays on its grid (add_dm_slopes).  Layers contribute zero to
+        // actuators whose projected point falls outside their grid.
         for (auto& d : g.dms) {
             if (d.extent_given) continue;
-            double e = std::numeric_limits<double>::infinity();
-            for (int l : d.layers) {
-                const auto& lay = g.layers[static_cast<size_t>(l)];
-                const double shift = std::max(std::abs(d.theta_x), std::abs(d.theta_y)) * lay.height;
-                e = std::min(e, lay.extent - 2.0 * shift);
-            }
-            if (!(e > 0.0) || !std::isfinite(e)) {
-                // DM without layers: span the telescope aperture
-                e = g.diameter;
-            }
-            d.extent = e;
+            double side = 0.0;
+            for (const auto& s : g.stars)
+                side = std::max(side, s.footprint(d.height) * g.diameter + 2.0 * std::hypot(s.theta_x, s.theta_y) * d.height);
+            d.extent = side + 2.0 * side / (d.n_act - 1);
         }
     }
     for (size_t w = 0; w < g.wfs.size(); ++w) {

@@ -517,7 +517,9 @@ __device__ void fit_actuator(const GeoParams& gp, const Bufs<T>& bf, int step, i
         at = T(0);
         for (int q = 0; q < cnt; ++q) {
             const int l = gp.ti[ofit + 1 + 3 * q], ox = gp.ti[ofit + 2 + 3 * q], oy = gp.ti[ofit + 3 + 3 * q];
-            at += bilinear<T>(phi_b + gp.coff[l], gp.side[l], gp.ti[oy + i], gp.ti[ox + j], tw[oy + i], tw[ox + j]);
+            const int ii = gp.ti[oy + i], jj = gp.ti[ox + j];
+            if (ii < 0 || jj < 0) continue;  // projected point off this layer's grid
+            at += bilinear<T>(phi_b + gp.coff[l], gp.side[l], ii, jj, tw[oy + i], tw[ox + j]);
         }
     }
     const size_t g = static_cast<size_t>(b) * gp.A + k;

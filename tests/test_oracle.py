@@ -216,8 +216,10 @@ def test_lnem_projection_restates_reference_sampling():
     extent is the reference's identity/bilinear fitting (reconstructor.hpp:294-302)."""
     import json
     j = load_preset(preset("small_mcao.json"))
+    o_ref = Oracle(j)
+    ext = [float(e) for e in o_ref.geometry()[0]]
     jp = dict(j, projection=1, dm_layer_mask=[1, 2, 4], dm_theta_x=[0.0] * 3, dm_theta_y=[0.0] * 3,
-              dm_extent_in=[0.0] * 3)
-    o_ref, o_proj = Oracle(j), Oracle(jp)
+              dm_extent_in=ext)
+    o_proj = Oracle(jp)
     x = np.random.default_rng(2).standard_normal(o_ref.dims.n)
     assert rel_err(o_proj.fit(x), o_ref.fit(x)) == 0.0
