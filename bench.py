@@ -251,16 +251,10 @@ def run_ours(args):
     import torch
     import paper_2009_00946_b200 as fg
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(local)
+    from paper_2009_00946_b200.replicas import init_replicas
+    rc = init_replicas()
+    world, rank, local = rc.world, rc.rank, rc.local_rank
+    torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     d = preset_dims(args.preset)
     b = args.precision // 8
@@ -268,7 +262,7 @@ def run_ours(args):
     rec = fg.Reconstructor(args.preset, precision=args.precision, batch=1, device=local)
     rec.build_preconditioner()
     F = 16
-    stream_host = slope_stream(rec, args.preset, F, seed=1 + rank)
+    stream_host = slope_stream(rec, args.preset, F, seed=rc.seed)
     stream = torch.from_numpy(stream_host).to(dev)
     st = torch.cuda.Stream(dev)  # a real stream: events, flushes and the graph all order on it
     torch.cuda.set_stream(st)
@@ -289,8 +283,7 @@ def run_ours(args):
     K = args.steps
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
-    if dist:
-        dist.barrier()
+    rc.barrier()
     torch.cuda.synchronize(dev)
     with Clocks(local) as clk:
         for k in range(K):
@@ -301,16 +294,12 @@ def run_ours(args):
             ends[k].record(st)
         torch.cuda.synchronize(dev)
     rec.sync()
-    if dist:
-        dist.barrier()
+    rc.barrier()
     ms = np.array([s.elapsed_time(e) for s, e in zip(starts, ends)])
     total_ms = float(ms.sum())
     p50, p99 = float(np.percentile(ms, 50)), float(np.percentile(ms, 99))
-    if dist:
-        t = torch.tensor([total_ms, p50, p99], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms, p50, p99 = (float(x) for x in t.tolist())
-    value = world * K / (total_ms / 1000.0)
+    total_ms, p50, p99 = rc.max_over_ranks([total_ms, p50, p99], device=dev)
+    value = rc.aggregate_throughput(K, total_ms)
 
     # ---- per-launch profile (events between launches on the launching stream) ----
     prof = {}
@@ -354,15 +343,12 @@ def run_ours(args):
         if k >= max(args.warmup, 3):
             e2e_ms.append((t1 - t0) * 1000.0)
     e2e_ms = np.array(e2e_ms)
-    e2e_val = world * 1000.0 / float(np.mean(e2e_ms))
-    if dist:
-        t = torch.tensor([float(np.mean(e2e_ms))], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_val = world * 1000.0 / float(t.item())
+    (e2e_mean,) = rc.max_over_ranks([float(np.mean(e2e_ms))], device=dev)
+    e2e_val = rc.aggregate_throughput(1, e2e_mean)
 
     # ---- batch-64 throughput (HBM-bound regime) ----------------
     batch_info = None
-    if args.batch64 and rank == 0 or (args.batch64 and dist):
+    if args.batch64:
         B = 64
         rb = fg.Reconstructor(args.preset, precision=args.precision, batch=B, device=local)
         rb.build_preconditioner()
@@ -434,8 +420,7 @@ def run_ours(args):
         if batch_info:
             line["batch64"] = batch_info
         print(json.dumps(line))
-    if dist:
-        dist.destroy_process_group()
+    rc.shutdown()
     return 0
 
 
