@@ -352,7 +352,7 @@ class Reconstructor:
             self._chk(-n)
         return out.reshape(32, 4096, 16)
 
-    KERNEL_KINDS = ("wfs_rhs", "adjoint", "fwd_rhs", "inv_pcg0", "inv_pcg", "wfs", "fwd_pcg", "inv_fit", "fit_control", "frame")
+    KERNEL_KINDS = ("wfs_rhs", "adjoint", "fwd_rhs", "inv_pcg0", "inv_pcg", "wfs", "fwd_pcg", "inv_fit", "fit_control", "gather")
 
     def profile_step(self):
         """One eager frame with events between launches: [(kind, ms), ...]."""

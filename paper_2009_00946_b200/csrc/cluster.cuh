@@ -1,26 +1,32 @@
 // Cluster-distributed layer kernels.
 //
-// One thread-block cluster per (layer, instance): rank r of the cluster owns
-// rows [r*R, r*R + R) of the 2^J x 2^J layer in its shared memory (pitch
-// side+1, odd, so row walks and column walks are bank-conflict free).  The
-// multilevel periodic Daubechies transform (wavelet.hpp:115-201) runs across
-// the cluster:
-//   * row passes touch only local rows;
-//   * column passes read remote rows through distributed shared memory
-//     (cooperative_groups map_shared_rank), stage results in registers across
-//     one cluster barrier and write local rows -- 2 cluster barriers per
-//     distributed level;
-//   * levels with s <= R live entirely in rank 0 and finish there.
-// Latency discipline: every global operand a kernel needs (PCG vectors of the
-// band, gather tables, psi blocks) is requested up front with cp.async into
-// shared memory, so each kernel pays one memory round trip per phase instead
-// of one per loop iteration.  The adjoint propagation sum_w P^T psi_w is
-// gathered straight into the band (separable, atomic-free, WFS ascending), so
-// the forward transform never round-trips its input through HBM.
+// One thread-block cluster of C CTAs per (layer, instance) runs the multilevel
+// periodic Daubechies transform (wavelet.hpp:115-201) with the ownership
+// layout of clayout.hpp: at level s rank q owns the filter positions
+// m in [q k, q k + k), k = s/(2C), so
+//   * its input rows are the approximation rows it produced itself one level
+//     finer (plus the row pass it already applied to them) -- column passes
+//     read local shared memory; only the FLEN-2 halo rows after its band
+//     (forward) or the FLEN/2-1 approximation rows before it (inverse) cross
+//     distributed shared memory;
+//   * one cluster barrier per level (ping-pong level buffers make the reads of
+//     level s and the writes of level s/2 (forward) / 2s (inverse) disjoint);
+//   * the coefficients it finalises (forward) / consumes (inverse) are a fixed
+//     per-rank "compact" set, which is also the set of coefficient-domain
+//     vector entries it updates in the fused PCG -- epilogues and updates are
+//     rank-local, and their operands are prefetched by TMA bulk copies at
+//     kernel start;
+//   * the T x T tail (levels below 2C) is finished by rank 0 (forward) or
+//     evaluated redundantly by every rank (inverse, so the first distributed
+//     level needs no barrier).
+// The adjoint propagation sum_w P^T psi_w is gathered straight into the
+// level-S band (separable, atomic-free, WFS ascending).
+// Determinism: every value has one producer and every reduction a fixed order.
 #pragma once
 
 #include <cooperative_groups.h>
 
+#include "clayout.hpp"
 #include "kernels.cuh"
 
 namespace fewha_gpu {
@@ -37,46 +43,17 @@ __device__ __forceinline__ void stamp(const GeoParams& gp, int k) {
     gp.stamps[blk * 16 + k] = t;
 }
 
-// ---- cp.async (LDGSTS) helpers ---------------------------------------------
-__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
-                 "l"(src));
-}
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
-                 "l"(src));
-}
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
-                 "l"(src));
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+// ---- cluster barrier (split arrive / wait) and DSMEM addressing ------------
+__device__ __forceinline__ void cl_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void cl_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void cl_sync() {
+    cl_arrive();
+    cl_wait();
 }
 template <typename T>
-__device__ __forceinline__ void cp_async_elem(T* dst, const T* src) {
-    if constexpr (sizeof(T) == 8) cp_async8(dst, src);
-    else cp_async4(dst, src);
+__device__ __forceinline__ T* rmt(T* p, int rank) {
+    return cg::this_cluster().map_shared_rank(p, static_cast<unsigned>(rank));
 }
-// contiguous bytes, cooperative over the CTA (sizes and addresses multiples of 4)
-__device__ __forceinline__ void cp_async_bytes(void* dst, const void* src, int nbytes) {
-    const int tid = threadIdx.x, nthr = blockDim.x;
-    auto* d = static_cast<unsigned char*>(dst);
-    const auto* s = static_cast<const unsigned char*>(src);
-    if (((reinterpret_cast<uintptr_t>(d) | reinterpret_cast<uintptr_t>(s) | static_cast<uintptr_t>(nbytes)) & 15) == 0) {
-        for (int o = tid * 16; o < nbytes; o += nthr * 16) cp_async16(d + o, s + o);
-    } else {
-        for (int o = tid * 4; o < nbytes; o += nthr * 4) cp_async4(d + o, s + o);
-    }
-}
-
-template <typename T>
-struct Band {
-    T* loc;            // this rank's band: R rows x P
-    T* rem[kMaxC];     // every rank's band (generic DSMEM addresses)
-    int R, P, rank, rsh;
-    __device__ __forceinline__ T* row(int i) const { return rem[i >> rsh] + (i & (R - 1)) * P; }
-};
 
 __device__ __forceinline__ int ilog2(int v) { return 31 - __clz(v); }
 
@@ -88,7 +65,7 @@ __device__ __forceinline__ void analysis_lines(T* buf, int P, int s, int nlines,
     constexpr int WIN = 2 * SEGM + FLEN - 2;
     const int h = s >> 1, mask = s - 1;
     const int seg = h < SEGM ? h : SEGM;
-    const int segs = h / seg;
+    const int segs = h >> ilog2(seg);
     const int nthr = blockDim.x, tid = threadIdx.x;
     int lines = nlines;
     while (lines * segs > nthr) lines >>= 1;
@@ -136,7 +113,7 @@ __device__ __forceinline__ void synthesis_lines(T* buf, int P, int s, int nlines
     constexpr int HF = FLEN / 2;
     const int h = s >> 1, hmask = h - 1;
     const int seg = h < SEGM ? h : SEGM;
-    const int segs = h / seg;
+    const int segs = h >> ilog2(seg);
     const int nthr = blockDim.x, tid = threadIdx.x;
     int lines = nlines;
     while (lines * segs > nthr) lines >>= 1;
@@ -173,343 +150,524 @@ __device__ __forceinline__ void synthesis_lines(T* buf, int P, int s, int nlines
     }
 }
 
-// --- distributed column passes (s >= 2R: s/R ranks active) -----------------
-// Forward: output row o of my band is approximation m = o (o < s/2) or detail
-// m = o - s/2; rows x[(2m+k) & (s-1)] come from any rank.  A thread walks SEG
-// consecutive output rows of one column with a sliding window of 2*SEG+FLEN-2
-// remote reads.
-template <typename T, int FLEN>
-__device__ __forceinline__ void fwd_columns_cluster(const Band<T>& bd, int s, const GeoParams& gp,
-                                                    cg::cluster_group& cl) {
-    constexpr int SEG = 8;
-    constexpr int WIN = 2 * SEG + FLEN - 2;
-    const int h = s >> 1, mask = s - 1;
-    const bool active = bd.rank < (s >> bd.rsh);
-    const int seg = bd.R < SEG ? bd.R : SEG;
-    const int segs = bd.R / seg;
-    const int items = segs * s;
-    const int ssh = ilog2(s);
-    const int tid = threadIdx.x, nthr = blockDim.x;
-    T out[2][SEG];
-    int jj[2], oo[2];
-    cl.sync();  // row pass results of every rank visible
-    if (s == gp.maxside) stamp(gp, 4);
-#pragma unroll
-    for (int rep = 0; rep < 2; ++rep) {
-        const int it = tid + rep * nthr;
-        jj[rep] = it & (s - 1);
-        oo[rep] = bd.rank * bd.R + (it >> ssh) * seg;
-        if (!active || it >= items) continue;
-        const int o0 = oo[rep];
-        const bool detail = o0 >= h;
-        const int m0 = detail ? o0 - h : o0;
-        const int j = jj[rep];
-        T win[WIN];
-#pragma unroll
-        for (int q = 0; q < WIN; ++q) {
-            if (q >= 2 * seg + FLEN - 2) break;
-            win[q] = bd.row((2 * m0 + q) & mask)[j];
-        }
-#pragma unroll
-        for (int e = 0; e < SEG; ++e) {
-            if (e >= seg) break;
-            T acc = T(0);
-#pragma unroll
-            for (int k = 0; k < FLEN; ++k)
-                acc += (detail ? Filt<T>::hi(gp, k) : Filt<T>::lo(gp, k)) * win[2 * e + k];
-            out[rep][e] = acc;
-        }
-    }
-    if (s == gp.maxside) stamp(gp, 5);
-    cl.sync();  // every rank done reading before anyone overwrites
-    if (s == gp.maxside) stamp(gp, 8);
-#pragma unroll
-    for (int rep = 0; rep < 2; ++rep) {
-        const int it = tid + rep * nthr;
-        if (!active || it >= items) continue;
-        const int lr = oo[rep] - bd.rank * bd.R;
-#pragma unroll
-        for (int e = 0; e < SEG; ++e) {
-            if (e >= seg) break;
-            bd.loc[(lr + e) * bd.P + jj[rep]] = out[rep][e];
-        }
-    }
-    __syncthreads();
+// ---------------------------------------------------------------------------
+// Per-CTA plan of one layer (clayout.hpp) and its compact sets.
+// ---------------------------------------------------------------------------
+constexpr int kMaxLev = 8;
+struct LPlan {
+    int S, C, lC, q, H, T, nlev, lsS;
+    const int* off;   // [nlev+1] compact level offsets (no halo); [nlev] = tail block
+    const int* offH;  // [nlev+1] the same with H halo rows
+};
+// Level offsets are computed once per CTA into shared memory (s_off: 2 x (kMaxLev+1));
+// the caller runs __syncthreads before the plan's offsets are used.
+__device__ __forceinline__ LPlan make_plan(int S, int C, int q, int H, int* s_off) {
+    LPlan p;
+    p.S = S;
+    p.C = C;
+    p.lC = ilog2(C);
+    p.q = q;
+    p.H = H;
+    p.T = clay::tail(S, C);
+    p.nlev = clay::nlev(S, C);
+    p.lsS = ilog2(S);
+    const int t = threadIdx.x;
+    if (t <= p.nlev) s_off[t] = clay::level_off(S, C, 0, t);
+    if (t >= 32 && t - 32 <= p.nlev) s_off[kMaxLev + 1 + t - 32] = clay::level_off(S, C, H, t - 32);
+    p.off = s_off;
+    p.offH = s_off + kMaxLev + 1;
+    return p;
 }
 
-// Inverse: output row t of my band from a-rows m and d-rows h+m, m = (t>>1)-kk.
-template <typename T, int FLEN>
-__device__ __forceinline__ void inv_columns_cluster(const Band<T>& bd, int s, const GeoParams& gp,
-                                                    cg::cluster_group& cl) {
-    constexpr int SEG = 4;  // output pairs per thread item
-    constexpr int HF = FLEN / 2;
-    const int h = s >> 1, hmask = h - 1;
-    const bool active = bd.rank < (s >> bd.rsh);
-    const int npairs = bd.R >> 1;
-    const int seg = npairs < SEG ? npairs : SEG;
-    const int segs = npairs / seg;
-    const int items = segs * s;
-    const int ssh = ilog2(s);
+// Visit every element rank q owns exactly once (thread-strided): f(o, zo, sc)
+// with o = compact index (= offset inside the rank's HBM block), zo = index in
+// the halo layout, sc = alpha-D scale index bit_width(max(row, col)).
+template <typename F>
+__device__ __forceinline__ void for_owned(const LPlan& p, F&& f) {
     const int tid = threadIdx.x, nthr = blockDim.x;
-    T wa[2][SEG + HF - 1], wd[2][SEG + HF - 1];
-    int jj[2], tt[2];
-    cl.sync();  // previous level complete on every rank
-#pragma unroll
-    for (int rep = 0; rep < 2; ++rep) {
-        const int it = tid + rep * nthr;
-        jj[rep] = it & (s - 1);
-        tt[rep] = bd.rank * bd.R + 2 * (it >> ssh) * seg;
-        if (!active || it >= items) continue;
-        const int m0 = tt[rep] >> 1;
-#pragma unroll
-        for (int i = 0; i < SEG + HF - 1; ++i) {
-            if (i >= seg + HF - 1) break;
-            const int m = (m0 - (HF - 1) + i) & hmask;
-            wa[rep][i] = bd.row(m)[jj[rep]];
-            wd[rep][i] = bd.row(h + m)[jj[rep]];
-        }
-    }
-    cl.sync();  // reads done before local rows are overwritten
-#pragma unroll
-    for (int rep = 0; rep < 2; ++rep) {
-        const int it = tid + rep * nthr;
-        if (!active || it >= items) continue;
-        const int lr = tt[rep] - bd.rank * bd.R;
-#pragma unroll
-        for (int u = 0; u < 2 * SEG; ++u) {
-            if (u >= 2 * seg) break;
-            T acc = T(0);
-#pragma unroll
-            for (int kk = 0; kk < HF; ++kk) {
-                const int k = (u & 1) + 2 * kk;
-                const int wi = (u >> 1) - kk + HF - 1;
-                acc += wa[rep][wi] * Filt<T>::lo(gp, k) + wd[rep][wi] * Filt<T>::hi(gp, k);
+    for (int lv = 0; lv < p.nlev; ++lv) {
+        const int s = p.S >> lv, h = s >> 1, k = h >> p.lC;
+        const int ls = ilog2(s), lh = ls - 1;
+        const int o = p.off[lv], oh = p.offH[lv];
+        const int nr = k + p.H;
+        const int na = k << lh, n = na + (k << ls);
+        for (int e = tid; e < n; e += nthr) {
+            int zo;
+            if (e < na) {
+                zo = oh + (((e >> lh) + p.H) << lh) + (e & (h - 1));
+            } else {
+                const int e2 = e - na;
+                zo = oh + (nr << lh) + (((e2 >> ls) + p.H) << ls) + (e2 & (s - 1));
             }
-            bd.loc[(lr + u) * bd.P + jj[rep]] = acc;
+            f(o + e, zo, ls);
         }
     }
-    __syncthreads();
+    if (p.q == 0) {
+        const int o = p.off[p.nlev], oh = p.offH[p.nlev];
+        const int T = p.T, lt = ilog2(T);
+        for (int e = tid; e < T * T; e += nthr)
+            f(o + e, oh + e, bit_width(static_cast<unsigned>(max(e >> lt, e & (T - 1)))));
+    }
 }
 
-// Full transforms over the cluster.  `side` = layer side (power of two).
-template <typename T, int FLEN>
-__device__ void cluster_dwt_forward(const Band<T>& bd, int side, const GeoParams& gp, cg::cluster_group& cl) {
-    int s = side;
-    for (; s >= 2 * bd.R; s >>= 1) {
-        if (bd.rank < (s >> bd.rsh)) analysis_lines<T, FLEN, false>(bd.loc, bd.P, s, bd.R, gp);
-        if (s == side) stamp(gp, 3);
-        fwd_columns_cluster<T, FLEN>(bd, s, gp, cl);
-        if (s == side) stamp(gp, 6);
+// Prefetch one contiguous block (count elements) into shared memory: a TMA bulk
+// copy on mbar issued by thread `issuer` when source, destination and size are
+// 16-byte aligned, a cooperative plain copy otherwise.  The caller runs
+// __syncthreads, thread 0 arrives on mbar and everyone waits on it.
+template <typename T>
+__device__ __forceinline__ void prefetch_block(const T* src, T* dst, int count, unsigned long long* mbar, int issuer) {
+    if (count <= 0) return;
+    const unsigned bytes = static_cast<unsigned>(count) * sizeof(T);
+    if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst) | bytes) & 15u) == 0) {
+        if (static_cast<int>(threadIdx.x) == issuer) bulk_g2s(dst, src, bytes, mbar);
+    } else {
+        for (int e = threadIdx.x; e < count; e += blockDim.x) dst[e] = src[e];
     }
+}
+
+// ---------------------------------------------------------------------------
+// Tail levels (T x T, T <= 8 at C = 8) as fused 2-D passes: one output per
+// thread, both filter directions at once, one CTA barrier per level.
+// Forward level s: out(i,j) = sum_t1 F1[t1] sum_t2 F2[t2] x[2m1+t1][2m2+t2]
+// (rows first, as wavelet.hpp:153-168), F = lo for the approximation half.
+// ---------------------------------------------------------------------------
+template <typename T, int FLEN>
+__device__ void tail_forward(const GeoParams& gp, const T* src, int ps, int Tt, T* b0, T* b1, T* f) {
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const T* cur = src;
+    int pc = ps;
+    T* nxt = b0;
+    for (int s = Tt; s >= 2; s >>= 1) {
+        const int h = s >> 1, ls = ilog2(s);
+        for (int e = tid; e < s * s; e += nthr) {
+            const int i = e >> ls, j = e & (s - 1);
+            const int m1 = i & (h - 1), m2 = j & (h - 1);
+            const bool a1 = i < h, a2 = j < h;
+            T acc = T(0);
+#pragma unroll
+            for (int t1 = 0; t1 < FLEN; ++t1) {
+                const T* row = cur + ((2 * m1 + t1) & (s - 1)) * pc;
+                T r = T(0);
+#pragma unroll
+                for (int t2 = 0; t2 < FLEN; ++t2)
+                    r += (a2 ? Filt<T>::lo(gp, t2) : Filt<T>::hi(gp, t2)) * row[(2 * m2 + t2) & (s - 1)];
+                acc += (a1 ? Filt<T>::lo(gp, t1) : Filt<T>::hi(gp, t1)) * r;
+            }
+            if (a1 && a2 && s > 2) nxt[i * (Tt + 1) + j] = acc;
+            else f[i * Tt + j] = acc;
+        }
+        __syncthreads();
+        cur = nxt;
+        pc = Tt + 1;
+        nxt = nxt == b0 ? b1 : b0;
+    }
+    if (Tt == 1 && tid == 0) f[0] = src[0];
+}
+
+// Inverse level s (columns first, then rows: wavelet.hpp:170-196):
+// out(2m1+u1, 2m2+u2) = sum_{kk2,b2} G_b2 sum_{kk1,b1} G_b1 X(b1 h + m1-kk1, b2 h + m2-kk2),
+// X = previous level output in the LL quadrant, the tail coefficients elsewhere.
+// Returns the buffer holding the T x T output (pitch T+1).
+template <typename T, int FLEN>
+__device__ T* tail_inverse(const GeoParams& gp, const T* zt, int Tt, T* b0, T* b1) {
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    constexpr int HF = FLEN / 2;
+    const T* cur = zt;  // LL source of level 2: the coarse coefficient itself
+    int pc = Tt;
+    T* nxt = b0;
+    for (int s = 2; s <= Tt; s <<= 1) {
+        const int h = s >> 1, ls = ilog2(s);
+        for (int e = tid; e < s * s; e += nthr) {
+            const int r = e >> ls, c = e & (s - 1);
+            const int m1 = r >> 1, u1 = r & 1, m2 = c >> 1, u2 = c & 1;
+            T acc = T(0);
+#pragma unroll
+            for (int kk2 = 0; kk2 < HF; ++kk2) {
+#pragma unroll
+                for (int b2 = 0; b2 < 2; ++b2) {
+                    const int cc = b2 * h + ((m2 - kk2) & (h - 1));
+                    T y = T(0);
+#pragma unroll
+                    for (int kk1 = 0; kk1 < HF; ++kk1) {
+                        const int k1 = u1 + 2 * kk1, ra = (m1 - kk1) & (h - 1);
+                        const T xa = (cc < h) ? cur[ra * pc + cc] : zt[ra * Tt + cc];
+                        const T xd = zt[(h + ra) * Tt + cc];
+                        y += xa * Filt<T>::lo(gp, k1) + xd * Filt<T>::hi(gp, k1);
+                    }
+                    const int k2 = u2 + 2 * kk2;
+                    acc += y * (b2 == 0 ? Filt<T>::lo(gp, k2) : Filt<T>::hi(gp, k2));
+                }
+            }
+            nxt[r * (Tt + 1) + c] = acc;
+        }
+        __syncthreads();
+        cur = nxt;
+        pc = Tt + 1;
+        nxt = nxt == b0 ? b1 : b0;
+    }
+    if (Tt == 1) {
+        if (tid == 0) b0[0] = zt[0];
+        __syncthreads();
+        return b0;
+    }
+    return const_cast<T*>(cur);
+}
+
+// ---------------------------------------------------------------------------
+// Forward transform over the cluster.  x0 holds this rank's level-S input
+// rows (band rows, pitch P, FLEN-2 spare rows for the halo); finals go to the
+// compact set f; tb (C x (C+1)) is rank 0's tail block.
+// ---------------------------------------------------------------------------
+template <typename T, int FLEN>
+__device__ void cdwt_forward(const GeoParams& gp, const LPlan& p, T* x0, T* x1, int P, T* f, T* tb, T* tb2) {
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const int S = p.S, C = p.C, q = p.q;
+    if (p.nlev == 0) {  // tail-only layer, whole on rank 0
+        if (q == 0) tail_forward<T, FLEN>(gp, x0, P, S, tb, tb2, f);
+        return;
+    }
+    analysis_lines<T, FLEN, false>(x0, P, S, S >> p.lC, gp);  // level-S row pass on the band rows
+    constexpr int HR = FLEN - 2;
+    constexpr int SEGM = SegOf<T>::value;
+    constexpr int WIN = 2 * SEGM + FLEN - 2;
+    T* cur = x0;
+    T* nxt = x1;
+    for (int lv = 0; lv < p.nlev; ++lv) {
+        const int s = S >> lv, h = s >> 1, k = h >> p.lC, rows = 2 * k;
+        const int ls = ilog2(s), lrows = ilog2(rows);
+        const bool last = lv == p.nlev - 1;
+        cl_sync();  // level-s input rows (row pass applied) of every rank are complete
+        if (lv == 0) stamp(gp, 3);
+        // the HR rows after mine (periodic) from their owners
+        for (int e = tid; e < HR * s; e += nthr) {
+            const int i = e >> ls, j = e & (s - 1);
+            const int gm = ((q + 1) * rows + i) & (s - 1);
+            const T* src = rmt(cur, gm >> lrows);
+            cur[(rows + i) * P + j] = src[(gm & (rows - 1)) * P + j];
+        }
+        __syncthreads();
+        if (lv == 0) stamp(gp, 4);
+        // column analysis of my k positions, every column: thread = (column, seg positions)
+        const int seg = k < SEGM ? k : SEGM;
+        const int items = (k >> ilog2(seg)) * s;
+        const int offA = p.off[lv], offD = offA + k * h;
+        T* tbq = last ? rmt(tb, 0) : nullptr;
+        for (int it = tid; it < items; it += nthr) {
+            const int j = it & (s - 1), i0 = (it >> ls) * seg;
+            T win[WIN];
+#pragma unroll
+            for (int t = 0; t < WIN; ++t) {
+                if (t >= 2 * seg + FLEN - 2) break;
+                win[t] = cur[(2 * i0 + t) * P + j];
+            }
+#pragma unroll
+            for (int e = 0; e < SEGM; ++e) {
+                if (e >= seg) break;
+                T a = T(0), d = T(0);
+#pragma unroll
+                for (int t = 0; t < FLEN; ++t) {
+                    a += Filt<T>::lo(gp, t) * win[2 * e + t];
+                    d += Filt<T>::hi(gp, t) * win[2 * e + t];
+                }
+                const int i = i0 + e;
+                if (j < h) {
+                    if (last) tbq[(q + i) * (C + 1) + j] = a;  // k == 1: tail row q
+                    else nxt[i * P + j] = a;
+                } else {
+                    f[offA + i * h + (j - h)] = a;
+                }
+                f[offD + i * s + j] = d;
+            }
+        }
+        __syncthreads();
+        if (lv == 0) stamp(gp, 5);
+        if (!last) analysis_lines<T, FLEN, false>(nxt, P, h, k, gp);  // row pass of level h
+        T* t_ = cur;
+        cur = nxt;
+        nxt = t_;
+    }
+    cl_sync();  // every rank's tail row is in rank 0's tb
     stamp(gp, 7);
-    if (bd.rank == 0) {
-        for (; s >= 2; s >>= 1) {
-            analysis_lines<T, FLEN, false>(bd.loc, bd.P, s, s, gp);
-            analysis_lines<T, FLEN, true>(bd.loc, bd.P, s, s, gp);
-        }
-    }
+    if (q == 0) tail_forward<T, FLEN>(gp, tb, C + 1, p.T, tb2, tb, f + p.off[p.nlev]);
 }
 
+// ---------------------------------------------------------------------------
+// Inverse transform over the cluster.  z: the input in the halo layout with
+// owned rows, halo rows and the tail block filled.  Returns the buffer holding
+// this rank's band rows of the nodal output (pitch *outP).  For layers with
+// distributed levels the caller must cl_wait() once before exiting (the
+// matching arrive follows this rank's last remote read).
+// ---------------------------------------------------------------------------
 template <typename T, int FLEN>
-__device__ void cluster_dwt_inverse(const Band<T>& bd, int side, const GeoParams& gp, cg::cluster_group& cl) {
-    const int local_top = side < bd.R ? side : bd.R;
-    if (bd.rank == 0) {
-        for (int s = 2; s <= local_top; s <<= 1) {
-            synthesis_lines<T, FLEN, true>(bd.loc, bd.P, s, s, gp);
-            synthesis_lines<T, FLEN, false>(bd.loc, bd.P, s, s, gp);
-        }
+__device__ T* cdwt_inverse(const GeoParams& gp, const LPlan& p, const T* z, T* x0, T* x1, T* aw, T* tb, T* tb2,
+                           int P, int* outP) {
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const int S = p.S, C = p.C, q = p.q, H = p.H;
+    constexpr int HF = FLEN / 2;
+    constexpr int SEGP = 4;  // output pairs per thread item
+    const int Tt = p.T;
+    // tail: T x T block (the whole layer when there are no distributed levels)
+    T* tl = tb;
+    if (p.nlev > 0 || q == 0) tl = tail_inverse<T, FLEN>(gp, z + p.offH[p.nlev], Tt, tb, tb2);
+    if (p.nlev == 0) {
+        *outP = Tt + 1;
+        return tl;
     }
     stamp(gp, 4);
-    for (int s = 2 * bd.R; s <= side; s <<= 1) {
-        inv_columns_cluster<T, FLEN>(bd, s, gp, cl);
-        if (bd.rank < (s >> bd.rsh)) synthesis_lines<T, FLEN, false>(bd.loc, bd.P, s, bd.R, gp);
+    T* prev = tl;
+    T* cur = x0;
+    T* other = x1;
+    for (int lv = p.nlev - 1; lv >= 0; --lv) {
+        const int s = S >> lv, h = s >> 1, k = h >> p.lC, m0 = q * k, nr = k + H;
+        const int ls = ilog2(s), lk = ilog2(k);
+        const bool first = lv == p.nlev - 1;
+        if (!first) cl_sync();  // the previous level's outputs of every rank are complete
+        const int oA = p.offH[lv], oD = oA + nr * h;
+        // approximation rows m = m0 - H + i: columns [0,h) from the previous level's
+        // output (own rows local, halo rows from their owners), [h,s) from z
+        for (int e = tid; e < nr * s; e += nthr) {
+            const int i = e >> ls, j = e & (s - 1);
+            T v;
+            if (j < h) {
+                const int mm = (m0 - H + i) & (h - 1);
+                if (first) {
+                    v = tl[mm * (C + 1) + j];
+                } else {
+                    const int own = mm >> lk;
+                    const T* src = own == q ? prev : rmt(prev, own);
+                    v = src[(mm & (k - 1)) * P + j];
+                }
+            } else {
+                v = z[oA + i * h + (j - h)];
+            }
+            aw[i * s + j] = v;
+        }
+        if (lv == 0) cl_arrive();  // my last remote read is done (caller waits before exit)
+        __syncthreads();
+        // column synthesis: output rows t in [0, 2k) of level s, every column
+        const int seg = k < SEGP ? k : SEGP;
+        const int items = (k >> ilog2(seg)) * s;
+        for (int it = tid; it < items; it += nthr) {
+            const int j = it & (s - 1), i0 = (it >> ls) * seg;
+            T wa[SEGP + HF - 1], wd[SEGP + HF - 1];
+#pragma unroll
+            for (int i = 0; i < SEGP + HF - 1; ++i) {
+                if (i >= seg + HF - 1) break;
+                wa[i] = aw[(i0 + i) * s + j];
+                wd[i] = z[oD + (i0 + i) * s + j];
+            }
+#pragma unroll
+            for (int u = 0; u < 2 * SEGP; ++u) {
+                if (u >= 2 * seg) break;
+                T acc = T(0);
+#pragma unroll
+                for (int kk = 0; kk < HF; ++kk) {
+                    const int kf = (u & 1) + 2 * kk;
+                    const int wi = (u >> 1) - kk + HF - 1;
+                    acc += wa[wi] * Filt<T>::lo(gp, kf) + wd[wi] * Filt<T>::hi(gp, kf);
+                }
+                cur[(2 * i0 + u) * P + j] = acc;
+            }
+        }
+        __syncthreads();
+        synthesis_lines<T, FLEN, false>(cur, P, s, 2 * k, gp);  // row synthesis of my output rows
+        prev = cur;
+        cur = other;
+        other = prev;
     }
-}
-
-template <typename T>
-__device__ __forceinline__ Band<T> make_band(T* loc, int side, cg::cluster_group& cl) {
-    Band<T> bd;
-    bd.loc = loc;
-    bd.R = side < 16 ? side : 16;
-    bd.rsh = ilog2(bd.R);
-    bd.P = side + 1;
-    bd.rank = static_cast<int>(cl.block_rank());
-    const int C = static_cast<int>(cl.num_blocks());
-    for (int r = 0; r < kMaxC; ++r) bd.rem[r] = r < C ? cl.map_shared_rank(loc, r) : loc;
-    return bd;
+    *outP = P;
+    return prev;
 }
 
 // ---------------------------------------------------------------------------
-// Band gather of sum_w P_{w,l}^T psi_w (operators.hpp:241-260, WFS ascending).
-// Per WFS, a host-built blob (GeoParams::gblob at o_gb) holds the padded
-// separable gather tables: column taps (int16 source column relative to the
-// WFS's first contributing column, weight) for every layer column and row taps
-// (int16 absolute aperture row, weight) for every layer row.  WFS are staged
-// in chunks that fit gp.chunk_bytes: descriptors first, then every psi block
-// and table with cp.async, one wait, one barrier.  Then per thread (layer
-// column J, a group of band rows): column contraction into a thread-private
-// smem column, row contraction into registers.
+// Adjoint propagation y_l = sum_w P_{w,l}^T psi_w (operators.hpp:241-260).
+// The bilinear stencil is separable (operators.hpp:208-210), so per WFS
+//   G(i, c)   = sum_q rw(i,q) psi(rs(i,q), c)      rows first, into shared G
+//   y(i, J)  += sum_{c: idx_c in {J-1, J}} w(c, J) G(i, c)   then columns
+// with w(c, J) = 1 - f_c (idx_c == J) or f_c (idx_c == J-1).  One CTA per
+// kGatherRows-row group of a layer (grid (kMaxGU, L, B): 144 CTAs at the ELT
+// scale).  Staging per chunk of WFS: the tables by one TMA bulk copy and each
+// WFS's psi rows [ilo, ihi) by one bulk copy each, issued by separate threads.
+// All WFS of a chunk are row-contracted in one pass, then column-contracted in
+// ascending WFS order into per-thread registers: one CTA barrier per chunk,
+// deterministic, atomic-free.
 // ---------------------------------------------------------------------------
-constexpr int kRowsPerThreadMax = 16;
-
-struct WDesc {
-    int ilo, ihi, jlo, jhi;  // psi source block of this band
-    int blob;                // byte offset of the (w,l) gather blob
-    int pad[3];
+// host-built staging descriptor of one (layer, row group, WFS) (engine.cu, o_gd)
+struct GDesc {
+    int ilo, ihi, jlo, jhi;  // psi source block of this row group
+    int src;                 // psi source element offset (woff + ilo * np)
+    int soff;                // psi stage byte offset inside its chunk
+    int toff, tb;            // table byte offset in gblob, table bytes
 };
 
-template <typename T, int KM>
-__device__ __forceinline__ void gather_contract(const T* blk, int nr, int nc, const short* cs, const T* cw,
-                                                const short* rs, const T* rw, int ilo, int J, int i0, int rows_pt,
-                                                T* hc, int nthr, int tid, T (&out)[kRowsPerThreadMax]) {
-    int c[KM];
-    T wx[KM];
-#pragma unroll
-    for (int q = 0; q < KM; ++q) {
-        c[q] = cs[J * KM + q];
-        wx[q] = cw[J * KM + q];
-    }
-    int ra = rs[i0 * KM] - ilo, rb = ra;
-#pragma unroll
-    for (int q = 0; q < KM; ++q) rb = max(rb, rs[(i0 + rows_pt - 1) * KM + q] - ilo);
-    ra = min(max(ra, 0), nr - 1);
-    rb = min(max(rb, ra), nr - 1);
-    for (int r = ra; r <= rb; ++r) {
-        const T* row = blk + r * nc;
-        T h = T(0);
-#pragma unroll
-        for (int q = 0; q < KM; ++q) h += wx[q] * row[c[q]];
-        hc[(r - ra) * nthr + tid] = h;
-    }
-#pragma unroll
-    for (int k = 0; k < kRowsPerThreadMax; ++k) {
-        if (k >= rows_pt) break;
-        const short* rr = rs + (i0 + k) * KM;
-        const T* ww = rw + (i0 + k) * KM;
-        T s = T(0);
-#pragma unroll
-        for (int q = 0; q < KM; ++q) s += ww[q] * hc[min(max(rr[q] - ilo - ra, 0), rb - ra) * nthr + tid];
-        out[k] += s;
-    }
-}
-
-// shared-memory layout of one staged WFS: [block nr*nc T][col src side*KM short]
-// [row src R*KM short][col w side*KM T][row w R*KM T], each 16-byte aligned
 __device__ __forceinline__ int align16(int v) { return (v + 15) & ~15; }
 
-// psi block staged as the contiguous full rows [ilo, ihi) of the WFS grid
-// (np columns), fetched from the 16-byte aligned address at or below its start.
+// Stage WFS [w0, w1) (warp 0 only): the tables by lane 31 (one contiguous copy),
+// psi blocks by lanes 0..n-1.  The caller __syncwarp()s and lane 0 arrives.
 template <typename T>
-__device__ __forceinline__ int staged_bytes(const WDesc& d, int side, int R, int KM, int np) {
-    return align16((d.ihi - d.ilo) * np * static_cast<int>(sizeof(T)) + 16) + align16(side * KM * 2) +
-           align16(R * KM * 2) + align16(side * KM * static_cast<int>(sizeof(T))) +
-           align16(R * KM * static_cast<int>(sizeof(T)));
+__device__ __forceinline__ void gather_issue(const GeoParams& gp, const T* psi_b, const GDesc* desc, int w0, int w1,
+                                             unsigned char* stage, unsigned long long* mbar, bool tables, bool psi) {
+    const int lane = threadIdx.x;
+    if (tables && lane == 31) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        const unsigned bytes = static_cast<unsigned>(desc[w1 - 1].toff + desc[w1 - 1].tb - desc[w0].toff);
+        bulk_g2s(stage, gp.gblob + desc[w0].toff, bytes, mbar);
+    }
+    if (psi && lane < w1 - w0) {
+        const int w = w0 + lane;
+        const GDesc d = desc[w];
+        const int nr = d.ihi - d.ilo, np = gp.ns[w] + 1;
+        if (nr > 0) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            const uintptr_t a = reinterpret_cast<uintptr_t>(psi_b + d.src);
+            const unsigned shift = static_cast<unsigned>(a & 15u);
+            bulk_g2s(stage + d.soff, reinterpret_cast<const void*>(a - shift),
+                     round16(shift + nr * np * static_cast<unsigned>(sizeof(T))), mbar);
+        }
+    }
 }
 
-template <typename T>
-__device__ void gather_band(const GeoParams& gp, const T* __restrict__ psi_b, int l, const Band<T>& bd, bool owner,
-                            T* hc, unsigned char* stage, WDesc* desc, Bulk& bulk) {
+// Contract the staged row group, chunk by chunk (chunk 0 already issued by the caller).
+template <typename T, int KM>
+__device__ void gather_group(const GeoParams& gp, const T* __restrict__ psi_b, int l, T* __restrict__ y, T* gbuf,
+                             unsigned char* stage, const GDesc* desc, unsigned long long* mbar) {
     const int side = gp.side[l];
+    const int R = side < kGatherRows ? side : kGatherRows;
     const int tid = threadIdx.x, nthr = blockDim.x;
-    const int KM = gp.gather_km;
-    const int groups = min(nthr / side, bd.R);  // threads per layer column
-    const int rows_pt = bd.R / groups;          // band rows per thread
-    const int J = tid & (side - 1), grp = tid >> ilog2(side);
+    const int lside = ilog2(side);
+    const int groups = min(nthr >> lside, R);  // threads per layer column
+    const int rows_pt = R / groups;            // group rows per thread
+    const int J = tid & (side - 1), grp = tid >> lside;
     const int i0 = grp * rows_pt;
-    const bool worker = owner && grp < groups;
-    T out[kRowsPerThreadMax];
+    const bool worker = grp < groups;
+    const int gst = kGatherRows * gp.bd_cols_max;  // G stride per WFS
+    const int o_rw = align16(R * KM * 2), o_f = o_rw + align16(R * KM * static_cast<int>(sizeof(T)));
+    const int o_idx = o_f + align16((side + 3) * 2);
+    T out[kGatherRows];
 #pragma unroll
-    for (int q = 0; q < kRowsPerThreadMax; ++q) out[q] = T(0);
-    // descriptors of every WFS for this (layer, rank), one parallel load
-    for (int w = tid; w < gp.W; w += nthr) {
-        const int* bs = gp.ti + gp.o_bs + ((w * gp.L + l) * kMaxC + bd.rank) * 4;
-        WDesc d;
-        d.ilo = bs[0];
-        d.ihi = bs[1];
-        d.jlo = bs[2];
-        d.jhi = bs[3];
-        d.blob = gp.ti[gp.o_gb + w * gp.L + l];
-        desc[w] = d;
-    }
-    __syncthreads();
-    stamp(gp, 12);
-    const unsigned char* blob = gp.gblob;
-    int w0 = 0;
-    while (w0 < gp.W) {
-        int w1 = w0, used = 0;
-        while (w1 < gp.W) {
-            const int need = staged_bytes<T>(desc[w1], side, bd.R, KM, gp.ns[w1] + 1);
-            if (w1 > w0 && used + need > gp.chunk_bytes) break;
-            used += need;
-            ++w1;
+    for (int k = 0; k < kGatherRows; ++k) out[k] = T(0);
+    for (int k = 0; k < gp.nchunk; ++k) {
+        const int w0 = gp.gchunk[k], w1 = gp.gchunk[k + 1];
+        if (k > 0 && tid < 32) {
+            gather_issue<T>(gp, psi_b, desc, w0, w1, stage, mbar, true, true);
+            __syncwarp();
+            if (tid == 0) mbar_arrive(mbar);
         }
-        // ---- stage the chunk: thread 0 issues TMA bulk copies, everyone waits ----
-        if (tid == 0) {
-            bulk.begin();
-            int off = 0;
-            for (int w = w0; w < w1; ++w) {
-                const WDesc d = desc[w];
-                const int nr = d.ihi - d.ilo, np = gp.ns[w] + 1;
-                unsigned char* p = stage + off;
-                off += staged_bytes<T>(d, side, bd.R, KM, np);
-                if (nr <= 0) continue;
-                const T* src = psi_b + gp.woff[w] + d.ilo * np;
-                const uintptr_t a = reinterpret_cast<uintptr_t>(src);
-                const unsigned shift = static_cast<unsigned>(a & 15u);
-                bulk.copy(p, reinterpret_cast<const void*>(a - shift), shift + nr * np * static_cast<unsigned>(sizeof(T)));
-                p += align16(nr * np * static_cast<int>(sizeof(T)) + 16);
-                const unsigned char* g = blob + d.blob;  // [col src][row src][col w][row w]
-                const int cs_b = side * KM * 2, cw_b = side * KM * static_cast<int>(sizeof(T));
-                const int g_rs = align16(cs_b), g_cw = g_rs + align16(cs_b), g_rw = g_cw + align16(cw_b);
-                const int r0 = bd.rank * bd.R;
-                bulk.copy(p, g, cs_b);
-                p += align16(cs_b);
-                bulk.copy(p, g + g_rs + r0 * KM * 2, bd.R * KM * 2);
-                p += align16(bd.R * KM * 2);
-                bulk.copy(p, g + g_cw, cw_b);
-                p += align16(cw_b);
-                bulk.copy(p, g + g_rw + r0 * KM * static_cast<int>(sizeof(T)), bd.R * KM * static_cast<int>(sizeof(T)));
-            }
-            bulk.commit();
-        }
-        stamp(gp, 13);
-        bulk.wait();
+        mbar_wait(mbar, static_cast<unsigned>(k & 1));
         stamp(gp, 1);
-        // ---- contract ----
+        const int t0 = desc[w0].toff;
+        // ---- rows: G_w(i, c) for every WFS of the chunk, one pass ----
+        for (int w = w0; w < w1; ++w) {
+            const GDesc d = desc[w];
+            const int nr = d.ihi - d.ilo, np = gp.ns[w] + 1, nc = d.jhi - d.jlo;
+            if (nr <= 0) continue;
+            const unsigned char* tp = stage + (d.toff - t0);
+            const unsigned shift = static_cast<unsigned>(reinterpret_cast<uintptr_t>(psi_b + d.src) & 15u);
+            const T* __restrict__ blk = reinterpret_cast<const T*>(stage + d.soff + shift) + d.jlo;  // blk[r*np + c]
+            const short* __restrict__ rs = reinterpret_cast<const short*>(tp);
+            const T* __restrict__ rw = reinterpret_cast<const T*>(tp + o_rw);
+            T* __restrict__ G = gbuf + (w - w0) * gst;
+            const int lc = 32 - __clz(nc - 1);  // columns padded to a power of two per row
+            const int cp = 1 << lc;
+            for (int e = tid; e < R << lc; e += nthr) {
+                const int i = e >> lc, c = e & (cp - 1);
+                if (c >= nc) continue;
+                T g = T(0);
+#pragma unroll
+                for (int q = 0; q < KM; ++q) g += rw[i * KM + q] * blk[rs[i * KM + q] * np + c];
+                G[i * nc + c] = g;
+            }
+        }
+        __syncthreads();
+        // ---- columns, WFS ascending ----
         if (worker) {
-            int off = 0;
             for (int w = w0; w < w1; ++w) {
-                const WDesc d = desc[w];
-                const int nr = d.ihi - d.ilo, np = gp.ns[w] + 1;
-                const unsigned char* p = stage + off;
-                off += staged_bytes<T>(d, side, bd.R, KM, np);
+                const GDesc d = desc[w];
+                const int nr = d.ihi - d.ilo, nc = d.jhi - d.jlo;
                 if (nr <= 0) continue;
-                const unsigned shift =
-                    static_cast<unsigned>(reinterpret_cast<uintptr_t>(psi_b + gp.woff[w] + d.ilo * np) & 15u);
-                const T* blk = reinterpret_cast<const T*>(p + shift) + d.jlo;  // (r, c) at blk[r*np + c]
-                p += align16(nr * np * static_cast<int>(sizeof(T)) + 16);
-                const short* cs = reinterpret_cast<const short*>(p);
-                p += align16(side * KM * 2);
-                const short* rs = reinterpret_cast<const short*>(p);
-                p += align16(bd.R * KM * 2);
-                const T* cw = reinterpret_cast<const T*>(p);
-                p += align16(side * KM * static_cast<int>(sizeof(T)));
-                const T* rw = reinterpret_cast<const T*>(p);
-                if (KM == 2) gather_contract<T, 2>(blk, nr, np, cs, cw, rs, rw, d.ilo, J, i0, rows_pt, hc, nthr, tid, out);
-                else if (KM == 3) gather_contract<T, 3>(blk, nr, np, cs, cw, rs, rw, d.ilo, J, i0, rows_pt, hc, nthr, tid, out);
-                else gather_contract<T, 4>(blk, nr, np, cs, cw, rs, rw, d.ilo, J, i0, rows_pt, hc, nthr, tid, out);
+                const unsigned char* tp = stage + (d.toff - t0);
+                const short* first = reinterpret_cast<const short*>(tp + o_f);
+                const short* cidx = reinterpret_cast<const short*>(tp + o_idx);
+                const T* cfr = reinterpret_cast<const T*>(tp + o_idx + align16(nc * 2));
+                const T* G = gbuf + (w - w0) * gst;
+                const int c0 = first[J], c1 = first[J + 2];
+                T wt[KM];
+                int cc[KM];
+#pragma unroll
+                for (int q = 0; q < KM; ++q) {
+                    const int c = min(c0 + q, nc - 1);
+                    const T fr = cfr[c];
+                    wt[q] = c0 + q < c1 ? (cidx[c] == J ? T(1) - fr : fr) : T(0);
+                    cc[q] = c;
+                }
+#pragma unroll
+                for (int k2 = 0; k2 < kGatherRows; ++k2) {
+                    if (k2 >= rows_pt) break;
+                    const T* g = G + (i0 + k2) * nc;
+                    T s = T(0);
+#pragma unroll
+                    for (int q = 0; q < KM; ++q) s += wt[q] * g[cc[q]];
+                    out[k2] += s;
+                }
             }
         }
         __syncthreads();  // chunk consumed before the next one is staged
-        w0 = w1;
     }
     if (worker) {
 #pragma unroll
-        for (int k = 0; k < kRowsPerThreadMax; ++k) {
+        for (int k = 0; k < kGatherRows; ++k) {
             if (k >= rows_pt) break;
-            bd.loc[(i0 + k) * bd.P + J] = out[k];
+            y[(i0 + k) * side + J] = out[k];
         }
     }
+}
+
+// grid (kMaxGU, L, B): one CTA per kGatherRows-row group of a layer; y nodal, row-major.
+// Descriptors and chunk 0's tables are requested before the programmatic-launch
+// wait (they are constant), the psi blocks after it.
+template <typename T>
+__global__ void __launch_bounds__(256, 2) k_gather(const GeoParams gp, const Bufs<T> bf) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ GDesc s_desc[kMaxW];
+    __shared__ unsigned long long s_mbar;
+    const int u = blockIdx.x, l = blockIdx.y, b = blockIdx.z;
+    const int side = gp.side[l];
+    const int R = side < kGatherRows ? side : kGatherRows;
+    if (u * R >= side) return;
+    const int tid = threadIdx.x;
+    stamp(gp, 0);
+    T* gbuf = reinterpret_cast<T*>(smem_raw);
+    unsigned char* stage = smem_raw + align16(gp.gbuf_bytes);
+    const T* psi = bf.psi + static_cast<size_t>(b) * gp.Nw;
+    if (tid < 32) {
+        if (tid < gp.W) {
+            const int4* d = reinterpret_cast<const int4*>(gp.ti + gp.o_gd + ((l * kMaxGU + u) * kMaxW + tid) * 8);
+            const int4 a = d[0], c = d[1];
+            s_desc[tid] = GDesc{a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
+        }
+        if (tid == 0) {
+            mbar_init(&s_mbar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        }
+        __syncwarp();
+        gather_issue<T>(gp, psi, s_desc, gp.gchunk[0], gp.gchunk[1], stage, &s_mbar, true, false);
+    }
+    pdl_wait();  // psi of the predecessor is complete
+    if (tid < 32) {
+        gather_issue<T>(gp, psi, s_desc, gp.gchunk[0], gp.gchunk[1], stage, &s_mbar, false, true);
+        __syncwarp();
+        if (tid == 0) mbar_arrive(&s_mbar);
+    }
+    __syncthreads();  // descriptors visible
+    stamp(gp, 12);
+    T* y = bf.y + static_cast<size_t>(b) * gp.n + gp.coff[l] + static_cast<size_t>(u) * R * side;
+    switch (gp.gather_km) {
+        case 1: gather_group<T, 1>(gp, psi, l, y, gbuf, stage, s_desc, &s_mbar); break;
+        case 2: gather_group<T, 2>(gp, psi, l, y, gbuf, stage, s_desc, &s_mbar); break;
+        case 3: gather_group<T, 3>(gp, psi, l, y, gbuf, stage, s_desc, &s_mbar); break;
+        default: gather_group<T, 4>(gp, psi, l, y, gbuf, stage, s_desc, &s_mbar); break;
+    }
+    stamp(gp, 2);
 }
 
 // Deterministic sum of the dot partials of one iteration by warp 0: fixed
@@ -532,70 +690,77 @@ __device__ __forceinline__ void warp_dot_sums(const double* rho_part, const doub
 }
 
 // ---------------------------------------------------------------------------
-// Phase A: grid (C, L, B), cluster (C,1,1); rank r owns band rows.
+// Inverse kernel: grid (C, L, B), cluster (C,1,1).
 //   kPlain: phi = W^-1 in;  kPcg: [update it-1] z = r/J, rho partial, phi = W^-1 z;
 //   kFit: [final update] phi = W^-1 c
-// Shared memory: band | prefetched band slices of r, 1/J, p, q, c, Mz.
+// Every rank prefetches its compact set of the operands, applies the fused
+// update there (pcg.hpp:101-104) and forms z; the halo rows and the tail of z
+// come from their owners after one cluster barrier.
 // ---------------------------------------------------------------------------
 template <typename T, int FLEN>
-__device__ __forceinline__ void inv_phase(const GeoParams& gp, const Bufs<T>& bf, int mode, int it, unsigned char* smem_raw, int l,
-                          int b, cg::cluster_group& cl) {
+__device__ __forceinline__ void inv_phase(const GeoParams& gp, const Bufs<T>& bf, int mode, int it,
+                                          unsigned char* smem_raw, int l, int b, int q, int C) {
     __shared__ double s_red[32];
     __shared__ double s_beta, s_alpha;
     __shared__ int s_apply;
-    const int side = gp.side[l];
-    const int lsd = ilog2(side);
-    Band<T> bd = make_band<T>(reinterpret_cast<T*>(smem_raw), side, cl);
-    const int C = static_cast<int>(cl.num_blocks());
-    const bool owner = (bd.rank << bd.rsh) < side;  // holds rows of this layer
-    const int r0 = bd.rank * bd.R;
-    const int ne = owner ? bd.R * side : 0;
-    const size_t base = static_cast<size_t>(b) * gp.n + gp.coff[l] + static_cast<size_t>(r0) * side;
-    const size_t jbase = gp.coff[l] + static_cast<size_t>(r0) * side;
-    const int nthr = blockDim.x, tid = threadIdx.x;
+    __shared__ unsigned long long s_mbar;
+    const int S = gp.side[l];
+    constexpr int H = FLEN / 2 - 1;
+    __shared__ int s_off[2 * (kMaxLev + 1)];
+    const LPlan p = make_plan(S, C, q, H, s_off);
+    const clay::InvSmem sm = clay::inv_smem(gp.maxside, C, FLEN, static_cast<int>(sizeof(T)));
+    const int P = gp.maxside + 1;
+    T* v[6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) v[i] = reinterpret_cast<T*>(smem_raw + sm.v + i * sm.vstride);
+    T *sr = v[0], *sj = v[1], *sp = v[2], *sq = v[3], *sc = v[4], *sm_ = v[5];
+    T* z = reinterpret_cast<T*>(smem_raw + sm.z);
+    T* x0 = reinterpret_cast<T*>(smem_raw + sm.x0);
+    T* x1 = reinterpret_cast<T*>(smem_raw + sm.x1);
+    T* aw = reinterpret_cast<T*>(smem_raw + sm.aw);
+    T* tb = reinterpret_cast<T*>(smem_raw + sm.tb);
+    T* tb2 = reinterpret_cast<T*>(smem_raw + sm.tb2);
+    const size_t lbase = static_cast<size_t>(b) * gp.n + gp.coff[l];
+    const int roff = clay::rank_off(S, C, q), cnt = clay::owned_count(S, C, q);
+    const size_t vbase = lbase + roff;  // this rank's block of every coefficient-domain vector
+    const int tid = threadIdx.x;
     const int slots = gp.L * C;  // dot partial slots per iteration
-    stamp(gp, 0);
-    // prefetch region after the band (16-byte aligned)
-    T* pre = reinterpret_cast<T*>(smem_raw + align16(bd.R * bd.P * static_cast<int>(sizeof(T))));
-    const int nb = ne * static_cast<int>(sizeof(T));
-    T *sr = pre, *sj = pre + ne, *sp = pre + 2 * ne, *sq = pre + 3 * ne, *sc = pre + 4 * ne, *sm = pre + 5 * ne;
     const int upd = mode == kFit ? gp.iters : it;
     const bool may_update = mode != kPlain && upd > 0;
-    __shared__ unsigned long long s_mbar;
-    Bulk bulk{&s_mbar, 0};
-    bulk.init();
-    if (tid == 0) {  // band slices by TMA bulk copy (16 KiB each at J=7 fp64)
-        bulk.begin();
-        if (nb > 0 && mode != kPlain) bulk.copy(sj, bf.jinv + jbase, nb);  // constant: before the wait
-    }
-    pdl_wait();  // the predecessor's outputs (r, c, p, q, Mz, dot partials) are complete
+    stamp(gp, 0);
     if (tid == 0) {
-        if (nb > 0) {
-            if (mode == kPlain) {
-                bulk.copy(sr, bf.in + base, nb);
-            } else {
-                bulk.copy(sr, bf.r + base, nb);
-                bulk.copy(sc, bf.c + base, nb);
-                if (may_update) {
-                    bulk.copy(sp, bf.p + base, nb);
-                    bulk.copy(sq, bf.q + base, nb);
-                    bulk.copy(sm, bf.mz + base, nb);
-                }
-            }
-        }
-        bulk.commit();
+        mbar_init(&s_mbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
+    __syncthreads();
+    prefetch_block(bf.jinv + gp.coff[l] + roff, sj, mode == kPlain ? 0 : cnt, &s_mbar, 0);  // constant
+    Carry cin{};
+    const int ci = b * (gp.iters + 1) + upd - 1;
+    if (may_update && tid == 0) cin = bf.carry[ci];
+    pdl_wait();  // the predecessor's outputs (r, c, p, q, Mz, dot partials) are complete
+    // thread 0 issues every block and arrives at once (misaligned blocks: cooperative copies)
+    if (mode == kPlain) {
+        prefetch_block(bf.in + vbase, sr, cnt, &s_mbar, 0);
+    } else {
+        prefetch_block(bf.r + vbase, sr, cnt, &s_mbar, 0);
+        prefetch_block(bf.c + vbase, sc, cnt, &s_mbar, 0);
+        if (may_update) {
+            prefetch_block(bf.p + vbase, sp, cnt, &s_mbar, 0);
+            prefetch_block(bf.q + vbase, sq, cnt, &s_mbar, 0);
+            prefetch_block(bf.mz + vbase, sm_, cnt, &s_mbar, 0);
+        }
+    }
+    if (tid == 0) mbar_arrive(&s_mbar);
     if (mode != kPlain && tid < 32) {
         // scalar recurrences of the iteration whose dots are complete (warp 0)
         ScalarStep st{};
         if (upd > 0) {
             double rho = 0.0, mu = 0.0;
-            const int ci = b * (gp.iters + 1) + upd - 1;
             const size_t pi = (static_cast<size_t>(b) * gp.iters + (upd - 1)) * slots;
             warp_dot_sums(bf.rho_part + pi, bf.mu_part + pi, slots, rho, mu);
             if (tid == 0) {
-                st = pcg_scalar_from_sums(gp, bf.carry[ci], rho, mu, upd - 1 == 0);
-                if (l == 0 && bd.rank == 0) {
+                st = pcg_scalar_from_sums(gp, cin, rho, mu, upd - 1 == 0);
+                if (l == 0 && q == 0) {
                     Carry o = st.out;
                     if (st.log) bf.rho_log[static_cast<size_t>(b) * gp.iters + o.nlog++] = st.logval;
                     bf.carry[ci + 1] = o;
@@ -608,53 +773,85 @@ __device__ __forceinline__ void inv_phase(const GeoParams& gp, const Bufs<T>& bf
             s_alpha = st.alpha;
         }
     }
-    bulk.wait();
-    __syncthreads();
+    __syncthreads();  // scalars published, cooperative copies visible
+    mbar_wait(&s_mbar, 0);
     stamp(gp, 1);
+    double racc = 0.0;
     if (mode == kPlain) {
-        for (int e = tid; e < ne; e += nthr) bd.loc[(e >> lsd) * bd.P + (e & (side - 1))] = sr[e];
+        for_owned(p, [&](int o, int zo, int) { z[zo] = sr[o]; });
     } else {
         const bool apply = s_apply != 0;
         const T beta = static_cast<T>(s_beta), alpha = static_cast<T>(s_alpha);
-        double racc = 0.0;
-        T* __restrict__ pr = bf.r + base;
-        T* __restrict__ pp = bf.p + base;
-        T* __restrict__ pq = bf.q + base;
-        T* __restrict__ pc = bf.c + base;
-        for (int e = tid; e < ne; e += nthr) {
-            T rr = sr[e], cc = sc[e];
-            const T ji = sj[e];
+        T* __restrict__ pr = bf.r + vbase;
+        T* __restrict__ pp = bf.p + vbase;
+        T* __restrict__ pq = bf.q + vbase;
+        T* __restrict__ pc = bf.c + vbase;
+        for_owned(p, [&](int o, int zo, int) {
+            T rr = sr[o], cc = sc[o];
+            const T ji = sj[o];
             if (apply) {  // pcg.hpp:101-104, z_old = r * (1/J)
-                const T pn = rr * ji + beta * sp[e];
-                const T qn = sm[e] + beta * sq[e];
+                const T pn = rr * ji + beta * sp[o];
+                const T qn = sm_[o] + beta * sq[o];
                 cc = cc + alpha * pn;
                 rr = rr - alpha * qn;
-                pp[e] = pn;
-                pq[e] = qn;
-                pc[e] = cc;
-                pr[e] = rr;
+                pp[o] = pn;
+                pq[o] = qn;
+                pc[o] = cc;
+                pr[o] = rr;
             }
-            T v;
+            T vz;
             if (mode == kPcg) {
-                v = rr * ji;
-                racc += static_cast<double>(rr) * static_cast<double>(v);
+                vz = rr * ji;
+                racc += static_cast<double>(rr) * static_cast<double>(vz);
             } else {
-                v = cc;
+                vz = cc;
             }
-            bd.loc[(e >> lsd) * bd.P + (e & (side - 1))] = v;
-        }
-        if (mode == kPcg) {
-            const double t = block_sum(racc, s_red);
-            if (tid == 0)
-                bf.rho_part[(static_cast<size_t>(b) * gp.iters + it) * slots + l * C + bd.rank] = t;
-        }
+            z[zo] = vz;
+        });
     }
-    __syncthreads();
+    if (mode == kPcg) {
+        const double t = block_sum(racc, s_red);
+        if (tid == 0) bf.rho_part[(static_cast<size_t>(b) * gp.iters + it) * slots + l * C + q] = t;
+    }
     stamp(gp, 2);
-    cluster_dwt_inverse<T, FLEN>(bd, side, gp, cl);
-    __syncthreads();
+    if (p.nlev > 0) {
+        cl_sync();  // every rank's owned z is complete
+        stamp(gp, 5);
+        const int nthr = blockDim.x;
+        for (int lv = 0; lv < p.nlev; ++lv) {
+            const int s = S >> lv, h = s >> 1, k = h >> p.lC, m0 = q * k, nr = k + H;
+            const int ls = ilog2(s), lh = ls - 1, lk = ilog2(k);
+            const int oA = p.offH[lv], oD = oA + nr * h;
+            const int na = H << lh, n = na + (H << ls);
+            for (int e = tid; e < n; e += nthr) {
+                const int i = e < na ? e >> lh : (e - na) >> ls;
+                const int mm = (m0 - H + i) & (h - 1);
+                const int own = mm >> lk, oi = (mm & (k - 1)) + H;
+                const T* zr = rmt(z, own);
+                if (e < na) {
+                    const int c = e & (h - 1);
+                    z[oA + i * h + c] = zr[oA + oi * h + c];
+                } else {
+                    const int c = (e - na) & (s - 1);
+                    z[oD + i * s + c] = zr[oD + oi * s + c];
+                }
+            }
+        }
+        if (q != 0) {
+            const int to = p.offH[p.nlev];
+            const T* z0 = rmt(z, 0);
+            for (int e = tid; e < p.T * p.T; e += nthr) z[to + e] = z0[to + e];
+        }
+        __syncthreads();
+    }
+    stamp(gp, 3);
+    int outP = P;
+    const T* out = cdwt_inverse<T, FLEN>(gp, p, z, x0, x1, aw, tb, tb2, P, &outP);
     stamp(gp, 9);
-    for (int e = tid; e < ne; e += nthr) bf.phi[base + e] = bd.loc[(e >> lsd) * bd.P + (e & (side - 1))];
+    const int R = clay::band_rows(S, C, q), r0 = clay::band_row0(S, C, q);
+    T* __restrict__ phi = bf.phi + lbase + static_cast<size_t>(r0) * S;
+    for (int e = tid; e < R * S; e += blockDim.x) phi[e] = out[(e >> p.lsS) * outP + (e & (S - 1))];
+    if (p.nlev > 0) cl_wait();  // no rank exits while its level outputs may still be read
 }
 
 template <typename T, int FLEN>
@@ -662,18 +859,18 @@ __global__ void __launch_bounds__(256) k_inv_cluster(const GeoParams gp, const B
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cg::cluster_group cl = cg::this_cluster();
     pdl_launch_dependents();
-    inv_phase<T, FLEN>(gp, bf, mode, it, smem_raw, blockIdx.y, blockIdx.z, cl);
-    cl.sync();  // no rank exits while its shared memory may still be read
+    inv_phase<T, FLEN>(gp, bf, mode, it, smem_raw, blockIdx.y, blockIdx.z, static_cast<int>(cl.block_rank()),
+                       static_cast<int>(cl.num_blocks()));
     stamp(gp, 11);
 }
 
 // ---------------------------------------------------------------------------
-// Phase C: grid (C, L, B), cluster (C,1,1).
-//   band <- sum_w P^T psi_w (gather=1) or y (gather=0, bare wavelet op);
-//   cluster W; epilogue per mode (kPlain / kApply / kPcg / kRhs).
-// Shared memory: band | epilogue prefetch (2 slices) | hc | staged chunk.
+// Forward kernel: grid (C, L, B), cluster (C,1,1).
+//   band <- y (k_gather's sum_w P^T psi_w, or the bare wavelet op's input);
+//   cluster W; epilogue per mode (kPlain / kApply / kPcg / kRhs) on the
+//   rank's compact set.
 //
-// gather = 1: y is a fitting-term output sum_w P^T Gamma^T(...).  Its coarse
+// fit_term = 1: y is a fitting-term output sum_w P^T Gamma^T(...).  Its coarse
 // (scale-0) coefficient is exactly zero in real arithmetic -- the bilinear
 // weights of every aperture node sum to one and each subaperture's Gamma^T
 // stencil (-x-y, x-y, -x+y, x+y; operators.hpp:182-185) sums to zero, so
@@ -684,105 +881,103 @@ __global__ void __launch_bounds__(256) k_inv_cluster(const GeoParams gp, const B
 // (gp.piston_exact) use the exact value.
 // ---------------------------------------------------------------------------
 template <typename T, int FLEN>
-__device__ __forceinline__ void fwd_phase(const GeoParams& gp, const Bufs<T>& bf, int mode, int it, int gather,
-                          unsigned char* smem_raw, int l, int b, cg::cluster_group& cl) {
+__device__ __forceinline__ void fwd_phase(const GeoParams& gp, const Bufs<T>& bf, int mode, int it, int fit_term,
+                                          unsigned char* smem_raw, int l, int b, int q, int C) {
     __shared__ double s_red[32];
-    __shared__ WDesc s_desc[kMaxW];
-    const int side = gp.side[l];
-    const int lsd = ilog2(side);
-    T* band = reinterpret_cast<T*>(smem_raw);
-    Band<T> bd = make_band<T>(band, side, cl);
-    const int C = static_cast<int>(cl.num_blocks());
-    const bool owner = (bd.rank << bd.rsh) < side;
-    const int r0 = bd.rank * bd.R;
-    const int ne = owner ? bd.R * side : 0;
-    const size_t base = static_cast<size_t>(b) * gp.n + gp.coff[l] + static_cast<size_t>(r0) * side;
-    const size_t jbase = gp.coff[l] + static_cast<size_t>(r0) * side;
-    const int nthr = blockDim.x, tid = threadIdx.x;
-    stamp(gp, 0);
-    const int band_b = align16(bd.R * bd.P * static_cast<int>(sizeof(T)));
-    const int slice_b = align16(bd.R * gp.maxside * static_cast<int>(sizeof(T)));
-    T* e0 = reinterpret_cast<T*>(smem_raw + band_b);
-    T* e1 = reinterpret_cast<T*>(smem_raw + band_b + slice_b);
-    T* hc = reinterpret_cast<T*>(smem_raw + band_b + 2 * slice_b);
-    unsigned char* stage = smem_raw + band_b + 2 * slice_b + align16(gp.hc_rows * nthr * static_cast<int>(sizeof(T)));
-    const int nb = ne * static_cast<int>(sizeof(T));
     __shared__ unsigned long long s_mbar[2];
-    Bulk epi{&s_mbar[0], 0}, stg{&s_mbar[1], 0};
-    epi.init();
-    stg.init();
-    pdl_wait();  // psi / y / r / b of the predecessor kernels are complete
-    // epilogue operands by TMA bulk copy, requested now, consumed after the transform
+    __shared__ double s_ad[16];  // alpha d_{l,scale} (operators.hpp:307-332)
+    __shared__ int s_off[2 * (kMaxLev + 1)];
+    const int S = gp.side[l];
+    const LPlan p = make_plan(S, C, q, 0, s_off);
+    const int nthr = blockDim.x, tid = threadIdx.x;
+    const clay::FwdSmem sm = clay::fwd_smem(gp.maxside, C, FLEN, static_cast<int>(sizeof(T)));
+    const int P = gp.maxside + 1;
+    T* x0 = reinterpret_cast<T*>(smem_raw + sm.x0);
+    T* e0 = reinterpret_cast<T*>(smem_raw + sm.e0);
+    T* e1 = reinterpret_cast<T*>(smem_raw + sm.e1);
+    T* x1 = reinterpret_cast<T*>(smem_raw + sm.x1);
+    T* f = reinterpret_cast<T*>(smem_raw + sm.f);
+    T* tb = reinterpret_cast<T*>(smem_raw + sm.tb);
+    T* tb2 = reinterpret_cast<T*>(smem_raw + sm.tb2);
+    const int R = clay::band_rows(S, C, q), r0 = clay::band_row0(S, C, q);
+    const size_t lbase = static_cast<size_t>(b) * gp.n + gp.coff[l];
+    const int roff = clay::rank_off(S, C, q), cnt = clay::owned_count(S, C, q);
+    const size_t vbase = lbase + roff;
+    stamp(gp, 0);
+    double my_ad = 0.0;
+    if (tid >= 64 && tid < 64 + 16 && tid - 64 <= gp.lorder[l]) my_ad = gp.td[gp.ti[gp.o_reg + l] + tid - 64];
     if (tid == 0) {
-        epi.begin();
-        if (nb > 0) {
-            if (mode == kApply) {
-                epi.copy(e0, bf.in + base, nb);
-            } else if (mode == kPcg) {
-                epi.copy(e0, bf.r + base, nb);
-                epi.copy(e1, bf.jinv + jbase, nb);
-            } else if (mode == kRhs) {
-                epi.copy(e0, bf.r + base, nb);
-                epi.copy(e1, bf.b + base, nb);
-            }
-        }
-        epi.commit();
+        mbar_init(&s_mbar[0], 1);
+        mbar_init(&s_mbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
-    if (!gather) {
-        if (tid == 0) {
-            stg.begin();
-            if (nb > 0) stg.copy(hc, bf.y + base, nb);
-            stg.commit();
-        }
-        stg.wait();
-        for (int e = tid; e < ne; e += nthr) bd.loc[(e >> lsd) * bd.P + (e & (side - 1))] = hc[e];
-    } else {
-        gather_band<T>(gp, bf.psi + static_cast<size_t>(b) * gp.Nw, l, bd, owner, hc, stage, s_desc, stg);
+    __syncthreads();
+    if (mode == kPcg) prefetch_block(bf.jinv + gp.coff[l] + roff, e1, cnt, &s_mbar[0], 0);  // constant
+    pdl_wait();  // y / r / b of the predecessor kernels are complete
+    // the band of y (one bulk copy into x1's space, then into the odd-pitch x0); thread 0
+    // issues every block and arrives at once (misaligned blocks: cooperative copies)
+    prefetch_block(bf.y + lbase + static_cast<size_t>(r0) * S, x1, R * S, &s_mbar[1], 0);
+    if (tid == 0) mbar_arrive(&s_mbar[1]);
+    // epilogue operands (this rank's blocks), requested now, consumed after the transform
+    if (mode == kApply) {
+        prefetch_block(bf.in + vbase, e0, cnt, &s_mbar[0], 0);
+    } else if (mode == kPcg) {
+        prefetch_block(bf.r + vbase, e0, cnt, &s_mbar[0], 0);
+    } else if (mode == kRhs) {
+        prefetch_block(bf.r + vbase, e0, cnt, &s_mbar[0], 0);
+        prefetch_block(bf.b + vbase, e1, cnt, &s_mbar[0], 0);
     }
+    if (tid == 0) mbar_arrive(&s_mbar[0]);
+    if (tid >= 64 && tid < 64 + 16) s_ad[tid - 64] = my_ad;
+    __syncthreads();  // s_ad, cooperative copies
+    mbar_wait(&s_mbar[1], 0);
+    stamp(gp, 1);
+    for (int e = tid; e < R * S; e += nthr) x0[(e >> p.lsS) * P + (e & (S - 1))] = x1[e];
     __syncthreads();
     stamp(gp, 2);
-    cluster_dwt_forward<T, FLEN>(bd, side, gp, cl);
+    cdwt_forward<T, FLEN>(gp, p, x0, x1, P, f, tb, tb2);
     __syncthreads();
     stamp(gp, 9);
-    epi.wait();
-    const double* ad = gp.td + gp.ti[gp.o_reg + l];
+    mbar_wait(&s_mbar[0], 0);
+    const double* ad = s_ad;
+    const bool zero_piston = fit_term && gp.piston_exact;
     double macc = 0.0;
-    for (int e = tid; e < ne; e += nthr) {
-        const int i = r0 + (e >> lsd), j = e & (side - 1);
-        const size_t g = base + e;
-        const T wy = (gather && gp.piston_exact && i == 0 && j == 0) ? T(0) : bd.loc[(e >> lsd) * bd.P + j];
+    T* __restrict__ out = bf.out + vbase;
+    T* __restrict__ mz = bf.mz + vbase;
+    T* __restrict__ pr = bf.r + vbase;
+    T* __restrict__ pb = bf.b + vbase;
+    const int o00 = (zero_piston && q == 0) ? p.off[p.nlev] : -1;  // tail (0,0)
+    for_owned(p, [&](int o, int, int sc) {
+        const T wy = o == o00 ? T(0) : f[o];
         if (mode == kPlain) {
-            bf.out[g] = wy;
+            out[o] = wy;
         } else if (mode == kApply) {
-            const T adv = static_cast<T>(ad[bit_width(static_cast<unsigned>(max(i, j)))]);
-            bf.out[g] = wy + adv * e0[e];
+            out[o] = wy + static_cast<T>(ad[sc]) * e0[o];
         } else if (mode == kPcg) {
-            const T adv = static_cast<T>(ad[bit_width(static_cast<unsigned>(max(i, j)))]);
-            const T z = e0[e] * e1[e];
-            const T s = wy + adv * z;
-            bf.mz[g] = s;
-            macc += static_cast<double>(s) * static_cast<double>(z);
+            const T zz = e0[o] * e1[o];
+            const T s = wy + static_cast<T>(ad[sc]) * zz;
+            mz[o] = s;
+            macc += static_cast<double>(s) * static_cast<double>(zz);
         } else {  // kRhs: r += b1 - b ; b = b1
-            bf.r[g] = e0[e] + (wy - e1[e]);
-            bf.b[g] = wy;
+            pr[o] = e0[o] + (wy - e1[o]);
+            pb[o] = wy;
         }
-    }
+    });
     if (mode == kPcg) {
         const double t = block_sum(macc, s_red);
-        if (tid == 0)
-            bf.mu_part[(static_cast<size_t>(b) * gp.iters + it) * (gp.L * C) + l * C + bd.rank] = t;
+        if (tid == 0) bf.mu_part[(static_cast<size_t>(b) * gp.iters + it) * (gp.L * C) + l * C + q] = t;
     }
     stamp(gp, 10);
 }
 
 template <typename T, int FLEN>
 __global__ void __launch_bounds__(256) k_fwd_cluster(const GeoParams gp, const Bufs<T> bf, int mode, int it,
-                                                      int gather) {
+                                                      int fit_term) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cg::cluster_group cl = cg::this_cluster();
     pdl_launch_dependents();
-    fwd_phase<T, FLEN>(gp, bf, mode, it, gather, smem_raw, blockIdx.y, blockIdx.z, cl);
-    cl.sync();
+    fwd_phase<T, FLEN>(gp, bf, mode, it, fit_term, smem_raw, blockIdx.y, blockIdx.z, static_cast<int>(cl.block_rank()),
+                       static_cast<int>(cl.num_blocks()));
     stamp(gp, 11);
 }
 

@@ -19,6 +19,8 @@ constexpr int kMaxW = 16;
 constexpr int kMaxM = 16;
 constexpr int kMaxC = 8;  // CTAs per layer cluster (portable cluster size)
 constexpr int kGatherKMax = 4;  // max bilinear-gather taps per layer node per axis
+constexpr int kGatherRows = 4;  // layer rows per CTA of the adjoint-propagation gather
+constexpr int kMaxGU = 32;      // row groups per layer (max side 128 / kGatherRows)
 
 // Fused-PCG carry (pcg.hpp:32-38 PcgScalars plus per-frame bookkeeping).
 struct Carry {
@@ -63,14 +65,16 @@ struct GeoParams {
     int ccl;          // CTAs per layer cluster
     int o_pg;         // [(w*L+l)*2 + {0 rows, 1 cols}] -> gather table: cnt[side], src[side*KM] (ti), wgt (td/tf)
     int gather_km;    // max gather taps per layer row/column
-    int o_bs;         // [((w*L+l)*kMaxC + rank)*4] psi source block {ilo, ihi, jlo, jhi} of each band
+    int o_bs;         // [((w*L+l)*kMaxGU + u)*4] psi source block {ilo, ihi, jlo, jhi} of each gather row group
     int bd_rows_max, bd_cols_max;
     unsigned long long* stamps;  // optional phase timestamps [block][16] (nullptr: off)
-    unsigned long long* fstamps; // optional frame-kernel phase timestamps [block][32]
     const unsigned char* gblob;  // per-(w,l) gather blobs of the engine's precision (see cluster.cuh)
-    int o_gb;                    // [w*L + l] byte offset of each blob (into ti)
-    int chunk_bytes;  // shared-memory budget of one staged WFS chunk in the band gather
-    int hc_rows;      // rows of the thread-private column scratch
+    int o_gb;                    // [l*kMaxGU + u] byte offset of each row group's table block (into ti)
+    int chunk_bytes;  // shared-memory bytes of the largest staged WFS chunk of the gather
+    int nchunk;                 // WFS chunks of the gather: [gchunk[k], gchunk[k+1])
+    int gchunk[kMaxW + 1];
+    int o_gd;                   // [((l*kMaxGU + u)*kMaxW + w)*8] gather staging descriptors (int4-aligned)
+    int gbuf_bytes;   // the gather's double-buffered row-contracted block (see cluster.cuh)
 };
 
 enum LayerMode : int {
@@ -92,7 +96,7 @@ enum KernelKind : int {
     kKindFwdPcg = 6,   // k_layer_forward kPcg: s = W y + alpha D z, mu
     kKindInvFit = 7,   // k_layer_inverse kFit: last update + W^-1 c
     kKindFit = 8,      // k_fit_control
-    kKindFrame = 9,    // k_frame: the whole step as one persistent cooperative launch
+    kKindGather = 9,   // k_gather: y = sum_w P^T psi_w
 };
 
 template <typename T>

@@ -16,7 +16,8 @@
 
 #include "daubechies_table.h"
 #include "device.hpp"
-#include "kernels.cuh"
+#include "cluster.cuh"
+#include "clayout.hpp"
 #include "launch.hpp"
 
 namespace fewha_gpu {
@@ -58,8 +59,40 @@ struct Plan {
     std::vector<std::uint8_t> masks;
     std::vector<int> wtiles, ltiles;
     std::vector<unsigned char> gblob, tblob;
+    std::vector<int> perm;  // Mallat coefficient index -> rank-blocked HBM index (clayout.hpp)
     int maxside = 0;
 };
+
+// Rank-blocked order of the coefficient-domain vectors: per layer, rank q's
+// owned set (level blocks A then D rows, then the tail on rank 0) at
+// rank_off(q), in the order the kernels' for_owned() visits it.
+std::vector<int> coeff_perm(const GeoParams& gp) {
+    std::vector<int> perm(static_cast<size_t>(gp.n), -1);
+    const int C = gp.ccl;
+    for (int l = 0; l < gp.L; ++l) {
+        const int S = gp.side[l], base = gp.coff[l];
+        for (int q = 0; q < C; ++q) {
+            int o = base + clay::rank_off(S, C, q);
+            for (int lv = 0; lv < clay::nlev(S, C); ++lv) {
+                const int s = S >> lv, h = s / 2, k = h / C, m0 = q * k;
+                for (int i = 0; i < k; ++i)
+                    for (int c = 0; c < h; ++c) perm[static_cast<size_t>(base + (m0 + i) * S + h + c)] = o++;
+                for (int i = 0; i < k; ++i)
+                    for (int c = 0; c < s; ++c) perm[static_cast<size_t>(base + (h + m0 + i) * S + c)] = o++;
+            }
+            if (q == 0) {
+                const int T = clay::tail(S, C);
+                for (int i = 0; i < T; ++i)
+                    for (int j = 0; j < T; ++j) perm[static_cast<size_t>(base + i * S + j)] = o++;
+            }
+            if (o != base + clay::rank_off(S, C, q) + clay::owned_count(S, C, q))
+                throw std::logic_error("coefficient layout: rank block size mismatch");
+        }
+    }
+    for (int v : perm)
+        if (v < 0) throw std::logic_error("coefficient layout: unassigned coefficient");
+    return perm;
+}
 
 int push_table(Plan& pl, const std::vector<Stencil1>& t) {
     const int off = static_cast<int>(pl.ti.size());
@@ -338,7 +371,7 @@ Plan build_plan(const Geometry& g, int elem_bytes) {
     pl.ti.insert(pl.ti.end(), tr.begin(), tr.end());
     pl.td.resize(pl.ti.size(), 0.0);
 
-    // ---- v2 cluster path: R = min(16, side) rows per CTA, C = maxside / R CTAs per layer
+    // ---- cluster path: C = maxside / min(16, maxside) CTAs per layer; band rows per rank: clayout.hpp
     {
         const int R = std::min(16, pl.maxside);
         gp.ccl = pl.maxside / R;
@@ -347,6 +380,7 @@ Plan build_plan(const Geometry& g, int elem_bytes) {
         // ascending source (operators.hpp:129-135 weights as bilinear_stencil assigns them)
         struct Entry { int src; double w; };
         std::vector<std::vector<std::vector<Entry>>> rows(W * L), cols(W * L);
+        std::vector<std::vector<Stencil1>> colst(W * L);  // per psi column: layer column idx, fraction
         int km = 1;
         for (int w = 0; w < W; ++w)
             for (int l = 0; l < L; ++l) {
@@ -365,6 +399,7 @@ Plan build_plan(const Geometry& g, int elem_bytes) {
                 };
                 rows[w * L + l] = build(ty);
                 cols[w * L + l] = build(tx);
+                colst[w * L + l] = tx;
             }
         if (km > kGatherKMax)
             throw ConfigError("invalid geometry: aperture sampling denser than the layer grid allows (gather taps " +
@@ -397,9 +432,10 @@ Plan build_plan(const Geometry& g, int elem_bytes) {
                 }
             }
         }
-        // band source blocks per (w, l, rank)
+        // psi source blocks per (w, l, gather row group u)
+        auto grp_rows = [](int side) { return std::min(kGatherRows, side); };
         gp.o_bs = static_cast<int>(pl.ti.size());
-        pl.ti.resize(pl.ti.size() + static_cast<size_t>(W * L * kMaxC * 4), 0);
+        pl.ti.resize(pl.ti.size() + static_cast<size_t>(W * L * kMaxGU * 4), 0);
         pl.td.resize(pl.ti.size(), 0.0);
         int rmax = 1, cmax = 1;
         for (int w = 0; w < W; ++w)
@@ -407,126 +443,215 @@ Plan build_plan(const Geometry& g, int elem_bytes) {
                 const auto& rt = rows[w * L + l];
                 const auto& ct = cols[w * L + l];
                 const int side = static_cast<int>(rt.size());
-                const int Rl = std::min(16, side);
                 int jlo = INT32_MAX, jhi = 0;
                 for (const auto& v : ct)
                     for (const auto& en : v) {
                         jlo = std::min(jlo, en.src);
                         jhi = std::max(jhi, en.src + 1);
                     }
-                for (int rank = 0; rank < gp.ccl; ++rank) {
+                const int Rl = grp_rows(side);
+                for (int u = 0; u < side / Rl; ++u) {
+                    const int I0 = u * Rl;
                     int ilo = INT32_MAX, ihi = 0;
-                    for (int I = rank * Rl; I < std::min(side, rank * Rl + Rl); ++I)
+                    for (int I = I0; I < I0 + Rl; ++I)
                         for (const auto& en : rt[I]) {
                             ilo = std::min(ilo, en.src);
                             ihi = std::max(ihi, en.src + 1);
                         }
-                    int* bs = &pl.ti[static_cast<size_t>(gp.o_bs + ((w * L + l) * kMaxC + rank) * 4)];
+                    int* bs = &pl.ti[static_cast<size_t>(gp.o_bs + ((w * L + l) * kMaxGU + u) * 4)];
                     if (ilo < ihi && jlo < jhi) {
                         bs[0] = ilo; bs[1] = ihi; bs[2] = jlo; bs[3] = jhi;
                         rmax = std::max(rmax, ihi - ilo);
                         cmax = std::max(cmax, jhi - jlo);
-                    } else {
-                        bs[0] = bs[1] = bs[2] = bs[3] = 0;
+                    } else {  // no source rows: empty block, but the WFS-wide column origin stays
+                        bs[0] = bs[1] = 0;  // (the gather blob's column sources are relative to it)
+                        bs[2] = jlo < jhi ? jlo : 0;
+                        bs[3] = jlo < jhi ? jhi : 0;
                     }
                 }
             }
         gp.bd_rows_max = rmax;
         gp.bd_cols_max = cmax;
-        // thread-private scratch rows: block rows one thread's band rows draw from
-        const int nthr = 256;
+        // staged bytes per WFS (mirrors gather_tab_bytes()/psi_bytes() in cluster.cuh)
         auto a16 = [](size_t v) { return (v + 15) & ~size_t(15); };
-        int hc_rows = 1;
-        size_t chunk_max = 0, single_max = 0;
-        for (int l = 0; l < L; ++l) {
-            const int side = gp.side[l];
-            const int Rl = std::min(16, side);
-            const int groups = std::max(1, std::min(nthr / side, Rl)), rows_pt = std::max(1, Rl / groups);
-            for (int rank = 0; rank < gp.ccl; ++rank) {
-                size_t total = 0;
-                for (int w = 0; w < W; ++w) {
-                    const int* bs = &pl.ti[static_cast<size_t>(gp.o_bs + ((w * L + l) * kMaxC + rank) * 4)];
-                    // mirrors staged_bytes() in cluster.cuh
-                    const size_t need = a16(static_cast<size_t>(bs[1] - bs[0]) * (g.wfs[w].n_subap + 1) * elem_bytes + 16) +
-                                        a16(static_cast<size_t>(side) * km * 2) + a16(static_cast<size_t>(Rl) * km * 2) +
-                                        a16(static_cast<size_t>(side) * km * elem_bytes) +
-                                        a16(static_cast<size_t>(Rl) * km * elem_bytes);
-                    total += need;
-                    single_max = std::max(single_max, need);
-                    const auto& rt = rows[w * L + l];
-                    for (int gI = 0; gI < groups; ++gI) {
-                        int lo = INT32_MAX, hi = -1;
-                        for (int I = rank * Rl + gI * rows_pt; I < std::min(side, rank * Rl + (gI + 1) * rows_pt); ++I)
-                            for (const auto& en : rt[I]) {
-                                lo = std::min(lo, en.src);
-                                hi = std::max(hi, en.src);
-                            }
-                        if (hi >= lo) hc_rows = std::max(hc_rows, hi - lo + 1);
-                    }
+        auto tab_bytes = [&](int R, int side, int nc) {
+            return a16(static_cast<size_t>(R) * km * 2) + a16(static_cast<size_t>(R) * km * elem_bytes) +
+                   a16(static_cast<size_t>(side + 3) * 2) + a16(static_cast<size_t>(nc) * 2) +
+                   a16(static_cast<size_t>(nc) * elem_bytes);
+        };
+        // WFS chunks (same for every row group): greedy over w by the worst row group's bytes,
+        // within a budget that keeps two gather CTAs per SM
+        auto need_of = [&](int w, int l, int u) {
+            const int side = gp.side[l], Rl = grp_rows(side);
+            const int* bs = &pl.ti[static_cast<size_t>(gp.o_bs + ((w * L + l) * kMaxGU + u) * 4)];
+            return std::pair<size_t, size_t>(
+                tab_bytes(Rl, side, bs[3] - bs[2]),
+                a16(static_cast<size_t>(bs[1] - bs[0]) * (g.wfs[w].n_subap + 1) * elem_bytes + 16));
+        };
+        std::vector<size_t> need_max(static_cast<size_t>(W), 0);
+        for (int w = 0; w < W; ++w)
+            for (int l = 0; l < L; ++l)
+                for (int u = 0; u < gp.side[l] / grp_rows(gp.side[l]); ++u) {
+                    const auto nb = need_of(w, l, u);
+                    need_max[static_cast<size_t>(w)] = std::max(need_max[static_cast<size_t>(w)], nb.first + nb.second);
                 }
-                chunk_max = std::max(chunk_max, total);
-            }
-        }
-        gp.hc_rows = hc_rows;
-        const size_t Rm = static_cast<size_t>(std::min(16, pl.maxside));
-        const size_t fixed = a16(Rm * (pl.maxside + 1) * elem_bytes) + 2 * a16(Rm * pl.maxside * elem_bytes) +
-                             a16(static_cast<size_t>(hc_rows) * nthr * elem_bytes) + 2048;
-        const size_t limit = 227 * 1024;
+        // row-contracted blocks G of every WFS of a chunk (group rows x psi block columns)
+        gp.gbuf_bytes = static_cast<int>(a16(static_cast<size_t>(W) * kGatherRows * cmax * elem_bytes));
+        const size_t fixed = a16(static_cast<size_t>(gp.gbuf_bytes)) + 1024;  // + static shared memory
+        const size_t limit = 110 * 1024;                                      // two CTAs per SM
         const size_t budget = limit > fixed ? limit - fixed : 0;
-        if (single_max > budget) throw ConfigError("invalid geometry: adjoint gather does not fit in shared memory");
-        gp.chunk_bytes = static_cast<int>(std::min(chunk_max, budget));
-        // gather blobs per (w,l): [col src int16][row src int16][col w][row w], 16-byte aligned parts;
-        // column sources relative to the WFS's first contributing column (the band block's jlo)
+        gp.nchunk = 0;
+        gp.gchunk[0] = 0;
+        size_t used = 0, chunk_max = 0;
+        for (int w = 0; w < W; ++w) {
+            if (need_max[static_cast<size_t>(w)] > budget)
+                throw ConfigError("invalid geometry: adjoint gather does not fit in shared memory");
+            if (w > gp.gchunk[gp.nchunk] && used + need_max[static_cast<size_t>(w)] > budget) {
+                gp.gchunk[++gp.nchunk] = w;
+                used = 0;
+            }
+            used += need_max[static_cast<size_t>(w)];
+            chunk_max = std::max(chunk_max, used);
+        }
+        gp.gchunk[++gp.nchunk] = W;
+        gp.chunk_bytes = static_cast<int>(chunk_max);
+        // gather tables per (layer, row group), WFS ascending, each WFS 16-byte aligned parts
+        //   [row src int16 R x KM][row w R x KM]                  padded row taps of the group
+        //   [first int16 side+3][col idx int16 nc][col frac nc]   compressed column stencil
+        // (mirrors k_gather() in cluster.cuh).  Row sources are relative to the group's psi
+        // block row ilo (zero-weight padding clamped into the block); column entries are
+        // the psi block columns jlo.. with their layer column idx and bilinear fraction f
+        // (layer column J receives 1-f from idx == J and f from idx == J-1, operators.hpp:
+        // 129-135); first[k] = first block column with idx >= k-1.
         gp.o_gb = static_cast<int>(pl.ti.size());
-        pl.ti.resize(pl.ti.size() + static_cast<size_t>(W * L), 0);
+        pl.ti.resize(pl.ti.size() + static_cast<size_t>(L * kMaxGU), 0);
         pl.td.resize(pl.ti.size(), 0.0);
         pl.gblob.clear();
-        for (int w = 0; w < W; ++w)
-            for (int l = 0; l < L; ++l) {
-                const auto& rt = rows[w * L + l];
-                const auto& ct = cols[w * L + l];
-                const int side = static_cast<int>(rt.size());
-                const int jlo = pl.ti[static_cast<size_t>(gp.o_bs + ((w * L + l) * kMaxC + 0) * 4 + 2)];
-                pl.ti[static_cast<size_t>(gp.o_gb + w * L + l)] = static_cast<int>(pl.gblob.size());
-                auto put_src = [&](const std::vector<std::vector<Entry>>& tab, int rel) {
+        auto padded = [&](const std::vector<std::vector<Entry>>& tab, std::vector<int>& src, std::vector<double>& wt) {
+            const int side = static_cast<int>(tab.size());
+            src.assign(static_cast<size_t>(side) * km, 0);
+            wt.assign(static_cast<size_t>(side) * km, 0.0);
+            int carry = 0;
+            for (const auto& v : tab)
+                if (!v.empty()) { carry = v.front().src; break; }
+            for (int I = 0; I < side; ++I)
+                for (int q = 0; q < km; ++q) {
+                    const bool valid = q < static_cast<int>(tab[I].size());
+                    if (valid) carry = tab[I][q].src;
+                    src[static_cast<size_t>(I) * km + q] = carry;
+                    wt[static_cast<size_t>(I) * km + q] = valid ? tab[I][q].w : 0.0;
+                }
+        };
+        auto put_i16 = [&](const std::vector<int>& src, int i0, int n, int rel, int lim) {
+            const size_t start = pl.gblob.size();
+            for (int I = i0; I < i0 + n; ++I)
+                for (int q = 0; q < km; ++q) {
+                    int v = src[static_cast<size_t>(I) * km + q] - rel;
+                    v = std::min(std::max(v, 0), std::max(lim - 1, 0));
+                    if (v > 32767) throw ConfigError("invalid geometry: gather index overflow");
+                    const short s16 = static_cast<short>(v);
+                    const auto* p = reinterpret_cast<const unsigned char*>(&s16);
+                    pl.gblob.insert(pl.gblob.end(), p, p + 2);
+                }
+            pl.gblob.resize(start + a16(pl.gblob.size() - start), 0);
+        };
+        auto put_wt = [&](const std::vector<double>& wt, int i0, int n) {
+            const size_t start = pl.gblob.size();
+            for (int I = i0; I < i0 + n; ++I)
+                for (int q = 0; q < km; ++q) {
+                    const double v = wt[static_cast<size_t>(I) * km + q];
+                    if (elem_bytes == 8) {
+                        const auto* p = reinterpret_cast<const unsigned char*>(&v);
+                        pl.gblob.insert(pl.gblob.end(), p, p + 8);
+                    } else {
+                        const float f = static_cast<float>(v);
+                        const auto* p = reinterpret_cast<const unsigned char*>(&f);
+                        pl.gblob.insert(pl.gblob.end(), p, p + 4);
+                    }
+                }
+            pl.gblob.resize(start + a16(pl.gblob.size() - start), 0);
+        };
+        auto put_raw = [&](const void* p, size_t n) {
+            const auto* b = static_cast<const unsigned char*>(p);
+            pl.gblob.insert(pl.gblob.end(), b, b + n);
+        };
+        auto pad16 = [&](size_t start) { pl.gblob.resize(start + a16(pl.gblob.size() - start), 0); };
+        std::vector<int> rsrc;
+        std::vector<double> rwt;
+        for (int l = 0; l < L; ++l)
+            for (int u = 0; u < gp.side[l] / grp_rows(gp.side[l]); ++u) {
+                pl.ti[static_cast<size_t>(gp.o_gb + l * kMaxGU + u)] = static_cast<int>(pl.gblob.size());
+                const int side = gp.side[l];
+                const int Rl = grp_rows(side), I0 = u * Rl;
+                for (int w = 0; w < W; ++w) {
+                    const int* bs = &pl.ti[static_cast<size_t>(gp.o_bs + ((w * L + l) * kMaxGU + u) * 4)];
                     const size_t start = pl.gblob.size();
-                    int carry = 0;
-                    for (const auto& v : tab)
-                        if (!v.empty()) { carry = v.front().src; break; }
-                    for (int I = 0; I < side; ++I)
-                        for (int q = 0; q < km; ++q) {
-                            if (q < static_cast<int>(tab[I].size())) carry = tab[I][q].src;
-                            const int v = carry - rel;
-                            if (v < -32768 || v > 32767) throw ConfigError("invalid geometry: gather index overflow");
-                            const short s16 = static_cast<short>(v);
-                            const auto* p = reinterpret_cast<const unsigned char*>(&s16);
-                            pl.gblob.insert(pl.gblob.end(), p, p + 2);
+                    padded(rows[w * L + l], rsrc, rwt);
+                    put_i16(rsrc, I0, Rl, bs[0], bs[1] - bs[0]);
+                    put_wt(rwt, I0, Rl);
+                    const auto& tx = colst[w * L + l];
+                    const int jlo = bs[2], nc = bs[3] - bs[2];
+                    size_t p0 = pl.gblob.size();
+                    for (int k = 0; k < side + 3; ++k) {
+                        int f0 = nc;
+                        for (int c = 0; c < nc; ++c)
+                            if (tx[static_cast<size_t>(jlo + c)].idx >= k - 1) { f0 = c; break; }
+                        const short v = static_cast<short>(f0);
+                        put_raw(&v, 2);
+                    }
+                    pad16(p0);
+                    p0 = pl.gblob.size();
+                    for (int c = 0; c < nc; ++c) {
+                        const short v = static_cast<short>(tx[static_cast<size_t>(jlo + c)].idx);
+                        put_raw(&v, 2);
+                    }
+                    pad16(p0);
+                    p0 = pl.gblob.size();
+                    for (int c = 0; c < nc; ++c) {
+                        const double fr = tx[static_cast<size_t>(jlo + c)].f;
+                        if (elem_bytes == 8) put_raw(&fr, 8);
+                        else {
+                            const float ff = static_cast<float>(fr);
+                            put_raw(&ff, 4);
                         }
-                    pl.gblob.resize(start + a16(pl.gblob.size() - start), 0);
-                };
-                auto put_w = [&](const std::vector<std::vector<Entry>>& tab) {
-                    const size_t start = pl.gblob.size();
-                    for (int I = 0; I < side; ++I)
-                        for (int q = 0; q < km; ++q) {
-                            const double v = q < static_cast<int>(tab[I].size()) ? tab[I][q].w : 0.0;
-                            if (elem_bytes == 8) {
-                                const auto* p = reinterpret_cast<const unsigned char*>(&v);
-                                pl.gblob.insert(pl.gblob.end(), p, p + 8);
-                            } else {
-                                const float f = static_cast<float>(v);
-                                const auto* p = reinterpret_cast<const unsigned char*>(&f);
-                                pl.gblob.insert(pl.gblob.end(), p, p + 4);
-                            }
-                        }
-                    pl.gblob.resize(start + a16(pl.gblob.size() - start), 0);
-                };
-                put_src(ct, jlo);
-                put_src(rt, 0);
-                put_w(ct);
-                put_w(rt);
+                    }
+                    pad16(p0);
+                    if (pl.gblob.size() - start != tab_bytes(Rl, side, nc))
+                        throw std::logic_error("gather tables: size mismatch");
+                }
+            }
+        // staging descriptors per (layer, row group, WFS), 8 ints (mirrors GDesc in cluster.cuh):
+        //   ilo ihi jlo jhi | psi source element offset | psi stage byte offset in its chunk |
+        //   table byte offset in gblob | table bytes
+        // In a chunk the tables of its WFS come first (one contiguous copy), then the psi blocks.
+        pl.ti.resize((pl.ti.size() + 3) & ~size_t(3), 0);  // int4-aligned
+        gp.o_gd = static_cast<int>(pl.ti.size());
+        pl.ti.resize(pl.ti.size() + static_cast<size_t>(L * kMaxGU * kMaxW * 8), 0);
+        pl.td.resize(pl.ti.size(), 0.0);
+        for (int l = 0; l < L; ++l)
+            for (int u = 0; u < gp.side[l] / grp_rows(gp.side[l]); ++u) {
+                size_t toff = static_cast<size_t>(pl.ti[static_cast<size_t>(gp.o_gb + l * kMaxGU + u)]);
+                for (int k = 0; k < gp.nchunk; ++k) {
+                    size_t tsum = 0;
+                    for (int w = gp.gchunk[k]; w < gp.gchunk[k + 1]; ++w) tsum += need_of(w, l, u).first;
+                    size_t poff = tsum;
+                    for (int w = gp.gchunk[k]; w < gp.gchunk[k + 1]; ++w) {
+                        const int* bs = &pl.ti[static_cast<size_t>(gp.o_bs + ((w * L + l) * kMaxGU + u) * 4)];
+                        const auto nb = need_of(w, l, u);
+                        int* d = &pl.ti[static_cast<size_t>(gp.o_gd + ((l * kMaxGU + u) * kMaxW + w) * 8)];
+                        d[0] = bs[0]; d[1] = bs[1]; d[2] = bs[2]; d[3] = bs[3];
+                        d[4] = gp.woff[w] + bs[0] * (g.wfs[w].n_subap + 1);
+                        d[5] = static_cast<int>(poff);
+                        d[6] = static_cast<int>(toff);
+                        d[7] = static_cast<int>(nb.first);
+                        poff += nb.second;
+                        toff += nb.first;
+                    }
+                }
             }
     }
     gp.n_ltiles = static_cast<int>(pl.ltiles.size() / 3);
+    pl.perm = coeff_perm(gp);
     return pl;
 }
 
@@ -616,19 +741,16 @@ inline bool pdl_enabled() {
 template <typename T>
 struct Launch {
     static size_t wfs_smem(const GeoParams& gp) { return wfs_tile_smem<T>(std::max(gp.L, gp.M)); }
-    static size_t adj_smem(const GeoParams& gp) {
-        return static_cast<size_t>(gp.lt_rows_max) * (gp.lt_cols_max + gp.ltile) * sizeof(T);
+    static size_t gather_smem(const GeoParams& gp) {
+        return ((static_cast<size_t>(gp.gbuf_bytes) + 15) & ~size_t(15)) + static_cast<size_t>(gp.chunk_bytes);
     }
     static size_t a16(size_t v) { return (v + 15) & ~size_t(15); }
-    static size_t band_rows(const GeoParams& gp) { return static_cast<size_t>(std::min(16, gp.maxside)); }
-    static size_t band_bytes(const GeoParams& gp) { return a16(band_rows(gp) * (gp.maxside + 1) * sizeof(T)); }
-    static size_t slice_bytes(const GeoParams& gp) { return a16(band_rows(gp) * gp.maxside * sizeof(T)); }
-    // band + 6 prefetched band slices (r, 1/J, p, q, c, Mz)
-    static size_t inv_cl_smem(const GeoParams& gp) { return band_bytes(gp) + 6 * slice_bytes(gp); }
-    // band + 2 epilogue slices + thread-private column scratch (256 threads) + one staged WFS chunk
-    static size_t fwd_cl_smem(const GeoParams& gp) {
-        return band_bytes(gp) + 2 * slice_bytes(gp) + a16(static_cast<size_t>(gp.hc_rows) * 256 * sizeof(T)) +
-               static_cast<size_t>(gp.chunk_bytes);
+    // shared-memory maps: clayout.hpp (the kernels derive the same offsets)
+    static size_t inv_cl_smem(const GeoParams& gp, int flen) {
+        return static_cast<size_t>(clay::inv_smem(gp.maxside, gp.ccl, flen, static_cast<int>(sizeof(T))).total);
+    }
+    static size_t fwd_cl_smem(const GeoParams& gp, int flen) {
+        return static_cast<size_t>(clay::fwd_smem(gp.maxside, gp.ccl, flen, static_cast<int>(sizeof(T))).total);
     }
 
 #define FEWHA_FLEN_SWITCH(flen, CALL)          \
@@ -651,8 +773,8 @@ struct Launch {
         int dev = 0, maxopt = 0;
         CK(cudaGetDevice(&dev));
         CK(cudaDeviceGetAttribute(&maxopt, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-        if (inv_cl_smem(gp) > static_cast<size_t>(maxopt) || fwd_cl_smem(gp) > static_cast<size_t>(maxopt) ||
-            wfs_smem(gp) > static_cast<size_t>(maxopt) || adj_smem(gp) > static_cast<size_t>(maxopt))
+        if (inv_cl_smem(gp, flen) > static_cast<size_t>(maxopt) || fwd_cl_smem(gp, flen) > static_cast<size_t>(maxopt) ||
+            wfs_smem(gp) > static_cast<size_t>(maxopt) || gather_smem(gp) > static_cast<size_t>(maxopt))
             throw ConfigError("invalid geometry: layer kernels exceed the device's shared memory");
         const size_t m = static_cast<size_t>(maxopt);
 #define FEWHA_SET(N) CK((set_layer_cluster_attrs<T, N>(m, m)))
@@ -668,13 +790,13 @@ struct Launch {
         };
         opt_in(k_wfs<T, false>, wfs_smem(gp));
         opt_in(k_wfs<T, true>, wfs_smem(gp));
-        opt_in(k_adjoint<T>, adj_smem(gp));
+        opt_in(k_gather<T>, gather_smem(gp));
     }
     // layer kernels: grid (C, L, count), cluster (C,1,1)
     static void cl(int flen, bool inverse, const GeoParams& gp, const Bufs<T>& bf, int mode, int it, int count,
-                   cudaStream_t st, int gather = 1) {
-        const size_t smem = inverse ? inv_cl_smem(gp) : fwd_cl_smem(gp);
-#define FEWHA_LAUNCH(N) CK((launch_layer_cluster<T, N>(inverse, gp, bf, mode, it, count, st, gather, smem)))
+                   cudaStream_t st, int fit_term = 1) {
+        const size_t smem = inverse ? inv_cl_smem(gp, flen) : fwd_cl_smem(gp, flen);
+#define FEWHA_LAUNCH(N) CK((launch_layer_cluster<T, N>(inverse, gp, bf, mode, it, count, st, fit_term, smem)))
         FEWHA_FLEN_SWITCH(flen, FEWHA_LAUNCH)
 #undef FEWHA_LAUNCH
     }
@@ -698,8 +820,12 @@ struct Launch {
         if (rhs) CK(cudaLaunchKernelEx(&cfg, k_wfs<T, true>, gp, bf, with_dm));
         else CK(cudaLaunchKernelEx(&cfg, k_wfs<T, false>, gp, bf, with_dm));
     }
-    static void adjoint(const GeoParams& gp, const T* psi, T* y, int count, cudaStream_t st) {
-        k_adjoint<T><<<dim3(gp.n_ltiles, count), 256, adj_smem(gp), st>>>(gp, psi, y);
+    // y = sum_w P^T psi_w: one CTA per kGatherRows rows of every layer
+    static void gather(const GeoParams& gp, const Bufs<T>& bf, int count, cudaStream_t st) {
+        cudaLaunchAttribute attr[1];
+        const int groups = gp.maxside / std::min(kGatherRows, gp.maxside);
+        cudaLaunchConfig_t cfg = pdl_cfg(dim3(groups, gp.L, count), gather_smem(gp), st, attr);
+        CK(cudaLaunchKernelEx(&cfg, k_gather<T>, gp, bf));
     }
     static void fit(const GeoParams& gp, const Bufs<T>& bf, int step, int count, cudaStream_t st) {
         cudaLaunchAttribute attr[1];
@@ -722,8 +848,6 @@ struct EngineImpl {
     bool own_stream = false;
     cudaGraphExec_t graph = nullptr;
     bool has_precond = false;
-    bool persistent = false;         // single-instance frames as one cooperative launch (frame.cuh)
-    unsigned int* bar = nullptr;     // its grid-barrier counter
     // optional per-phase timestamps of the cluster kernels (profiling only)
     unsigned long long* stamp_buf = nullptr;
     int stamp_slot = -1;  // < 0: stamping off
@@ -731,8 +855,7 @@ struct EngineImpl {
     GeoParams gps() {
         GeoParams g2 = gp;
         if (stamp_slot >= 0 && stamp_slot < kStampSlots) {
-            if (persistent) g2.fstamps = stamp_buf;  // [block][32] in the first slots
-            else g2.stamps = stamp_buf + static_cast<size_t>(stamp_slot++) * kStampBlocks * 16;
+            g2.stamps = stamp_buf + static_cast<size_t>(stamp_slot++) * kStampBlocks * 16;
         }
         return g2;
     }
@@ -800,18 +923,11 @@ struct EngineImpl {
         bf.jac = static_cast<const T*>(jac);
         bf.jinv = static_cast<const T*>(jinv);
         const int B = batch;
-        if (persistent) {
-            const size_t smem = std::max(Launch<T>::fwd_cl_smem(gp), Launch<T>::inv_cl_smem(gp));
-#define FEWHA_PF(N) CK((launch_frame_persistent<T, N>(gps(), bf, bar, st, smem)))
-            FEWHA_FLEN_SWITCH(flen, FEWHA_PF)
-#undef FEWHA_PF
-            mark(kKindFrame);
-            CK(cudaGetLastError());
-            return;
-        }
         // RHS with the pseudo open-loop term (reconstructor.hpp:316-323)
         Launch<T>::wfs(true, gps(), bf, gp.closed, B, st);
         mark(kKindWfsRhs);
+        Launch<T>::gather(gps(), bf, B, st);
+        mark(kKindGather);
         Launch<T>::cl(flen, false, gps(), bf, kRhs, 0, B, st);
         mark(kKindFwdRhs);
         // fused PCG (pcg.hpp:68-106), the update of iteration k fused into k+1's W^-1
@@ -820,6 +936,8 @@ struct EngineImpl {
             mark(it == 0 ? kKindInvPcg0 : kKindInvPcg);
             Launch<T>::wfs(false, gps(), bf, 0, B, st);
             mark(kKindWfs);
+            Launch<T>::gather(gps(), bf, B, st);
+            mark(kKindGather);
             Launch<T>::cl(flen, false, gps(), bf, kPcg, it, B, st);
             mark(kKindFwdPcg);
         }
@@ -887,6 +1005,7 @@ struct EngineImpl {
         Bufs<T> bf = w.bf;
         Launch<T>::cl(flen, true, g, bf, kPlain, 0, count, st);
         Launch<T>::wfs(false, g, bf, 0, count, st);
+        Launch<T>::gather(g, bf, count, st);
         Launch<T>::cl(flen, false, g, bf, kApply, 0, count, st);
     }
 
@@ -927,11 +1046,11 @@ struct EngineImpl {
             const int cnt = static_cast<int>(std::min<size_t>(chunk, probes.size() - p0));
             CK(cudaMemsetAsync(pd.in, 0, sizeof(double) * n * cnt, stream));
             for (int k = 0; k < cnt; ++k)
-                CK(cudaMemcpyAsync(pd.in + k * n + probes[p0 + k].rep, one.data(), sizeof(double),
+                CK(cudaMemcpyAsync(pd.in + k * n + plan.perm[probes[p0 + k].rep], one.data(), sizeof(double),
                                    cudaMemcpyHostToDevice, stream));
             apply_M_dev<double>(pd, cnt, stream, gp64);
             for (int k = 0; k < cnt; ++k)
-                CK(cudaMemcpyAsync(&probed[p0 + k], pd.out + k * n + probes[p0 + k].rep, sizeof(double),
+                CK(cudaMemcpyAsync(&probed[p0 + k], pd.out + k * n + plan.perm[probes[p0 + k].rep], sizeof(double),
                                    cudaMemcpyDeviceToHost, stream));
             CK(cudaStreamSynchronize(stream));
         }
@@ -959,8 +1078,12 @@ struct EngineImpl {
             if (!(v > 0.0))
                 throw std::runtime_error("preconditioner: non-positive diagonal entry (operator symmetry broken?)");
         precond = diag;
-        std::vector<double> inv(n);
-        for (size_t k = 0; k < n; ++k) inv[k] = 1.0 / diag[k];
+        std::vector<double> inv(n), dperm(n);
+        for (size_t k = 0; k < n; ++k) {  // device copies in the rank-blocked order
+            dperm[static_cast<size_t>(plan.perm[k])] = diag[k];
+            inv[static_cast<size_t>(plan.perm[k])] = 1.0 / diag[k];
+        }
+        diag.swap(dperm);
         if (precision == 64) {
             CK(cudaMemcpy(jac, diag.data(), n * sizeof(double), cudaMemcpyHostToDevice));
             CK(cudaMemcpy(jinv, inv.data(), n * sizeof(double), cudaMemcpyHostToDevice));
@@ -1007,6 +1130,24 @@ void d2h_conv(double* dst, const T* src, size_t n, cudaStream_t st) {
         CK(cudaStreamSynchronize(st));
         std::copy(tmp.begin(), tmp.end(), dst);
     }
+}
+// Coefficient-domain vectors: the API's Mallat order <-> the device's
+// rank-blocked order (clayout.hpp), `count` instances of n.
+template <typename T>
+void h2d_coeff(T* dst, const double* src, const std::vector<int>& perm, size_t count, cudaStream_t st) {
+    const size_t n = perm.size();
+    std::vector<double> tmp(n * count);
+    for (size_t b = 0; b < count; ++b)
+        for (size_t i = 0; i < n; ++i) tmp[b * n + static_cast<size_t>(perm[i])] = src[b * n + i];
+    h2d_conv<T>(dst, tmp.data(), n * count, st);
+}
+template <typename T>
+void d2h_coeff(double* dst, const T* src, const std::vector<int>& perm, size_t count, cudaStream_t st) {
+    const size_t n = perm.size();
+    std::vector<double> tmp(n * count);
+    d2h_conv<T>(tmp.data(), src, n * count, st);
+    for (size_t b = 0; b < count; ++b)
+        for (size_t i = 0; i < n; ++i) dst[b * n + i] = tmp[b * n + static_cast<size_t>(perm[i])];
 }
 }  // namespace
 
@@ -1060,30 +1201,6 @@ Engine::Engine(Geometry g, int precision, int batch, int device) : p_(std::make_
         P.jinv = dalloc<float>(P.gp.n);
     }
     Launch<double>::set_attrs(P.gp64, P.flen);  // probes always fp64
-    {
-        const char* env = std::getenv("FEWHA_PERSISTENT");
-        // opt-in until its phases outrun the launch gaps they remove
-        const bool allow = batch == 1 && env && env[0] == '1' && !P.g.projection;
-        int ok = 0;
-        if (allow) {
-            if (precision == 64) {
-                const size_t smem = std::max(Launch<double>::fwd_cl_smem(P.gp), Launch<double>::inv_cl_smem(P.gp));
-#define FEWHA_FIT(N) CK((frame_persistent_fits<double, N>(P.gp, smem, &ok)))
-                FEWHA_FLEN_SWITCH(P.flen, FEWHA_FIT)
-#undef FEWHA_FIT
-            } else {
-                const size_t smem = std::max(Launch<float>::fwd_cl_smem(P.gp), Launch<float>::inv_cl_smem(P.gp));
-#define FEWHA_FIT(N) CK((frame_persistent_fits<float, N>(P.gp, smem, &ok)))
-                FEWHA_FLEN_SWITCH(P.flen, FEWHA_FIT)
-#undef FEWHA_FIT
-            }
-        }
-        if (ok) {
-            P.bar = dalloc<unsigned int>(1);
-            P.fr.add(P.bar);
-            P.persistent = true;
-        }
-    }
     P.fr.add(P.jac);
     P.fr.add(P.jinv);
     reset();
@@ -1137,12 +1254,12 @@ void Engine::step(const double* slopes, double* coeffs, double* dm, double* rho,
     CK(cudaMemcpyAsync(nl.data(), dnl, B * sizeof(int), cudaMemcpyDeviceToHost, st));
     if (rho) CK(cudaMemcpyAsync(rho, drho, B * it * sizeof(double), cudaMemcpyDeviceToHost, st));
     if (P.precision == 64) {
-        if (coeffs) CK(cudaMemcpyAsync(coeffs, P.sd.bf.c, B * n * sizeof(double), cudaMemcpyDeviceToHost, st));
         if (dm) CK(cudaMemcpyAsync(dm, P.sd.bf.a_out, B * A * sizeof(double), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
+        if (coeffs) d2h_coeff<double>(coeffs, P.sd.bf.c, P.plan.perm, B, st);
     } else {
         CK(cudaStreamSynchronize(st));
-        if (coeffs) d2h_conv<float>(coeffs, P.sf.bf.c, B * n, st);
+        if (coeffs) d2h_coeff<float>(coeffs, P.sf.bf.c, P.plan.perm, B, st);
         if (dm) d2h_conv<float>(dm, P.sf.bf.a_out, B * A, st);
     }
     if (n_rho) std::copy(nl.begin(), nl.end(), n_rho);
@@ -1176,11 +1293,11 @@ void Engine::get_state(int inst, double* c, double* b, double* r, double* p, dou
         using T = std::remove_pointer_t<decltype(w.bf.c)>;
         const cudaStream_t st = P.s();
         CK(cudaStreamSynchronize(st));
-        d2h_conv<T>(c, w.bf.c + inst * n, n, st);
-        d2h_conv<T>(b, w.bf.b + inst * n, n, st);
-        d2h_conv<T>(r, w.bf.r + inst * n, n, st);
-        d2h_conv<T>(p, w.bf.p + inst * n, n, st);
-        d2h_conv<T>(q, w.bf.q + inst * n, n, st);
+        d2h_coeff<T>(c, w.bf.c + inst * n, P.plan.perm, 1, st);
+        d2h_coeff<T>(b, w.bf.b + inst * n, P.plan.perm, 1, st);
+        d2h_coeff<T>(r, w.bf.r + inst * n, P.plan.perm, 1, st);
+        d2h_coeff<T>(p, w.bf.p + inst * n, P.plan.perm, 1, st);
+        d2h_coeff<T>(q, w.bf.q + inst * n, P.plan.perm, 1, st);
         d2h_conv<T>(a_prev2, w.bf.a_prev2 + inst * A, A, st);
         d2h_conv<T>(a_prev, w.bf.a_prev + inst * A, A, st);
         Carry cr;
@@ -1203,11 +1320,11 @@ void Engine::set_state(int inst, const double* c, const double* b, const double*
         using T = std::remove_pointer_t<decltype(w.bf.c)>;
         const cudaStream_t st = P.s();
         CK(cudaStreamSynchronize(st));
-        h2d_conv<T>(w.bf.c + inst * n, c, n, st);
-        h2d_conv<T>(w.bf.b + inst * n, b, n, st);
-        h2d_conv<T>(w.bf.r + inst * n, r, n, st);
-        h2d_conv<T>(w.bf.p + inst * n, p, n, st);
-        h2d_conv<T>(w.bf.q + inst * n, q, n, st);
+        h2d_coeff<T>(w.bf.c + inst * n, c, P.plan.perm, 1, st);
+        h2d_coeff<T>(w.bf.b + inst * n, b, P.plan.perm, 1, st);
+        h2d_coeff<T>(w.bf.r + inst * n, r, P.plan.perm, 1, st);
+        h2d_coeff<T>(w.bf.p + inst * n, p, P.plan.perm, 1, st);
+        h2d_coeff<T>(w.bf.q + inst * n, q, P.plan.perm, 1, st);
         h2d_conv<T>(w.bf.a_prev2 + inst * A, a_prev2, A, st);
         h2d_conv<T>(w.bf.a_prev + inst * A, a_prev, A, st);
         Carry cr{sc[0], sc[1], 0.0, sc[2] != 0.0 ? 1 : 0, 0, 0, 0};
@@ -1254,7 +1371,7 @@ void Engine::sync_check() {
         if (s) throw std::runtime_error("pcg_solve: non-finite scalar (indefinite operator?)");
 }
 
-int Engine::launches_per_step() const { return p_->persistent ? 1 : 4 + 3 * p_->gp.iters; }
+int Engine::launches_per_step() const { return 5 + 4 * p_->gp.iters; }
 
 int Engine::profile_step(float* ms, int* kinds, int max) {
     auto& P = *p_;
@@ -1271,8 +1388,7 @@ int Engine::profile_step(float* ms, int* kinds, int max) {
     return P.precision == 64 ? P.profile_frame<double>(ms, kinds, max) : P.profile_frame<float>(ms, kinds, max);
 }
 
-// Micro-benchmark of one layer transform kernel: single-CTA (variant 1, `threads`)
-// or cluster-distributed (variant 0).  Returns mean ms per launch over `reps`.
+// Micro-benchmark of the cluster layer transform kernel (variant, threads: unused).  Returns mean ms per launch over `reps`.
 float Engine::bench_dwt(int variant, int inverse, int reps, int threads) {
     auto& P = *p_;
     CK(cudaSetDevice(P.device));
@@ -1282,13 +1398,7 @@ float Engine::bench_dwt(int variant, int inverse, int reps, int threads) {
         if (w.count < 1) w.alloc(P.gp, 1, P.fr, false);
         Bufs<T> bf = w.bf;
         auto once = [&] {
-            if (variant == 1) {
-#define FEWHA_DS(N) CK((launch_dwt_single<T, N>(P.gp, inverse ? w.in : bf.y, inverse ? bf.phi : w.out, inverse, 1, threads, P.stream)))
-                FEWHA_FLEN_SWITCH(P.flen, FEWHA_DS)
-#undef FEWHA_DS
-            } else {
-                Launch<T>::cl(P.flen, inverse != 0, P.gp, bf, kPlain, 0, 1, P.stream, 0);
-            }
+            Launch<T>::cl(P.flen, inverse != 0, P.gp, bf, kPlain, 0, 1, P.stream, 0);
         };
         for (int i = 0; i < 3; ++i) once();
         cudaEvent_t a, b;
@@ -1367,10 +1477,9 @@ void Engine::apply_M(const double* in, double* out, int count) {
     auto& P = *p_;
     FEWHA_DISPATCH({
         with_ops<T>(P, count, [&](Work<T>& w) {
-            const size_t n = static_cast<size_t>(P.gp.n) * count;
-            h2d_conv<T>(w.in, in, n, P.stream);
+            h2d_coeff<T>(w.in, in, P.plan.perm, count, P.stream);
             P.apply_M_dev<T>(w, count, P.stream, P.gp);
-            d2h_conv<T>(out, w.out, n, P.stream);
+            d2h_coeff<T>(out, w.out, P.plan.perm, count, P.stream);
         });
     })
 }
@@ -1382,8 +1491,9 @@ void Engine::build_rhs(const double* meas, double* out, int count) {
             CK(cudaMemcpy(w.meas, meas, sizeof(double) * P.gp.S * count, cudaMemcpyHostToDevice));
             Bufs<T> bf = w.bf;
             Launch<T>::wfs(true, P.gp, bf, 0, count, P.stream);
+            Launch<T>::gather(P.gp, bf, count, P.stream);
             Launch<T>::cl(P.flen, false, P.gp, bf, kPlain, 0, count, P.stream);
-            d2h_conv<T>(out, w.out, static_cast<size_t>(P.gp.n) * count, P.stream);
+            d2h_coeff<T>(out, w.out, P.plan.perm, count, P.stream);
         });
     })
 }
@@ -1420,7 +1530,7 @@ void Engine::fit(const double* c, double* a, int count) {
     auto& P = *p_;
     FEWHA_DISPATCH({
         with_ops<T>(P, count, [&](Work<T>& w) {
-            h2d_conv<T>(w.in, c, static_cast<size_t>(P.gp.n) * count, P.stream);
+            h2d_coeff<T>(w.in, c, P.plan.perm, count, P.stream);
             Bufs<T> bf = w.bf;
             Launch<T>::cl(P.flen, true, P.gp, bf, kPlain, 0, count, P.stream);
             Launch<T>::fit(P.gp, bf, 0, count, P.stream);
@@ -1436,13 +1546,13 @@ void Engine::wavelet(int inverse, double* data, int count) {
             const size_t n = static_cast<size_t>(P.gp.n) * count;
             Bufs<T> bf = w.bf;
             if (inverse) {
-                h2d_conv<T>(w.in, data, n, P.stream);
+                h2d_coeff<T>(w.in, data, P.plan.perm, count, P.stream);
                 Launch<T>::cl(P.flen, true, P.gp, bf, kPlain, 0, count, P.stream);
                 d2h_conv<T>(data, bf.phi, n, P.stream);
             } else {
                 h2d_conv<T>(bf.y, data, n, P.stream);
-                Launch<T>::cl(P.flen, false, P.gp, bf, kPlain, 0, count, P.stream, /*gather=*/0);
-                d2h_conv<T>(data, w.out, n, P.stream);
+                Launch<T>::cl(P.flen, false, P.gp, bf, kPlain, 0, count, P.stream, /*fit_term=*/0);
+                d2h_coeff<T>(data, w.out, P.plan.perm, count, P.stream);
             }
         });
     })
@@ -1464,7 +1574,7 @@ void Engine::propagate_transpose(const double* wf, double* layers, int count) {
     FEWHA_DISPATCH({
         with_ops<T>(P, count, [&](Work<T>& w) {
             h2d_conv<T>(w.bf.psi, wf, static_cast<size_t>(P.gp.Nw) * count, P.stream);
-            Launch<T>::adjoint(P.gp, w.bf.psi, w.bf.y, count, P.stream);
+            Launch<T>::gather(P.gp, w.bf, count, P.stream);
             d2h_conv<T>(layers, w.bf.y, static_cast<size_t>(P.gp.n) * count, P.stream);
         });
     })

@@ -13,20 +13,9 @@ namespace fewha_gpu {
 
 template <typename T, int FLEN>
 cudaError_t launch_layer_cluster(bool inverse, const GeoParams& gp, const Bufs<T>& bf, int mode, int it, int count,
-                                 cudaStream_t st, int gather, size_t smem);
+                                 cudaStream_t st, int fit_term, size_t smem);
 
 template <typename T, int FLEN>
 cudaError_t set_layer_cluster_attrs(size_t smem_inv, size_t smem_fwd);
-
-template <typename T, int FLEN>
-cudaError_t launch_frame_persistent(const GeoParams& gp, const Bufs<T>& bf, unsigned int* bar, cudaStream_t st,
-                                    size_t smem);
-
-template <typename T, int FLEN>
-cudaError_t frame_persistent_fits(const GeoParams& gp, size_t smem, int* ok);
-
-template <typename T, int FLEN>
-cudaError_t launch_dwt_single(const GeoParams& gp, const T* in, T* out, int inverse, int count, int threads,
-                              cudaStream_t st);
 
 }  // namespace fewha_gpu

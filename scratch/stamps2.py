@@ -1,7 +1,7 @@
 import sys; sys.path.insert(0, '.')
 import numpy as np
 import paper_2009_00946_b200 as fg
-rec = fg.Reconstructor("presets/elt_mcao84.json", precision=64)
+rec = fg.Reconstructor("presets/elt_mcao84_3dm.json", precision=64)
 rec.build_preconditioner()
 s = np.random.default_rng(0).standard_normal(rec.dims.S) * 0.01
 for _ in range(3): rec.step(s)

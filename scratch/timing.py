@@ -1,7 +1,7 @@
 import sys, time; sys.path.insert(0, '.')
 import numpy as np, torch
 import paper_2009_00946_b200 as fg
-rec = fg.Reconstructor("presets/elt_mcao84.json")
+rec = fg.Reconstructor("presets/elt_mcao84_3dm.json")
 rec.build_preconditioner()
 S = rec.dims.S
 s = np.random.default_rng(0).standard_normal(S) * 0.01

@@ -309,3 +309,60 @@ def test_lnem_loop_vs_oracle(name, precision):
         assert rel_err(g.coeffs(), c_o) <= tol, ("c", k)
         assert rel_err(a_g, a_o) <= tol, ("a", k)
         assert rel_err(g.last_rho, rho_o) <= (tol if precision == 64 else 1e-3), ("rho", k)
+
+
+def _variant(tmp_path, base, name, orders=None, wavelet=None):
+    j = json.load(open(preset(base + ".json")))
+    if orders is not None:
+        for lay, J in zip(j["layers"], orders):
+            lay["grid_order"] = J
+    if wavelet is not None:
+        j["solver"]["wavelet_order"] = wavelet
+    p = tmp_path / f"{name}.json"
+    p.write_text(json.dumps(j))
+    return str(p)
+
+
+# Layer sides below the cluster's (tail-only and short distributed layers), Haar
+# (no halo) and long filters (halo rows wrapping the whole cluster ring).
+TRANSFORM_VARIANTS = {
+    "elt_mixed_db10": ("elt_mcao84", [7, 6, 6, 5, 7, 6, 5, 7, 7], 10),
+    "elt_mixed_haar": ("elt_mcao84", [7, 6, 6, 5, 7, 6, 5, 7, 7], 1),
+    "elt_db6": ("elt_mcao84", None, 6),
+    "small_mixed_db4": ("small_mcao", [5, 4, 2], 4),
+    "small_mixed_db2": ("small_mcao", [5, 3, 1], 2),
+}
+
+
+@pytest.mark.parametrize("case", sorted(TRANSFORM_VARIANTS))
+def test_transforms_mixed_sides_and_orders(case, tmp_path, precision):
+    base, orders, wav = TRANSFORM_VARIANTS[case]
+    path = _variant(tmp_path, base, case, orders, wav)
+    try:
+        g = fg.Reconstructor(path, precision=precision)
+    except fg.ConfigError as e:
+        pytest.skip(f"geometry not supported by the gather tables: {e}")
+    o = Oracle(path)
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal(o.dims.n)
+    m = rng.standard_normal(o.dims.S)
+    tol = OP_TOL[precision]
+    checks = {
+        "W^-1": (g.wavelet(x, True), o.wavelet(x, True)),
+        "W": (g.wavelet(x, False), o.wavelet(x, False)),
+        "M": (g.apply_M(x), o.apply_M(x)),
+        "rhs": (g.build_rhs(m), o.build_rhs(m)),
+    }
+    bad = {k: rel_err(u, v) for k, (u, v) in checks.items() if not rel_err(u, v) <= tol}
+    assert not bad, bad
+    if precision == 64:
+        # a short closed loop through the fused PCG kernels
+        o.build_preconditioner()
+        g.build_preconditioner()
+        lay = smooth_layers(o, 3)
+        for k in range(3):
+            s = noisy_slopes(o, lay, 100 + k, o.get_state()["a_prev2"])
+            a_g = g.step(s)
+            c_o, a_o, rho_o = o.step(s)
+            assert rel_err(g.coeffs(), c_o) <= STEP_TOL[64], ("c", k, rel_err(g.coeffs(), c_o))
+            assert rel_err(a_g, a_o) <= STEP_TOL[64], ("a", k, rel_err(a_g, a_o))
