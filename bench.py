@@ -336,10 +336,10 @@ def run_ours(args):
         flush.zero_()
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
-        rc = lib.fewha_gpu_step(rec._h, C.cast(pin_s[k % F].data_ptr(), dp), None, C.cast(pin_a.data_ptr(), dp),
-                                C.cast(pin_rho.data_ptr(), dp), nr)
+        code = lib.fewha_gpu_step(rec._h, C.cast(pin_s[k % F].data_ptr(), dp), None, C.cast(pin_a.data_ptr(), dp),
+                                  C.cast(pin_rho.data_ptr(), dp), nr)
         t1 = time.perf_counter()
-        rec._chk(rc)
+        rec._chk(code)
         if k >= max(args.warmup, 3):
             e2e_ms.append((t1 - t0) * 1000.0)
     e2e_ms = np.array(e2e_ms)
