@@ -541,7 +541,8 @@ __device__ void gather_group(const GeoParams& gp, const T* __restrict__ psi_b, i
     const int i0 = grp * rows_pt;
     const bool worker = grp < groups;
     const int gst = kGatherRows * gp.bd_cols_max;  // G stride per WFS
-    const int o_rw = align16(R * KM * 2), o_f = o_rw + align16(R * KM * static_cast<int>(sizeof(T)));
+    const int km = KM > 0 ? KM : gp.gather_km;  // taps per row in the staged tables
+    const int o_rw = align16(R * km * 2), o_f = o_rw + align16(R * km * static_cast<int>(sizeof(T)));
     const int o_idx = o_f + align16((side + 3) * 2);
     T out[kGatherRows];
 #pragma unroll
@@ -573,8 +574,12 @@ __device__ void gather_group(const GeoParams& gp, const T* __restrict__ psi_b, i
                 const int i = e >> lc, c = e & (cp - 1);
                 if (c >= nc) continue;
                 T g = T(0);
+                if constexpr (KM > 0) {
 #pragma unroll
-                for (int q = 0; q < KM; ++q) g += rw[i * KM + q] * blk[rs[i * KM + q] * np + c];
+                    for (int q = 0; q < KM; ++q) g += rw[i * KM + q] * blk[rs[i * KM + q] * np + c];
+                } else {  // dense aperture sampling of a coarse layer: runtime tap count
+                    for (int q = 0; q < km; ++q) g += rw[i * km + q] * blk[rs[i * km + q] * np + c];
+                }
                 G[i * nc + c] = g;
             }
         }
@@ -591,10 +596,24 @@ __device__ void gather_group(const GeoParams& gp, const T* __restrict__ psi_b, i
                 const T* cfr = reinterpret_cast<const T*>(tp + o_idx + align16(nc * 2));
                 const T* G = gbuf + (w - w0) * gst;
                 const int c0 = first[J], c1 = first[J + 2];
-                T wt[KM];
-                int cc[KM];
+                if constexpr (KM == 0) {
+                    for (int k2 = 0; k2 < kGatherRows; ++k2) {
+                        if (k2 >= rows_pt) break;
+                        const T* g = G + (i0 + k2) * nc;
+                        T s = T(0);
+                        for (int c = c0; c < c1; ++c) {
+                            const T fr = cfr[c];
+                            s += (cidx[c] == J ? T(1) - fr : fr) * g[c];
+                        }
+                        out[k2] += s;
+                    }
+                    continue;
+                }
+                constexpr int KQ = KM > 0 ? KM : 1;
+                T wt[KQ];
+                int cc[KQ];
 #pragma unroll
-                for (int q = 0; q < KM; ++q) {
+                for (int q = 0; q < KQ; ++q) {
                     const int c = min(c0 + q, nc - 1);
                     const T fr = cfr[c];
                     wt[q] = c0 + q < c1 ? (cidx[c] == J ? T(1) - fr : fr) : T(0);
@@ -606,7 +625,7 @@ __device__ void gather_group(const GeoParams& gp, const T* __restrict__ psi_b, i
                     const T* g = G + (i0 + k2) * nc;
                     T s = T(0);
 #pragma unroll
-                    for (int q = 0; q < KM; ++q) s += wt[q] * g[cc[q]];
+                    for (int q = 0; q < KQ; ++q) s += wt[q] * g[cc[q]];
                     out[k2] += s;
                 }
             }
@@ -665,7 +684,8 @@ __global__ void __launch_bounds__(256, 2) k_gather(const GeoParams gp, const Buf
         case 1: gather_group<T, 1>(gp, psi, l, y, gbuf, stage, s_desc, &s_mbar); break;
         case 2: gather_group<T, 2>(gp, psi, l, y, gbuf, stage, s_desc, &s_mbar); break;
         case 3: gather_group<T, 3>(gp, psi, l, y, gbuf, stage, s_desc, &s_mbar); break;
-        default: gather_group<T, 4>(gp, psi, l, y, gbuf, stage, s_desc, &s_mbar); break;
+        case 4: gather_group<T, 4>(gp, psi, l, y, gbuf, stage, s_desc, &s_mbar); break;
+        default: gather_group<T, 0>(gp, psi, l, y, gbuf, stage, s_desc, &s_mbar); break;
     }
     stamp(gp, 2);
 }

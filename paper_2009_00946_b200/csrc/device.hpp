@@ -18,7 +18,6 @@ constexpr int kMaxL = 16;
 constexpr int kMaxW = 16;
 constexpr int kMaxM = 16;
 constexpr int kMaxC = 8;  // CTAs per layer cluster (portable cluster size)
-constexpr int kGatherKMax = 4;  // max bilinear-gather taps per layer node per axis
 constexpr int kGatherRows = 4;  // layer rows per CTA of the adjoint-propagation gather
 constexpr int kMaxGU = 32;      // row groups per layer (max side 128 / kGatherRows)
 
@@ -63,7 +62,6 @@ struct GeoParams {
     int o_tr;  // [(tile*W + w)*4] psi source block {ilo, ihi, jlo, jhi} of each layer tile (into ti)
     // v2 cluster path
     int ccl;          // CTAs per layer cluster
-    int o_pg;         // [(w*L+l)*2 + {0 rows, 1 cols}] -> gather table: cnt[side], src[side*KM] (ti), wgt (td/tf)
     int gather_km;    // max gather taps per layer row/column
     int o_bs;         // [((w*L+l)*kMaxGU + u)*4] psi source block {ilo, ihi, jlo, jhi} of each gather row group
     int bd_rows_max, bd_cols_max;

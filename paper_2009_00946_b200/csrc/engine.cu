@@ -401,37 +401,8 @@ Plan build_plan(const Geometry& g, int elem_bytes) {
                 cols[w * L + l] = build(tx);
                 colst[w * L + l] = tx;
             }
-        if (km > kGatherKMax)
-            throw ConfigError("invalid geometry: aperture sampling denser than the layer grid allows (gather taps " +
-                              std::to_string(km) + " > " + std::to_string(kGatherKMax) + ")");
+        // (km > 4: coarse layers under dense aperture sampling take the runtime-tap path)
         gp.gather_km = km;
-        // padded tables: [side][kGatherKMax] (src in ti, weight in td); padding repeats the last
-        // valid source (or the nearest non-empty node's) with weight 0 so tables stay monotone
-        gp.o_pg = static_cast<int>(pl.ti.size());
-        pl.ti.resize(pl.ti.size() + static_cast<size_t>(W * L * 2), 0);
-        pl.td.resize(pl.ti.size(), 0.0);
-        for (int p = 0; p < W * L; ++p) {
-            for (int axis = 0; axis < 2; ++axis) {
-                const auto& tab = axis == 0 ? rows[p] : cols[p];
-                const int side = static_cast<int>(tab.size());
-                const int off = static_cast<int>(pl.ti.size());
-                pl.ti[static_cast<size_t>(gp.o_pg + p * 2 + axis)] = off;
-                pl.ti.resize(pl.ti.size() + static_cast<size_t>(side) * kGatherKMax, 0);
-                pl.td.resize(pl.ti.size(), 0.0);
-                int first_src = 0;
-                for (const auto& v : tab)
-                    if (!v.empty()) { first_src = v.front().src; break; }
-                int carry = first_src;
-                for (int I = 0; I < side; ++I) {
-                    for (int q = 0; q < kGatherKMax; ++q) {
-                        const bool valid = q < static_cast<int>(tab[I].size());
-                        if (valid) carry = tab[I][q].src;
-                        pl.ti[off + I * kGatherKMax + q] = carry;
-                        pl.td[off + I * kGatherKMax + q] = valid ? tab[I][q].w : 0.0;
-                    }
-                }
-            }
-        }
         // psi source blocks per (w, l, gather row group u)
         auto grp_rows = [](int side) { return std::min(kGatherRows, side); };
         gp.o_bs = static_cast<int>(pl.ti.size());
