@@ -79,7 +79,8 @@ def kernel_bytes(kind, d, b):
     n, S, Nw, A = d["n"], d["S"], d["Nw"], d["A"]
     return {
         "wfs_rhs": 8 * S + b * (A + Nw),          # slopes (fp64) + a_prev2 -> psi
-        "adjoint": b * (Nw + n),                  # psi -> y
+        "adjoint": b * (Nw + n),                  # psi -> y (legacy kind id)
+        "gather": b * (Nw + n),                   # psi -> y (k_gather)
         "fwd_rhs": b * (3 * n + 2 * n),           # y, r, b -> r, b
         "inv_pcg0": b * (2 * n + n),              # r, J -> phi
         "inv_pcg": b * (6 * n + 4 * n + n),       # r, J, p, q, c, Mz -> p, q, c, r, phi
