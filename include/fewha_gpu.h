@@ -150,6 +150,31 @@ int fewha_gpu_sh_transpose(fewha_gpu_t h, const double* meas, double* wf, int co
  * a may be NULL (no correction).  layers: nodal [count][n]. */
 int fewha_gpu_forward_slopes(fewha_gpu_t h, const double* layers, const double* a, double* meas, int count);
 
+/* --- per-WFS sharding (the north star's multi-GPU split) -------
+ * Shard `rank` of `world` owns a contiguous WFS range, balanced by wavefront
+ * nodes: its WFS kernels (Gamma, C^-1, P) run only those WFS and its adjoint
+ * gather sums only their P^T psi.  The partial layer sums are all-reduced after
+ * the RHS and after every apply_M (iters+1 exchanges per frame); everything else
+ * (W, W^-1, alpha D, Jacobi, dots, updates, fit) is replicated and stays bitwise
+ * identical on every shard.  Not in the reference (its solver is single-node,
+ * SPEC.md:381); it replaces the per-WFS loop inside apply_M (reconstructor.hpp:
+ * 180-195) and build_rhs (:222-240) across processes. */
+/* host only: the WFS range [begin, end) of shard rank/world of a preset */
+int fewha_gpu_shard_range(const char* preset_json_path, int rank, int world, int* wfs_begin, int* wfs_end);
+/* a fresh 128-byte ncclUniqueId (rank 0 creates it and broadcasts it) */
+int fewha_gpu_nccl_unique_id(unsigned char* id);
+/* Make h shard rank/world.  nccl_id (128 bytes): join a multi-process NCCL
+ * exchange (one process per GPU; the frame graph captures ncclAllReduce).
+ * nccl_id NULL and world > 1: member of an in-process group, stepped only by
+ * fewha_gpu_group_step_device.  world 1 with an id runs the NCCL path alone. */
+int fewha_gpu_shard(fewha_gpu_t h, int rank, int world, const unsigned char* nccl_id);
+int fewha_gpu_shard_wfs(fewha_gpu_t h, int* wfs_begin, int* wfs_end);
+/* One frame of an in-process group (members[r] = shard r, each with its own
+ * slopes slot and stream): segments in lockstep, each exchange a fixed
+ * rank-order sum of the members' partial layer sums read directly from their
+ * buffers (peer loads across devices).  Asynchronous; fewha_gpu_sync each. */
+int fewha_gpu_group_step_device(fewha_gpu_t* members, int world);
+
 #ifdef __cplusplus
 }
 #endif

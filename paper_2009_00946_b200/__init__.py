@@ -34,7 +34,8 @@ EXPORTS = (
     "fewha_gpu_load_slopes", "fewha_gpu_step_device", "fewha_gpu_sync", "fewha_gpu_launches_per_step", "fewha_gpu_profile_step", "fewha_gpu_phase_stamps", "fewha_gpu_apply_M",
     "fewha_gpu_build_rhs", "fewha_gpu_add_dm_slopes", "fewha_gpu_fit_to_mirrors", "fewha_gpu_wavelet",
     "fewha_gpu_propagate", "fewha_gpu_propagate_transpose", "fewha_gpu_sh", "fewha_gpu_sh_transpose",
-    "fewha_gpu_forward_slopes",
+    "fewha_gpu_forward_slopes", "fewha_gpu_shard_range", "fewha_gpu_nccl_unique_id", "fewha_gpu_shard",
+    "fewha_gpu_shard_wfs", "fewha_gpu_group_step_device",
 )
 
 
@@ -125,6 +126,12 @@ def lib() -> C.CDLL:
             getattr(L, "fewha_gpu_" + name).argtypes = [vp, dp, dp, C.c_int]
         L.fewha_gpu_wavelet.argtypes = [vp, C.c_int, dp, C.c_int]
         L.fewha_gpu_forward_slopes.argtypes = [vp, dp, dp, dp, C.c_int]
+        ip = C.POINTER(C.c_int)
+        L.fewha_gpu_shard_range.argtypes = [C.c_char_p, C.c_int, C.c_int, ip, ip]
+        L.fewha_gpu_nccl_unique_id.argtypes = [C.c_char_p]
+        L.fewha_gpu_shard.argtypes = [vp, C.c_int, C.c_int, C.c_char_p]
+        L.fewha_gpu_shard_wfs.argtypes = [vp, ip, ip]
+        L.fewha_gpu_group_step_device.argtypes = [C.POINTER(vp), C.c_int]
         _lib_handle = L
     return _lib_handle
 
@@ -138,6 +145,34 @@ def _f64(a, n=None):
     if n is not None and a.size != n:
         raise ArgumentError(f"expected {n} values, got {a.size}")
     return a
+
+
+def _raise_create(rc):
+    if rc != FEWHA_OK:
+        raise _ERR.get(rc, FewhaError)(lib().fewha_gpu_create_error().decode())
+
+
+def shard_range(preset, rank: int, world: int) -> tuple[int, int]:
+    """WFS range [begin, end) owned by shard rank/world (host only, no device):
+    contiguous ranges minimising the largest per-shard wavefront node count."""
+    b, e = C.c_int(), C.c_int()
+    _raise_create(lib().fewha_gpu_shard_range(os.fspath(preset).encode(), rank, world, C.byref(b), C.byref(e)))
+    return b.value, e.value
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh 128-byte ncclUniqueId (rank 0 makes it, every rank passes it to shard())."""
+    buf = C.create_string_buffer(128)
+    _raise_create(lib().fewha_gpu_nccl_unique_id(buf))
+    return buf.raw
+
+
+def group_step_device(members) -> None:
+    """One frame of an in-process shard group (members[r] is shard r of len(members))."""
+    arr = (C.c_void_p * len(members))(*[m._h for m in members])
+    rc = lib().fewha_gpu_group_step_device(arr, len(members))
+    if rc != FEWHA_OK:
+        raise _ERR.get(rc, FewhaError)(lib().fewha_gpu_last_error(members[0]._h).decode())
 
 
 @dataclass
@@ -319,6 +354,18 @@ class Reconstructor:
         return out if count == 1 else out.reshape(count, self.dims.S)
 
     # -- CUDA-resident path -----------------------------------------------------------
+    def shard(self, rank: int, world: int, nccl_id: bytes | None = None):
+        """Own the WFS of shard rank/world.  nccl_id: multi-process
+        NCCL exchange of the partial layer sums; None: in-process group member."""
+        if nccl_id is not None and len(nccl_id) != 128:
+            raise ArgumentError("nccl_id must be 128 bytes")
+        self._chk(self._L.fewha_gpu_shard(self._h, rank, world, nccl_id))
+
+    def shard_wfs(self) -> tuple[int, int]:
+        b, e = C.c_int(), C.c_int()
+        self._chk(self._L.fewha_gpu_shard_wfs(self._h, C.byref(b), C.byref(e)))
+        return b.value, e.value
+
     def set_stream(self, stream_handle: int):
         self._chk(self._L.fewha_gpu_set_stream(self._h, C.c_void_p(stream_handle)))
 
@@ -326,6 +373,12 @@ class Reconstructor:
         b = _DevBufs()
         self._chk(self._L.fewha_gpu_device_buffers(self._h, C.byref(b)))
         return {k: getattr(b, k) for k, _ in _DevBufs._fields_}
+
+    def load_slopes(self, slopes):
+        """Stage host slopes [batch][S] into the resident slot (synchronous copy)."""
+        s = _f64(slopes, self.dims.S * self.dims.batch)
+        self._chk(self._L.fewha_gpu_load_slopes(self._h, s.ctypes.data_as(C.c_void_p), 0))
+        self.sync()
 
     def load_slopes_device(self, d_ptr: int):
         """Stage device slopes [batch][S] fp64 into the resident slot (async)."""

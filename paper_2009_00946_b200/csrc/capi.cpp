@@ -7,8 +7,10 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <vector>
 
 #include "engine.hpp"
+#include "nccl_dl.hpp"
 
 using fewha_gpu::ArgError;
 using fewha_gpu::ConfigError;
@@ -222,6 +224,50 @@ int fewha_gpu_sh_transpose(fewha_gpu_t h, const double* meas, double* wf, int co
 }
 int fewha_gpu_forward_slopes(fewha_gpu_t h, const double* layers, const double* a, double* meas, int count) {
     H_GUARD(h->eng->forward_slopes(layers, a, meas, count))
+}
+
+// ---- per-WFS sharding ----
+int fewha_gpu_shard_range(const char* path, int rank, int world, int* wfs_begin, int* wfs_end) {
+    if (!path) return FEWHA_ARG;
+    return guard(g_create_error, [&] {
+        const auto r = fewha_gpu::shard_range(fewha_gpu::parse_preset_file(path), rank, world);
+        if (wfs_begin) *wfs_begin = r.first;
+        if (wfs_end) *wfs_end = r.second;
+    });
+}
+
+int fewha_gpu_nccl_unique_id(unsigned char* id) {
+    if (!id) return FEWHA_ARG;
+    return guard(g_create_error, [&] {
+        const auto& api = fewha_gpu::NcclApi::get();
+        ncclUniqueId u;
+        api.check(api.GetUniqueId(&u), "ncclGetUniqueId");
+        static_assert(sizeof(u) == 128, "ncclUniqueId is 128 bytes");
+        std::memcpy(id, &u, sizeof(u));
+    });
+}
+
+int fewha_gpu_shard(fewha_gpu_t h, int rank, int world, const unsigned char* nccl_id) {
+    H_GUARD(h->eng->shard(rank, world, nccl_id))
+}
+
+int fewha_gpu_shard_wfs(fewha_gpu_t h, int* wfs_begin, int* wfs_end) {
+    H_GUARD({
+        const auto r = h->eng->shard_wfs();
+        if (wfs_begin) *wfs_begin = r.first;
+        if (wfs_end) *wfs_end = r.second;
+    })
+}
+
+int fewha_gpu_group_step_device(fewha_gpu_t* members, int world) {
+    if (!members || world < 1) return FEWHA_ARG;
+    for (int r = 0; r < world; ++r)
+        if (!members[r]) return FEWHA_ARG;
+    return guard(members[0]->err, [&] {
+        std::vector<Engine*> m;
+        for (int r = 0; r < world; ++r) m.push_back(members[r]->eng.get());
+        fewha_gpu::group_step_device(m);
+    });
 }
 
 }  // extern "C"

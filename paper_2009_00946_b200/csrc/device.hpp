@@ -55,11 +55,10 @@ struct GeoParams {
     int n_wtiles, wtile;
     int wt_first[kMaxW + 1];  // first tile of each WFS (prefix), tiles row-major per WFS
     int wt_cols[kMaxW];       // tiles per row of WFS w
+    int wa, wb;               // WFS owned by this plan's per-WFS kernels (all unless sharded)
+    int wt_base, wt_count;    // their tiles: [wt_base, wt_base + wt_count)
     const unsigned char* tblob;  // per-tile stencil tables [tile][screen][axis][H] idx, then weights
     int tt_stride_l, tt_stride_d, tt_off_d;  // byte stride per tile (layer / DM screens), DM base
-    const int* ltiles;  // [n_ltiles][3] (l, I0, J0) for the adjoint-propagation kernel
-    int n_ltiles, ltile, lt_rows_max, lt_cols_max;
-    int o_tr;  // [(tile*W + w)*4] psi source block {ilo, ihi, jlo, jhi} of each layer tile (into ti)
     // v2 cluster path
     int ccl;          // CTAs per layer cluster
     int gather_km;    // max gather taps per layer row/column
@@ -86,7 +85,7 @@ enum LayerMode : int {
 // kernel kinds reported by fewha_gpu_profile_step
 enum KernelKind : int {
     kKindWfsRhs = 0,   // k_wfs<RHS>: Gamma^T C^-1 (s + Gamma P_dm a)
-    kKindAdjoint = 1,  // k_adjoint: sum_w P^T psi
+    kKindAdjoint = 1,  // (unused id: the adjoint is k_gather, kKindGather)
     kKindFwdRhs = 2,   // k_layer_forward kRhs: b1 = W y, r += b1 - b
     kKindInvPcg0 = 3,  // k_layer_inverse kPcg it=0: z = r/J, W^-1 z
     kKindInvPcg = 4,   // k_layer_inverse kPcg it>0: fused p,q,c,r update + z + W^-1 z

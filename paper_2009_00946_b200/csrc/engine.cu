@@ -19,6 +19,7 @@
 #include "cluster.cuh"
 #include "clayout.hpp"
 #include "launch.hpp"
+#include "nccl_dl.hpp"
 
 namespace fewha_gpu {
 
@@ -57,7 +58,7 @@ struct Plan {
     std::vector<int> ti;
     std::vector<double> td;
     std::vector<std::uint8_t> masks;
-    std::vector<int> wtiles, ltiles;
+    std::vector<int> wtiles;
     std::vector<unsigned char> gblob, tblob;
     std::vector<int> perm;  // Mallat coefficient index -> rank-blocked HBM index (clayout.hpp)
     int maxside = 0;
@@ -123,13 +124,20 @@ int push_ranges(Plan& pl, const std::vector<Stencil1>& t, int n_target) {
     return off;
 }
 
-Plan build_plan(const Geometry& g, int elem_bytes) {
+// wa..wb: the WFS this plan's per-WFS kernels own (all of them unless sharded,
+// SURVEY 8e): the WFS kernels run only those tiles and the adjoint gather sums
+// only those WFS.
+Plan build_plan(const Geometry& g, int elem_bytes, int wa = 0, int wb = -1) {
     Plan pl;
     GeoParams& gp = pl.gp;
     const int L = static_cast<int>(g.layers.size()), W = static_cast<int>(g.wfs.size()),
               M = static_cast<int>(g.dms.size());
     if (L > kMaxL || W > kMaxW || M > kMaxM)
         throw ConfigError("invalid geometry: at most 16 layers, 16 wfs and 16 dms are supported on the device");
+    if (wb < 0) wb = W;
+    if (wa < 0 || wa >= wb || wb > W) throw ArgError("shard: empty or out-of-range WFS range");
+    gp.wa = wa;
+    gp.wb = wb;
     gp.L = L;
     gp.W = W;
     gp.M = M;
@@ -285,6 +293,8 @@ Plan build_plan(const Geometry& g, int elem_bytes) {
     }
     gp.n_wtiles = static_cast<int>(pl.wtiles.size() / 3);
     gp.wt_first[W] = gp.n_wtiles;
+    gp.wt_base = gp.wt_first[wa];
+    gp.wt_count = gp.wt_first[wb] - gp.wt_first[wa];
     // per-tile stencil tables of the tile's halo rows/columns for every screen, in the
     // shared-memory layout of wfs_tile (kernels.cuh): [screen][axis][H] idx | [screen][axis][H] weight
     {
@@ -324,52 +334,6 @@ Plan build_plan(const Geometry& g, int elem_bytes) {
         gp.tt_stride_d = static_cast<int>(td_.second);
         gp.tt_off_d = static_cast<int>(td_.first);
     }
-
-    // layer tiles for the adjoint gather; shrink until the psi block fits.
-    // Per (tile, WFS) the exact source block: union of the per-node ranges.
-    std::vector<int> tr;
-    for (int tp : {32, 16, 8, 4, 2}) {
-        gp.ltile = tp;
-        pl.ltiles.clear();
-        tr.clear();
-        int rows_max = 1, cols_max = 1;
-        for (int l = 0; l < L; ++l) {
-            const int side = gp.side[l];
-            for (int I0 = 0; I0 < side; I0 += tp)
-                for (int J0 = 0; J0 < side; J0 += tp) {
-                    pl.ltiles.insert(pl.ltiles.end(), {l, I0, J0});
-                    const int nI = std::min(tp, side - I0), nJ = std::min(tp, side - J0);
-                    for (int w = 0; w < W; ++w) {
-                        const int* dir = &pl.ti[static_cast<size_t>((w * L + l) * 4)];
-                        auto span = [&](int ranges, int a0, int cnt) {
-                            int lo = INT32_MAX, hi = 0;
-                            for (int a = a0; a < a0 + cnt; ++a) {
-                                const int rl = pl.ti[ranges + 2 * a], rh = pl.ti[ranges + 2 * a + 1];
-                                if (rl < rh) {
-                                    lo = std::min(lo, rl);
-                                    hi = std::max(hi, rh);
-                                }
-                            }
-                            return lo < hi ? std::pair<int, int>{lo, hi} : std::pair<int, int>{0, 0};
-                        };
-                        const auto [ilo, ihi] = span(dir[2], I0, nI);
-                        const auto [jlo, jhi] = span(dir[3], J0, nJ);
-                        const bool hit = ilo < ihi && jlo < jhi;
-                        tr.insert(tr.end(), {hit ? ilo : 0, hit ? ihi : 0, hit ? jlo : 0, hit ? jhi : 0});
-                        if (!hit) continue;
-                        rows_max = std::max(rows_max, ihi - ilo);
-                        cols_max = std::max(cols_max, jhi - jlo);
-                    }
-                }
-        }
-        gp.lt_rows_max = rows_max;
-        gp.lt_cols_max = cols_max;
-        const size_t bytes = static_cast<size_t>(rows_max) * (cols_max + tp) * elem_bytes;
-        if (bytes <= 160 * 1024 && tp * tp <= 256 * 16) break;
-    }
-    gp.o_tr = static_cast<int>(pl.ti.size());
-    pl.ti.insert(pl.ti.end(), tr.begin(), tr.end());
-    pl.td.resize(pl.ti.size(), 0.0);
 
     // ---- cluster path: C = maxside / min(16, maxside) CTAs per layer; band rows per rank: clayout.hpp
     {
@@ -472,9 +436,9 @@ Plan build_plan(const Geometry& g, int elem_bytes) {
         const size_t limit = 110 * 1024;                                      // two CTAs per SM
         const size_t budget = limit > fixed ? limit - fixed : 0;
         gp.nchunk = 0;
-        gp.gchunk[0] = 0;
+        gp.gchunk[0] = wa;
         size_t used = 0, chunk_max = 0;
-        for (int w = 0; w < W; ++w) {
+        for (int w = wa; w < wb; ++w) {
             if (need_max[static_cast<size_t>(w)] > budget)
                 throw ConfigError("invalid geometry: adjoint gather does not fit in shared memory");
             if (w > gp.gchunk[gp.nchunk] && used + need_max[static_cast<size_t>(w)] > budget) {
@@ -484,7 +448,7 @@ Plan build_plan(const Geometry& g, int elem_bytes) {
             used += need_max[static_cast<size_t>(w)];
             chunk_max = std::max(chunk_max, used);
         }
-        gp.gchunk[++gp.nchunk] = W;
+        gp.gchunk[++gp.nchunk] = wb;
         gp.chunk_bytes = static_cast<int>(chunk_max);
         // gather tables per (layer, row group), WFS ascending, each WFS 16-byte aligned parts
         //   [row src int16 R x KM][row w R x KM]                  padded row taps of the group
@@ -602,6 +566,7 @@ Plan build_plan(const Geometry& g, int elem_bytes) {
         for (int l = 0; l < L; ++l)
             for (int u = 0; u < gp.side[l] / grp_rows(gp.side[l]); ++u) {
                 size_t toff = static_cast<size_t>(pl.ti[static_cast<size_t>(gp.o_gb + l * kMaxGU + u)]);
+                for (int w = 0; w < wa; ++w) toff += need_of(w, l, u).first;  // tables of WFS this plan skips
                 for (int k = 0; k < gp.nchunk; ++k) {
                     size_t tsum = 0;
                     for (int w = gp.gchunk[k]; w < gp.gchunk[k + 1]; ++w) tsum += need_of(w, l, u).first;
@@ -621,7 +586,6 @@ Plan build_plan(const Geometry& g, int elem_bytes) {
                 }
             }
     }
-    gp.n_ltiles = static_cast<int>(pl.ltiles.size() / 3);
     pl.perm = coeff_perm(gp);
     return pl;
 }
@@ -787,7 +751,7 @@ struct Launch {
     }
     static void wfs(bool rhs, const GeoParams& gp, const Bufs<T>& bf, int with_dm, int count, cudaStream_t st) {
         cudaLaunchAttribute attr[1];
-        cudaLaunchConfig_t cfg = pdl_cfg(dim3(gp.n_wtiles, count), wfs_smem(gp), st, attr, 512);
+        cudaLaunchConfig_t cfg = pdl_cfg(dim3(gp.wt_count, count), wfs_smem(gp), st, attr, 512);
         if (rhs) CK(cudaLaunchKernelEx(&cfg, k_wfs<T, true>, gp, bf, with_dm));
         else CK(cudaLaunchKernelEx(&cfg, k_wfs<T, false>, gp, bf, with_dm));
     }
@@ -815,6 +779,12 @@ struct EngineImpl {
     DevFree fr;
     GeoParams gp{};      // with device table pointers (engine precision)
     GeoParams gp64{};    // fp64 plan for the preconditioner probes (== gp in fp64 engines)
+    GeoParams gpf{};     // plan of the frame's per-WFS kernels (== gp unless sharded)
+    // per-WFS sharding: this engine owns WFS [gpf.wa, gpf.wb)
+    bool sharded = false;
+    int shard_rank = 0, shard_world = 1;
+    std::vector<void*> ypart;  // [iters+1] partial adjoint layer sums [B][n], one per exchange
+    ncclComm_t comm = nullptr;  // multi-process exchange (NCCL); null for in-process groups
     cudaStream_t stream = nullptr, user_stream = nullptr;
     bool own_stream = false;
     cudaGraphExec_t graph = nullptr;
@@ -824,7 +794,7 @@ struct EngineImpl {
     int stamp_slot = -1;  // < 0: stamping off
     static constexpr int kStampSlots = 32, kStampBlocks = 4096;
     GeoParams gps() {
-        GeoParams g2 = gp;
+        GeoParams g2 = gpf;
         if (stamp_slot >= 0 && stamp_slot < kStampSlots) {
             g2.stamps = stamp_buf + static_cast<size_t>(stamp_slot++) * kStampBlocks * 16;
         }
@@ -850,7 +820,6 @@ struct EngineImpl {
         float* tf = dalloc<float>(plan.td.size());
         std::uint8_t* mk = dalloc<std::uint8_t>(plan.masks.size());
         int* wt = dalloc<int>(plan.wtiles.size());
-        int* lt = dalloc<int>(plan.ltiles.size());
         unsigned char* gb = dalloc<unsigned char>(plan.gblob.size());
         fr.add(gb);
         unsigned char* tb = dalloc<unsigned char>(plan.tblob.size());
@@ -859,7 +828,7 @@ struct EngineImpl {
             CK(cudaMemcpy(tb, plan.tblob.data(), plan.tblob.size(), cudaMemcpyHostToDevice));
         if (!plan.gblob.empty())
             CK(cudaMemcpy(gb, plan.gblob.data(), plan.gblob.size(), cudaMemcpyHostToDevice));
-        for (void* p : {(void*)ti, (void*)td, (void*)tf, (void*)mk, (void*)wt, (void*)lt}) fr.add(p);
+        for (void* p : {(void*)ti, (void*)td, (void*)tf, (void*)mk, (void*)wt}) fr.add(p);
         std::vector<float> tdf(plan.td.begin(), plan.td.end());
         CK(cudaMemcpy(ti, plan.ti.data(), plan.ti.size() * sizeof(int), cudaMemcpyHostToDevice));
         CK(cudaMemcpy(td, plan.td.data(), plan.td.size() * sizeof(double), cudaMemcpyHostToDevice));
@@ -867,14 +836,12 @@ struct EngineImpl {
         if (!plan.masks.empty())
             CK(cudaMemcpy(mk, plan.masks.data(), plan.masks.size(), cudaMemcpyHostToDevice));
         CK(cudaMemcpy(wt, plan.wtiles.data(), plan.wtiles.size() * sizeof(int), cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(lt, plan.ltiles.data(), plan.ltiles.size() * sizeof(int), cudaMemcpyHostToDevice));
         GeoParams g = plan.gp;
         g.ti = ti;
         g.td = td;
         g.tf = tf;
         g.masks = mk;
         g.wtiles = wt;
-        g.ltiles = lt;
         g.gblob = gb;
         g.tblob = tb;
         return g;
@@ -886,37 +853,79 @@ struct EngineImpl {
     }
 
     // ---- one frame of Reconstructor::step on the state workspace ----------
+    // The frame is iters+2 segments; segments 0..iters end with an adjoint gather
+    // whose layer sums are exchanged between shards when sharded:
+    //   seg 0          RHS: Gamma^T C^-1 (s + Gamma P_dm a) -> sum P^T psi
+    //   seg 1          W (RHS, r update) | W^-1 z_0 | Gamma..P | sum P^T psi
+    //   seg k (2..it)  W (PCG k-2)       | update + W^-1 z_{k-1} | ... | sum P^T psi
+    //   seg it+1       W (PCG it-1)      | last update + W^-1 c | fit + control
     // `mark(kind)` runs after every launch (profiling hook; a no-op for capture).
-    template <typename T, typename Mark>
-    void launch_frame(cudaStream_t st, Mark&& mark) {
-        Work<T>& w = state<T>();
-        Bufs<T> bf = w.bf;
+    template <typename T>
+    Bufs<T> frame_bufs() {
+        Bufs<T> bf = state<T>().bf;
         bf.jac = static_cast<const T*>(jac);
         bf.jinv = static_cast<const T*>(jinv);
-        const int B = batch;
-        // RHS with the pseudo open-loop term (reconstructor.hpp:316-323)
-        Launch<T>::wfs(true, gps(), bf, gp.closed, B, st);
-        mark(kKindWfsRhs);
-        Launch<T>::gather(gps(), bf, B, st);
-        mark(kKindGather);
-        Launch<T>::cl(flen, false, gps(), bf, kRhs, 0, B, st);
-        mark(kKindFwdRhs);
-        // fused PCG (pcg.hpp:68-106), the update of iteration k fused into k+1's W^-1
-        for (int it = 0; it < gp.iters; ++it) {
-            Launch<T>::cl(flen, true, gps(), bf, kPcg, it, B, st);
-            mark(it == 0 ? kKindInvPcg0 : kKindInvPcg);
+        return bf;
+    }
+    int n_segments() const { return gp.iters + 2; }
+
+    template <typename T, typename Mark>
+    void launch_segment(int seg, cudaStream_t st, Mark&& mark) {
+        Bufs<T> bf = frame_bufs<T>();
+        const int B = batch, it = gp.iters;
+        auto gather = [&] {
+            Bufs<T> gb = bf;
+            if (sharded) gb.y = static_cast<T*>(ypart[static_cast<size_t>(seg)]);  // partial sums
+            Launch<T>::gather(gps(), gb, B, st);
+            mark(kKindGather);
+        };
+        if (seg == 0) {  // RHS with the pseudo open-loop term (reconstructor.hpp:316-323)
+            Launch<T>::wfs(true, gps(), bf, gp.closed, B, st);
+            mark(kKindWfsRhs);
+            gather();
+            return;
+        }
+        // W of the previous gather: the RHS (r += b1 - b) or PCG iteration seg-2
+        if (seg == 1) {
+            Launch<T>::cl(flen, false, gps(), bf, kRhs, 0, B, st);
+            mark(kKindFwdRhs);
+        } else {
+            Launch<T>::cl(flen, false, gps(), bf, kPcg, seg - 2, B, st);
+            mark(kKindFwdPcg);
+        }
+        if (seg <= it) {  // fused PCG (pcg.hpp:68-106): update of k-1 fused into k's W^-1
+            const int k = seg - 1;
+            Launch<T>::cl(flen, true, gps(), bf, kPcg, k, B, st);
+            mark(k == 0 ? kKindInvPcg0 : kKindInvPcg);
             Launch<T>::wfs(false, gps(), bf, 0, B, st);
             mark(kKindWfs);
-            Launch<T>::gather(gps(), bf, B, st);
-            mark(kKindGather);
-            Launch<T>::cl(flen, false, gps(), bf, kPcg, it, B, st);
-            mark(kKindFwdPcg);
+            gather();
+            return;
         }
         // last update + fitting W^-1 c, then fit + control + rotation
         Launch<T>::cl(flen, true, gps(), bf, kFit, 0, B, st);
         mark(kKindInvFit);
-        Launch<T>::fit(gp, bf, 1, B, st);
+        Launch<T>::fit(gpf, bf, 1, B, st);
         mark(kKindFit);
+    }
+
+    // NCCL exchange of segment `seg`'s partial layer sums (multi-process shards)
+    template <typename T>
+    void exchange_nccl(int seg, cudaStream_t st) {
+        const auto& api = NcclApi::get();
+        api.check(api.AllReduce(ypart[static_cast<size_t>(seg)], state<T>().bf.y,
+                                static_cast<size_t>(gp.n) * batch, sizeof(T) == 8 ? ncclFloat64 : ncclFloat32,
+                                ncclSum, comm, st),
+                  "ncclAllReduce");
+    }
+
+    template <typename T, typename Mark>
+    void launch_frame(cudaStream_t st, Mark&& mark) {
+        if (sharded && !comm) throw ArgError("shard group members step through fewha_gpu_group_step_device");
+        for (int seg = 0; seg < n_segments(); ++seg) {
+            launch_segment<T>(seg, st, mark);
+            if (sharded && seg <= gp.iters) exchange_nccl<T>(seg, st);
+        }
         CK(cudaGetLastError());
     }
 
@@ -962,6 +971,7 @@ struct EngineImpl {
     template <typename T>
     void ensure_graph() {
         if (graph) return;
+        if (sharded && !comm) throw ArgError("shard group members step through fewha_gpu_group_step_device");
         cudaGraph_t gr;
         CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
         launch_frame<T>(stream);
@@ -1158,6 +1168,7 @@ Engine::Engine(Geometry g, int precision, int batch, int device) : p_(std::make_
     CK(cudaSetDevice(device));
     P.gp = P.upload_plan(P.plan);
     P.gp64 = precision == 64 ? P.gp : P.upload_plan(plan64);
+    P.gpf = P.gp;
     CK(cudaStreamCreateWithFlags(&P.stream, cudaStreamNonBlocking));
     P.own_stream = true;
     if (precision == 64) {
@@ -1181,6 +1192,7 @@ Engine::~Engine() {
     if (!p_) return;
     cudaSetDevice(p_->device);
     p_->invalidate_graph();
+    if (p_->comm) NcclApi::get().CommDestroy(p_->comm);
     if (p_->own_stream && p_->stream) cudaStreamDestroy(p_->stream);
 }
 
@@ -1201,7 +1213,163 @@ void Engine::override_loop(int loop_mode, double gain) {
         P.g.gain = gain;
         P.gp.gain = gain;
     }
+    P.gpf.closed = P.gp.closed;
+    P.gpf.gain = P.gp.gain;
     P.invalidate_graph();
+}
+
+// ---------------------------------------------------------------------------
+// Per-WFS sharding
+// ---------------------------------------------------------------------------
+std::pair<int, int> shard_range(const Geometry& g, int rank, int world) {
+    const int W = static_cast<int>(g.wfs.size());
+    if (world < 1 || world > W) throw ArgError("shard: world must be in [1, number of WFS]");
+    if (rank < 0 || rank >= world) throw ArgError("shard: rank out of range");
+    // contiguous WFS ranges minimising the largest per-rank cost (linear
+    // partition, exact DP); cost = (n_s+1)^2 wavefront nodes of the WFS
+    std::vector<double> pre(static_cast<size_t>(W) + 1, 0.0);
+    for (int w = 0; w < W; ++w) {
+        const double np = g.wfs[w].n_subap + 1.0;
+        pre[static_cast<size_t>(w) + 1] = pre[static_cast<size_t>(w)] + np * np;
+    }
+    const double inf = 1e300;
+    // best[k][j]: min over partitions of WFS [0, j) into k ranges of the max range cost
+    std::vector<std::vector<double>> best(static_cast<size_t>(world) + 1, std::vector<double>(static_cast<size_t>(W) + 1, inf));
+    std::vector<std::vector<int>> cut(best.size(), std::vector<int>(static_cast<size_t>(W) + 1, 0));
+    best[0][0] = 0.0;
+    for (int k = 1; k <= world; ++k)
+        for (int j = k; j <= W; ++j)
+            for (int i = k - 1; i < j; ++i) {  // last range [i, j); ties keep the earliest cut
+                const double v = std::max(best[k - 1][i], pre[j] - pre[i]);
+                if (v < best[k][j]) {
+                    best[k][j] = v;
+                    cut[k][j] = i;
+                }
+            }
+    std::vector<int> bounds(static_cast<size_t>(world) + 1);
+    bounds[static_cast<size_t>(world)] = W;
+    for (int k = world, j = W; k > 0; --k) {
+        j = cut[k][j];
+        bounds[static_cast<size_t>(k) - 1] = j;
+    }
+    return {bounds[static_cast<size_t>(rank)], bounds[static_cast<size_t>(rank) + 1]};
+}
+
+void Engine::shard(int rank, int world, const void* nccl_id) {
+    auto& P = *p_;
+    CK(cudaSetDevice(P.device));
+    const auto [wa, wb] = shard_range(P.g, rank, world);
+    if (P.comm) {
+        NcclApi::get().CommDestroy(P.comm);
+        P.comm = nullptr;
+    }
+    P.shard_rank = rank;
+    P.shard_world = world;
+    P.sharded = world > 1 || nccl_id != nullptr;
+    Plan sp = build_plan(P.g, P.precision / 8, wa, wb);
+    sp.gp.piston_exact = P.gp.piston_exact;
+    std::copy(std::begin(P.gp.flo), std::end(P.gp.flo), sp.gp.flo);
+    std::copy(std::begin(P.gp.fhi), std::end(P.gp.fhi), sp.gp.fhi);
+    std::copy(std::begin(P.gp.flo_f), std::end(P.gp.flo_f), sp.gp.flo_f);
+    std::copy(std::begin(P.gp.fhi_f), std::end(P.gp.fhi_f), sp.gp.fhi_f);
+    sp.gp.closed = P.gp.closed;
+    sp.gp.gain = P.gp.gain;
+    P.gpf = world > 1 ? P.upload_plan(sp) : P.gp;
+    if (P.sharded && P.ypart.empty()) {
+        const size_t es = P.precision / 8, bytes = es * static_cast<size_t>(P.gp.n) * P.batch;
+        for (int e = 0; e <= P.gp.iters; ++e) {
+            void* p = nullptr;
+            CK(cudaMalloc(&p, bytes));
+            CK(cudaMemset(p, 0, bytes));
+            P.fr.add(p);
+            P.ypart.push_back(p);
+        }
+    }
+    if (nccl_id) {
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_id, sizeof(id));
+        const auto& api = NcclApi::get();
+        api.check(api.CommInitRank(&P.comm, world, id, rank), "ncclCommInitRank");
+    }
+    P.invalidate_graph();
+}
+
+std::pair<int, int> Engine::shard_wfs() const { return {p_->gpf.wa, p_->gpf.wb}; }
+
+void* Engine::shard_partial(int seg) const {
+    const auto& P = *p_;
+    if (!P.sharded || seg < 0 || seg >= static_cast<int>(P.ypart.size())) return nullptr;
+    return P.ypart[static_cast<size_t>(seg)];
+}
+
+// In-process shard group (one process driving the members, on one device or on
+// several with peer access): segments in lockstep on every member's stream, the
+// exchange of segment k a fixed-order sum of all members' partials (k_exchange)
+// after every member's segment k (cross-stream events).  Each member's partial
+// buffer of segment k is rewritten only in the next frame, after every member
+// passed exchange k, so no buffer is read and rewritten concurrently.
+void group_step_device(const std::vector<Engine*>& members) {
+    const int world = static_cast<int>(members.size());
+    if (world < 1 || world > kMaxW) throw ArgError("shard group: 1..16 members");
+    std::vector<EngineImpl*> m(static_cast<size_t>(world));
+    for (int r = 0; r < world; ++r) {
+        m[static_cast<size_t>(r)] = members[static_cast<size_t>(r)]->p_.get();
+        const auto& P = *m[static_cast<size_t>(r)];
+        if (!P.sharded || P.comm || P.shard_rank != r || P.shard_world != world)
+            throw ArgError("shard group: member " + std::to_string(r) + " is not rank " + std::to_string(r) + " of " +
+                           std::to_string(world) + " without NCCL");
+        if (P.precision != m[0]->precision || P.batch != m[0]->batch || P.gp.n != m[0]->gp.n)
+            throw ArgError("shard group: members differ in precision, batch or geometry");
+    }
+    for (auto* P : m) {
+        CK(cudaSetDevice(P->device));
+        if (!P->has_precond) P->build_precond();
+        for (auto* Q : m)
+            if (Q->device != P->device) {
+                const cudaError_t pe = cudaDeviceEnablePeerAccess(Q->device, 0);
+                if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) CK(pe);
+                if (pe == cudaErrorPeerAccessAlreadyEnabled) (void)cudaGetLastError();
+            }
+    }
+    std::vector<cudaEvent_t> ev(static_cast<size_t>(world));
+    for (int r = 0; r < world; ++r) {
+        CK(cudaSetDevice(m[static_cast<size_t>(r)]->device));
+        CK(cudaEventCreateWithFlags(&ev[static_cast<size_t>(r)], cudaEventDisableTiming));
+    }
+    auto run = [&](auto tag) {
+        using T = decltype(tag);
+        const int nseg = m[0]->n_segments(), iters = m[0]->gp.iters;
+        const long long n_el = static_cast<long long>(m[0]->gp.n) * m[0]->batch;
+        const long long n_vec = n_el / (16 / static_cast<long long>(sizeof(T)));
+        for (int seg = 0; seg < nseg; ++seg) {
+            for (int r = 0; r < world; ++r) {
+                auto* P = m[static_cast<size_t>(r)];
+                CK(cudaSetDevice(P->device));
+                P->launch_segment<T>(seg, P->s(), [](int) {});
+                CK(cudaEventRecord(ev[static_cast<size_t>(r)], P->s()));
+            }
+            if (seg > iters) break;
+            PeerParts parts{};
+            parts.world = world;
+            for (int r = 0; r < world; ++r) parts.p[r] = m[static_cast<size_t>(r)]->ypart[static_cast<size_t>(seg)];
+            for (int r = 0; r < world; ++r) {
+                auto* P = m[static_cast<size_t>(r)];
+                CK(cudaSetDevice(P->device));
+                for (int q = 0; q < world; ++q)
+                    if (q != r) CK(cudaStreamWaitEvent(P->s(), ev[static_cast<size_t>(q)], 0));
+                const int grid = static_cast<int>(std::min<long long>((n_vec + 255) / 256, 148 * 8));
+                k_exchange<T><<<grid, 256, 0, P->s()>>>(parts, P->state<T>().bf.y, n_vec);
+                CK(cudaGetLastError());
+            }
+            // the events are re-recorded by the next segment; the waits above already captured them
+        }
+    };
+    if (m[0]->precision == 64) run(double{});
+    else run(float{});
+    for (int r = 0; r < world; ++r) {
+        CK(cudaSetDevice(m[static_cast<size_t>(r)]->device));
+        CK(cudaEventDestroy(ev[static_cast<size_t>(r)]));
+    }
 }
 
 void Engine::build_preconditioner() { p_->build_precond(); }

@@ -4,6 +4,7 @@
 
 #include <memory>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "geometry.hpp"
@@ -11,6 +12,12 @@
 namespace fewha_gpu {
 
 struct EngineImpl;
+
+class Engine;
+// contiguous WFS range [first, second) of shard `rank` of `world` (balanced by wavefront nodes)
+std::pair<int, int> shard_range(const Geometry& g, int rank, int world);
+// one frame of an in-process shard group, members in rank order
+void group_step_device(const std::vector<Engine*>& members);
 
 class Engine {
 public:
@@ -47,6 +54,14 @@ public:
     float bench_dwt(int variant, int inverse, int reps, int threads);
     int read_stamps(unsigned long long* out, size_t n);
     void device_buffers(void** slopes, void** coeffs, void** dm, double** rho, int** status, int** n_rho);
+
+    // per-WFS sharding: own WFS shard_range(g, rank, world); nccl_id
+    // (128-byte ncclUniqueId) joins a multi-process NCCL exchange, null forms an
+    // in-process group member (group_step_device)
+    void shard(int rank, int world, const void* nccl_id);
+    std::pair<int, int> shard_wfs() const;
+    void* shard_partial(int seg) const;
+    friend void group_step_device(const std::vector<Engine*>& members);
 
     // operator entry points (count stacked host inputs)
     void apply_M(const double* in, double* out, int count);

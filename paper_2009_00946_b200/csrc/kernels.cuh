@@ -27,6 +27,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <type_traits>
 
 #include "device.hpp"
 
@@ -405,81 +406,7 @@ template <typename T, bool RHS>
 __global__ void __launch_bounds__(512, 2) k_wfs(const GeoParams gp, const Bufs<T> bf, int with_dm) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     pdl_launch_dependents();
-    wfs_tile<T, RHS>(gp, bf, with_dm, blockIdx.x, blockIdx.y, smem_raw);
-}
-
-// ---------------------------------------------------------------------------
-// Phase C1: y_l = sum_w P_{w,l}^T psi_w on one layer tile per CTA: separable
-// gather (columns, then rows), WFS in ascending order.  No atomics.
-// ---------------------------------------------------------------------------
-template <typename T>
-__global__ void __launch_bounds__(256) k_adjoint(const GeoParams gp, const T* __restrict__ psi_all, T* __restrict__ y_all) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int TP = gp.ltile;
-    T* blk = reinterpret_cast<T*>(smem_raw);           // [rows_max][cols_max]
-    T* hc = blk + gp.lt_rows_max * gp.lt_cols_max;     // [rows_max][TP]
-    const int tile = blockIdx.x, b = blockIdx.y;
-    const int l = gp.ltiles[3 * tile], I0 = gp.ltiles[3 * tile + 1], J0 = gp.ltiles[3 * tile + 2];
-    const int side = gp.side[l];
-    const int nI = min(TP, side - I0), nJ = min(TP, side - J0);
-    const int tid = threadIdx.x, nthr = blockDim.x;
-    const T* tw = weights<T>(gp);
-    constexpr int kMaxPer = 16;
-    T acc[kMaxPer];
-#pragma unroll
-    for (int q = 0; q < kMaxPer; ++q) acc[q] = T(0);
-
-    for (int w = 0; w < gp.W; ++w) {
-        const int* dir = gp.ti + gp.o_pl + (w * gp.L + l) * 4;
-        const int ox = dir[0], oy = dir[1], orr = dir[2], occ = dir[3];
-        const int* tr = gp.ti + gp.o_tr + (tile * gp.W + w) * 4;
-        const int ilo = tr[0], ihi = tr[1], jlo = tr[2], jhi = tr[3];
-        if (ilo >= ihi || jlo >= jhi) continue;  // footprint misses this tile
-        const int nr = ihi - ilo, nc = jhi - jlo, np = gp.ns[w] + 1;
-        const T* psi = psi_all + static_cast<size_t>(b) * gp.Nw + gp.woff[w];
-        __syncthreads();
-        for (int idx = tid; idx < nr * nc; idx += nthr) {
-            const int r = idx / nc, c = idx % nc;
-            blk[r * nc + c] = psi[(ilo + r) * np + jlo + c];
-        }
-        __syncthreads();
-        for (int idx = tid; idx < nr * nJ; idx += nthr) {
-            const int r = idx / nJ, tj = idx % nJ, J = J0 + tj;
-            const int jl = gp.ti[occ + 2 * J], jh = gp.ti[occ + 2 * J + 1];
-            T s = T(0);
-            for (int j = jl; j < jh; ++j) {
-                const T fx = tw[ox + j];
-                const T wgt = gp.ti[ox + j] == J ? T(1) - fx : fx;
-                s += wgt * blk[r * nc + (j - jlo)];
-            }
-            hc[r * TP + tj] = s;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int q = 0; q < kMaxPer; ++q) {
-            const int idx = tid + q * nthr;
-            if (idx >= TP * TP) break;
-            const int ti_ = idx / TP, tj = idx % TP;
-            if (ti_ >= nI || tj >= nJ) continue;
-            const int I = I0 + ti_;
-            const int il = gp.ti[orr + 2 * I], ih = gp.ti[orr + 2 * I + 1];
-            T s = T(0);
-            for (int i = il; i < ih; ++i) {
-                const T fy = tw[oy + i];
-                const T wgt = gp.ti[oy + i] == I ? T(1) - fy : fy;
-                s += wgt * hc[(i - ilo) * TP + tj];
-            }
-            acc[q] += s;
-        }
-    }
-    T* y = y_all + static_cast<size_t>(b) * gp.n + gp.coff[l];
-#pragma unroll
-    for (int q = 0; q < kMaxPer; ++q) {
-        const int idx = tid + q * nthr;
-        if (idx >= TP * TP) break;
-        const int ti_ = idx / TP, tj = idx % TP;
-        if (ti_ < nI && tj < nJ) y[(I0 + ti_) * side + J0 + tj] = acc[q];
-    }
+    wfs_tile<T, RHS>(gp, bf, with_dm, gp.wt_base + blockIdx.x, blockIdx.y, smem_raw);
 }
 
 // ---------------------------------------------------------------------------
@@ -638,6 +565,38 @@ template <typename Src, typename Dst>
 __global__ void k_convert(const Src* in, Dst* out, size_t n) {
     const size_t k = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (k < n) out[k] = static_cast<Dst>(in[k]);
+}
+
+
+// ---------------------------------------------------------------------------
+// Per-WFS sharding: y = sum_r ypart_r, the adjoint layer sums of
+// the shard group's members added in rank order (identical on every member, so
+// the replicated PCG state stays bitwise equal).  `parts` holds the members'
+// partial buffers: local on one device, NVLink peer loads across devices with
+// peer access enabled.  16-byte vector loads; n_vec = elements / (16/sizeof(T)).
+// ---------------------------------------------------------------------------
+struct PeerParts {
+    const void* p[kMaxW];
+    int world;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_exchange(const PeerParts parts, T* __restrict__ y, long long n_vec) {
+    using V = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
+    constexpr int E = 16 / sizeof(T);
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n_vec;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const V* p0 = static_cast<const V*>(parts.p[0]);
+        V acc = p0[i];
+        T* a = reinterpret_cast<T*>(&acc);
+        for (int r = 1; r < parts.world; ++r) {
+            const V v = static_cast<const V*>(parts.p[r])[i];
+            const T* b = reinterpret_cast<const T*>(&v);
+#pragma unroll
+            for (int e = 0; e < E; ++e) a[e] += b[e];
+        }
+        reinterpret_cast<V*>(y)[i] = acc;
+    }
 }
 
 }  // namespace fewha_gpu

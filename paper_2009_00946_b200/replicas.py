@@ -78,3 +78,24 @@ def init_replicas(backend=None):
     else:
         dist.init_process_group(backend)
     return ReplicaContext(rank=rank, world=world, local_rank=local, dist=dist)
+
+
+def share_nccl_id(rc: ReplicaContext, make_id) -> bytes | None:
+    """Rank 0 makes a 128-byte NCCL unique id (make_id()) and every rank gets it
+    over the process group (broadcast_object_list); world 1 -> None."""
+    if rc.dist is None:
+        return None
+    obj = [make_id() if rc.rank == 0 else None]
+    rc.dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+def shard_frame(rec, rc: ReplicaContext):
+    """Per-WFS sharding of ONE reconstruction frame over the ranks:
+    rank r owns fewha_gpu_shard_range(r, world) and the partial adjoint layer
+    sums are all-reduced through NCCL inside the frame graph.  Returns the
+    owned WFS range."""
+    import paper_2009_00946_b200 as fg
+    nid = share_nccl_id(rc, fg.nccl_unique_id)
+    rec.shard(rc.rank, rc.world, nid)
+    return rec.shard_wfs()

@@ -78,3 +78,70 @@ def test_nccl_without_device_fails_loudly(monkeypatch):
     from paper_2009_00946_b200.replicas import init_replicas
     with pytest.raises(RuntimeError, match="CUDA device"):
         init_replicas(backend="nccl")
+
+
+# ---- per-WFS sharding host logic ------------------------------------
+
+def _shard_worker(rank, world, port, q):
+    os.environ.update({"RANK": str(rank), "WORLD_SIZE": str(world), "LOCAL_RANK": str(rank),
+                       "MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
+    import paper_2009_00946_b200 as fg
+    from conftest import preset
+    from paper_2009_00946_b200.replicas import init_replicas, share_nccl_id
+    rc = init_replicas(backend="gloo")
+    try:
+        nid = share_nccl_id(rc, fg.nccl_unique_id)
+        rng = fg.shard_range(preset("elt_mcao84_3dm.json"), rc.rank, rc.world)
+        q.put((rank, nid, rng))
+    finally:
+        rc.shutdown()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_shard_setup_gloo(world):
+    """Every rank receives rank 0's NCCL id, and the ranks' WFS ranges tile [0, W)."""
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_shard_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    res = sorted(q.get(timeout=10) for _ in range(world))
+    ids = {r[1] for r in res}
+    assert len(ids) == 1 and len(next(iter(ids))) == 128
+    ranges = [r[2] for r in res]
+    assert ranges[0][0] == 0 and ranges[-1][1] == 9
+    for (a0, b0), (a1, b1) in zip(ranges, ranges[1:]):
+        assert b0 == a1 and a0 < b0
+
+
+def _nodes(path):
+    import json
+    return [(w["n_subap"] + 1) ** 2 for w in json.load(open(path))["wfs"]]
+
+
+@pytest.mark.parametrize("name", ["elt_mcao84_3dm.json", "small_mcao.json", "elt_moao84.json"])
+def test_shard_ranges_are_optimal_contiguous_partitions(name):
+    """fewha_gpu_shard_range: contiguous, covering, non-empty, and minimising the
+    largest per-shard wavefront node count (checked by brute force)."""
+    import itertools
+    import paper_2009_00946_b200 as fg
+    from conftest import preset
+    path = preset(name)
+    cost = _nodes(path)
+    W = len(cost)
+    for world in range(1, W + 1):
+        rng = [fg.shard_range(path, r, world) for r in range(world)]
+        assert rng[0][0] == 0 and rng[-1][1] == W
+        assert all(a < b for a, b in rng) and all(rng[i][1] == rng[i + 1][0] for i in range(world - 1))
+        got = max(sum(cost[a:b]) for a, b in rng)
+        best = min(max(sum(cost[a:b]) for a, b in zip((0,) + c, c + (W,)))
+                   for c in itertools.combinations(range(1, W), world - 1))
+        assert got == best, (world, got, best)
+    with pytest.raises(fg.ArgumentError):
+        fg.shard_range(path, 0, W + 1)
+    with pytest.raises(fg.ArgumentError):
+        fg.shard_range(path, 2, 2)
