@@ -27,6 +27,10 @@ shadow of the same preset (same layers, WFS and PCG; 9 identity-fitted DMs).
 host thread, on the same config and slope stream.
 N > 1: one process per GPU, independent instances per rank (replicas,
 "scaling": "weak"); the path has no exchange step in this mode.
+--shard (N > 1): per-WFS sharding of ONE instance's frame: rank r
+owns a contiguous WFS range, the partial adjoint layer sums are all-reduced
+through NCCL inside the frame graph; value = frames/s of that one instance
+("scaling": "strong").
 """
 from __future__ import annotations
 
@@ -261,9 +265,15 @@ def run_ours(args):
     b = args.precision // 8
 
     rec = fg.Reconstructor(args.preset, precision=args.precision, batch=1, device=local)
+    shard = args.shard and world > 1
+    shard_wfs = None
+    if shard:
+        from paper_2009_00946_b200.replicas import shard_frame
+        shard_wfs = shard_frame(rec, rc)
     rec.build_preconditioner()
     F = 16
-    stream_host = slope_stream(rec, args.preset, F, seed=rc.seed)
+    # sharded ranks reconstruct the same frame: a common slope stream
+    stream_host = slope_stream(rec, args.preset, F, seed=1 if shard else rc.seed)
     stream = torch.from_numpy(stream_host).to(dev)
     st = torch.cuda.Stream(dev)  # a real stream: events, flushes and the graph all order on it
     torch.cuda.set_stream(st)
@@ -300,7 +310,7 @@ def run_ours(args):
     total_ms = float(ms.sum())
     p50, p99 = float(np.percentile(ms, 50)), float(np.percentile(ms, 99))
     total_ms, p50, p99 = rc.max_over_ranks([total_ms, p50, p99], device=dev)
-    value = rc.aggregate_throughput(K, total_ms)
+    value = K / (total_ms / 1000.0) if shard else rc.aggregate_throughput(K, total_ms)
 
     # ---- per-launch profile (events between launches on the launching stream) ----
     prof = {}
@@ -345,11 +355,11 @@ def run_ours(args):
             e2e_ms.append((t1 - t0) * 1000.0)
     e2e_ms = np.array(e2e_ms)
     (e2e_mean,) = rc.max_over_ranks([float(np.mean(e2e_ms))], device=dev)
-    e2e_val = rc.aggregate_throughput(1, e2e_mean)
+    e2e_val = 1000.0 / e2e_mean if shard else rc.aggregate_throughput(1, e2e_mean)
 
     # ---- batch-64 throughput (HBM-bound regime) ----------------
     batch_info = None
-    if args.batch64:
+    if args.batch64 and not shard:
         B = 64
         rb = fg.Reconstructor(args.preset, precision=args.precision, batch=B, device=local)
         rb.build_preconditioner()
@@ -394,13 +404,15 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": round(total_ms / K, 5), "p50_ms": round(p50, 5),
-            "p99_ms": round(p99, 5), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "p99_ms": round(p99, 5), "higher_is_better": True, "scaling": "strong" if shard else "weak",
+            "vs_baseline": None,
             "dtype": "f64" if args.precision == 64 else "f32", "data": "synthetic",
             "config": {"workload": "ELT MCAO-84 (BASELINE config 3: 84x84 SH, 6 LGS + 3 NGS, 9 layers, 3 DMs), "
                                    "1 instance/rank, closed loop, 4 PCG iters, single-frame latency",
                        "preset": os.path.relpath(args.preset, ROOT), "n_coeff": d["n"], "n_slopes": S,
                        "n_act": d["A"], "l2": "flushed (256 MiB write) before every timed frame",
-                       "parallelism": f"replicas x{world}"},
+                       "parallelism": (f"wfs-shard x{world} (rank 0 owns WFS {shard_wfs})" if shard
+                                       else f"replicas x{world}")},
             "frame_roofline": {"bytes_per_frame": fb, "achieved_gbs": round(fb / (p50 / 1000.0) / 1e9, 2),
                                "frac_at_p50": round(fb / (p50 / 1000.0) / 1e9 / peak, 5),
                                "roofline_us": round(fb / (peak * 1e9) * 1e6, 3)},
@@ -436,6 +448,7 @@ def main():
     ap.add_argument("--cpu-frames", type=int, default=150)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-batch64", dest="batch64", action="store_false")
+    ap.add_argument("--shard", action="store_true", help="N>1: per-WFS sharding of one frame (NCCL exchange)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

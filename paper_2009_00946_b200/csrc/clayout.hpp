@@ -43,19 +43,25 @@ FEWHA_HD int lg2(int v) {
     return r;
 #endif
 }
-FEWHA_HD bool dist(int S, int C) { return S >= 2 * C; }
-FEWHA_HD int tail(int S, int C) { return dist(S, C) ? C : S; }
-FEWHA_HD int nlev(int S, int C) {
+// Tail size D (a power of two, C <= D): levels s >= 2D are distributed over
+// the cluster, the D x D tail (levels below) runs on rank 0 inside one CTA --
+// the coarse levels cost a cluster barrier each but almost no arithmetic, so
+// finishing them locally is cheaper.  Layers with S < 2D are tail-only (whole
+// layer on rank 0).  The host picks D = 2C (measured best), else 4C, else C, whose kernels
+// fit in shared memory (GeoParams::ctail).
+FEWHA_HD bool dist(int S, int C, int D) { return S >= 2 * D; }
+FEWHA_HD int tail(int S, int C, int D) { return dist(S, C, D) ? D : S; }
+FEWHA_HD int nlev(int S, int C, int D) {
     int n = 0;
-    for (int s = S; dist(s, C); s >>= 1) ++n;
+    for (int s = S; dist(s, C, D); s >>= 1) ++n;
     return n;
 }
 // band rows of rank q at level S (input of the forward gather, output of the inverse)
-FEWHA_HD int band_rows(int S, int C, int q) { return dist(S, C) ? S >> lg2(C) : (q == 0 ? S : 0); }
-FEWHA_HD int band_row0(int S, int C, int q) { return dist(S, C) ? q * (S >> lg2(C)) : 0; }
+FEWHA_HD int band_rows(int S, int C, int D, int q) { return dist(S, C, D) ? S >> lg2(C) : (q == 0 ? S : 0); }
+FEWHA_HD int band_row0(int S, int C, int D, int q) { return dist(S, C, D) ? q * (S >> lg2(C)) : 0; }
 // offset (elements) of level lv's block in the compact layout with H halo rows;
 // lv == nlev gives the tail block's offset
-FEWHA_HD int level_off(int S, int C, int H, int lv) {
+FEWHA_HD int level_off(int S, int C, int H, int lv) {  // (independent of D)
     int off = 0;
     const int lc = lg2(C);
     for (int i = 0; i < lv; ++i) {
@@ -65,21 +71,21 @@ FEWHA_HD int level_off(int S, int C, int H, int lv) {
     return off;
 }
 // total compact size (elements), tail block always reserved
-FEWHA_HD int compact_size(int S, int C, int H) {
-    const int T = tail(S, C);
-    return level_off(S, C, H, nlev(S, C)) + T * T;
+FEWHA_HD int compact_size(int S, int C, int D, int H) {
+    const int T = tail(S, C, D);
+    return level_off(S, C, H, nlev(S, C, D)) + T * T;
 }
 // elements rank q owns, and the offset of its block inside the layer (rank-blocked order)
-FEWHA_HD int owned_count(int S, int C, int q) {
-    const int T = tail(S, C);
-    if (!dist(S, C)) return q == 0 ? T * T : 0;
-    return level_off(S, C, 0, nlev(S, C)) + (q == 0 ? T * T : 0);
+FEWHA_HD int owned_count(int S, int C, int D, int q) {
+    const int T = tail(S, C, D);
+    if (!dist(S, C, D)) return q == 0 ? T * T : 0;
+    return level_off(S, C, 0, nlev(S, C, D)) + (q == 0 ? T * T : 0);
 }
-FEWHA_HD int rank_off(int S, int C, int q) {
+FEWHA_HD int rank_off(int S, int C, int D, int q) {
     if (q == 0) return 0;
-    const int T = tail(S, C);
-    if (!dist(S, C)) return T * T;
-    return q * level_off(S, C, 0, nlev(S, C)) + T * T;
+    const int T = tail(S, C, D);
+    if (!dist(S, C, D)) return T * T;
+    return q * level_off(S, C, 0, nlev(S, C, D)) + T * T;
 }
 
 FEWHA_HD int a16(int v) { return (v + 15) & ~15; }
@@ -91,18 +97,26 @@ FEWHA_HD int a16(int v) { return (v + 15) & ~15; }
 struct FwdSmem {
     int x0, e0, e1, x1, f, tb, tb2, total;
 };
-FEWHA_HD FwdSmem fwd_smem(int maxside, int C, int flen, int elem) {
+// largest tail block of any layer (distributed tail D, or a tail-only layer of side < 2D)
+FEWHA_HD int tail_max(int maxside, int C, int D) {
+    const int Tm = tail(maxside, C, D), tonly = maxside < D ? maxside : D;
+    return Tm > tonly ? Tm : tonly;
+}
+FEWHA_HD FwdSmem fwd_smem(int maxside, int C, int D, int flen, int elem) {
     FwdSmem m{};
-    const int P = maxside + 1, R = band_rows(maxside, C, 0);
-    const int xb = a16((R + flen - 2) * P * elem), cb = a16(compact_size(maxside, C, 0) * elem);
+    const int P = maxside + 1, R = band_rows(maxside, C, D, 0);
+    const int tonly = maxside < D ? maxside : D;
+    const int xrows = (R + flen - 2) > tonly ? (R + flen - 2) : tonly;  // tail-only layers use the band too
+    const int xb = a16(xrows * P * elem), cb = a16(compact_size(maxside, C, D, 0) * elem);
     m.x0 = 0;
     m.e0 = xb;
     m.e1 = m.e0 + cb;
     m.x1 = m.e1 + cb;
     m.f = m.x1 + xb;
     m.tb = m.f + cb;
-    m.tb2 = m.tb + a16(C * (C + 1) * elem);
-    m.total = m.tb2 + a16(C * (C + 1) * elem);
+    const int Tb = tail_max(maxside, C, D);
+    m.tb2 = m.tb + a16(Tb * (Tb + 1) * elem);
+    m.total = m.tb2 + a16(Tb * (Tb + 1) * elem);
     return m;
 }
 
@@ -113,19 +127,22 @@ FEWHA_HD FwdSmem fwd_smem(int maxside, int C, int flen, int elem) {
 struct InvSmem {
     int v, vstride, z, x0, x1, aw, tb, tb2, total;
 };
-FEWHA_HD InvSmem inv_smem(int maxside, int C, int flen, int elem) {
+FEWHA_HD InvSmem inv_smem(int maxside, int C, int D, int flen, int elem) {
     InvSmem m{};
-    const int P = maxside + 1, R = band_rows(maxside, C, 0), H = flen / 2 - 1;
-    m.vstride = a16(compact_size(maxside, C, 0) * elem);
+    const int P = maxside + 1, R = band_rows(maxside, C, D, 0), H = flen / 2 - 1;
+    m.vstride = a16(compact_size(maxside, C, D, 0) * elem);
     m.v = 0;
     m.z = 6 * m.vstride;
-    m.x0 = m.z + a16(compact_size(maxside, C, H) * elem);
+    m.x0 = m.z + a16(compact_size(maxside, C, D, H) * elem);
     m.x1 = m.x0 + a16(R * P * elem);
     m.aw = m.x1 + a16(R * P * elem);
-    const int kmax = dist(maxside, C) ? maxside >> (lg2(C) + 1) : 0;
+    const int kmax = dist(maxside, C, D) ? maxside >> (lg2(C) + 1) : 0;
     m.tb = m.aw + a16((kmax + H) * maxside * elem);
-    m.tb2 = m.tb + a16(C * (C + 1) * elem);
-    m.total = m.tb2 + a16(C * (C + 1) * elem);
+    // tb2 aliases x1: the tail is finished (and, if its output sits in tb2, consumed
+    // by the first distributed level, which writes x0) before x1 is first written
+    const int Tb = tail_max(maxside, C, D);
+    m.tb2 = m.x1;
+    m.total = m.tb + a16(Tb * (Tb + 1) * elem);
     return m;
 }
 

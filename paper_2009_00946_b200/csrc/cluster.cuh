@@ -161,15 +161,15 @@ struct LPlan {
 };
 // Level offsets are computed once per CTA into shared memory (s_off: 2 x (kMaxLev+1));
 // the caller runs __syncthreads before the plan's offsets are used.
-__device__ __forceinline__ LPlan make_plan(int S, int C, int q, int H, int* s_off) {
+__device__ __forceinline__ LPlan make_plan(int S, int C, int D, int q, int H, int* s_off) {
     LPlan p;
     p.S = S;
     p.C = C;
     p.lC = ilog2(C);
     p.q = q;
     p.H = H;
-    p.T = clay::tail(S, C);
-    p.nlev = clay::nlev(S, C);
+    p.T = clay::tail(S, C, D);
+    p.nlev = clay::nlev(S, C, D);
     p.lsS = ilog2(S);
     const int t = threadIdx.x;
     if (t <= p.nlev) s_off[t] = clay::level_off(S, C, 0, t);
@@ -231,13 +231,35 @@ __device__ __forceinline__ void prefetch_block(const T* src, T* dst, int count, 
 // Forward level s: out(i,j) = sum_t1 F1[t1] sum_t2 F2[t2] x[2m1+t1][2m2+t2]
 // (rows first, as wavelet.hpp:153-168), F = lo for the approximation half.
 // ---------------------------------------------------------------------------
+constexpr int kFusedTail = 8;  // tail levels s <= 8 as fused 2-D passes, larger ones separable
+
 template <typename T, int FLEN>
 __device__ void tail_forward(const GeoParams& gp, const T* src, int ps, int Tt, T* b0, T* b1, T* f) {
     const int tid = threadIdx.x, nthr = blockDim.x;
     const T* cur = src;
     int pc = ps;
     T* nxt = b0;
-    for (int s = Tt; s >= 2; s >>= 1) {
+    int s0 = Tt;
+    if (Tt > kFusedTail) {
+        // levels s > 8: separable in-place row then column passes on b0 (pitch Tt+1);
+        // the detail quadrants of each level are final
+        const int lt = ilog2(Tt);
+        for (int e = tid; e < Tt * Tt; e += nthr) b0[(e >> lt) * (Tt + 1) + (e & (Tt - 1))] = src[(e >> lt) * ps + (e & (Tt - 1))];
+        __syncthreads();
+        for (; s0 > kFusedTail; s0 >>= 1) {
+            const int h = s0 >> 1, ls = ilog2(s0);
+            analysis_lines<T, FLEN, false>(b0, Tt + 1, s0, s0, gp);
+            analysis_lines<T, FLEN, true>(b0, Tt + 1, s0, s0, gp);
+            for (int e = tid; e < s0 * s0; e += nthr) {  // the next level rewrites only the h x h block
+                const int i = e >> ls, j = e & (s0 - 1);
+                if (i >= h || j >= h) f[i * Tt + j] = b0[i * (Tt + 1) + j];
+            }
+        }
+        cur = b0;
+        pc = Tt + 1;
+        nxt = b1;
+    }
+    for (int s = s0; s >= 2; s >>= 1) {
         const int h = s >> 1, ls = ilog2(s);
         for (int e = tid; e < s * s; e += nthr) {
             const int i = e >> ls, j = e & (s - 1);
@@ -275,7 +297,8 @@ __device__ T* tail_inverse(const GeoParams& gp, const T* zt, int Tt, T* b0, T* b
     const T* cur = zt;  // LL source of level 2: the coarse coefficient itself
     int pc = Tt;
     T* nxt = b0;
-    for (int s = 2; s <= Tt; s <<= 1) {
+    const int sf = Tt < kFusedTail ? Tt : kFusedTail;
+    for (int s = 2; s <= sf; s <<= 1) {
         const int h = s >> 1, ls = ilog2(s);
         for (int e = tid; e < s * s; e += nthr) {
             const int r = e >> ls, c = e & (s - 1);
@@ -310,7 +333,18 @@ __device__ T* tail_inverse(const GeoParams& gp, const T* zt, int Tt, T* b0, T* b
         __syncthreads();
         return b0;
     }
-    return const_cast<T*>(cur);
+    T* buf = const_cast<T*>(cur);  // sf x sf output, pitch Tt+1
+    for (int s = 2 * sf; s <= Tt; s <<= 1) {  // separable levels: columns, then rows (wavelet.hpp:170-196)
+        const int h = s >> 1, ls = ilog2(s);
+        for (int e = tid; e < s * s; e += nthr) {
+            const int i = e >> ls, j = e & (s - 1);
+            if (i >= h || j >= h) buf[i * (Tt + 1) + j] = zt[i * Tt + j];
+        }
+        __syncthreads();
+        synthesis_lines<T, FLEN, true>(buf, Tt + 1, s, s, gp);
+        synthesis_lines<T, FLEN, false>(buf, Tt + 1, s, s, gp);
+    }
+    return buf;
 }
 
 // ---------------------------------------------------------------------------
@@ -371,7 +405,7 @@ __device__ void cdwt_forward(const GeoParams& gp, const LPlan& p, T* x0, T* x1, 
                 }
                 const int i = i0 + e;
                 if (j < h) {
-                    if (last) tbq[(q + i) * (C + 1) + j] = a;  // k == 1: tail row q
+                    if (last) tbq[(q * k + i) * (p.T + 1) + j] = a;  // tail rows [q k, q k + k)
                     else nxt[i * P + j] = a;
                 } else {
                     f[offA + i * h + (j - h)] = a;
@@ -388,7 +422,7 @@ __device__ void cdwt_forward(const GeoParams& gp, const LPlan& p, T* x0, T* x1, 
     }
     cl_sync();  // every rank's tail row is in rank 0's tb
     stamp(gp, 7);
-    if (q == 0) tail_forward<T, FLEN>(gp, tb, C + 1, p.T, tb2, tb, f + p.off[p.nlev]);
+    if (q == 0) tail_forward<T, FLEN>(gp, tb, p.T + 1, p.T, tb2, tb, f + p.off[p.nlev]);
 }
 
 // ---------------------------------------------------------------------------
@@ -431,7 +465,7 @@ __device__ T* cdwt_inverse(const GeoParams& gp, const LPlan& p, const T* z, T* x
             if (j < h) {
                 const int mm = (m0 - H + i) & (h - 1);
                 if (first) {
-                    v = tl[mm * (C + 1) + j];
+                    v = tl[mm * (Tt + 1) + j];
                 } else {
                     const int own = mm >> lk;
                     const T* src = own == q ? prev : rmt(prev, own);
@@ -727,8 +761,8 @@ __device__ __forceinline__ void inv_phase(const GeoParams& gp, const Bufs<T>& bf
     const int S = gp.side[l];
     constexpr int H = FLEN / 2 - 1;
     __shared__ int s_off[2 * (kMaxLev + 1)];
-    const LPlan p = make_plan(S, C, q, H, s_off);
-    const clay::InvSmem sm = clay::inv_smem(gp.maxside, C, FLEN, static_cast<int>(sizeof(T)));
+    const LPlan p = make_plan(S, C, gp.ctail, q, H, s_off);
+    const clay::InvSmem sm = clay::inv_smem(gp.maxside, C, gp.ctail, FLEN, static_cast<int>(sizeof(T)));
     const int P = gp.maxside + 1;
     T* v[6];
 #pragma unroll
@@ -741,7 +775,7 @@ __device__ __forceinline__ void inv_phase(const GeoParams& gp, const Bufs<T>& bf
     T* tb = reinterpret_cast<T*>(smem_raw + sm.tb);
     T* tb2 = reinterpret_cast<T*>(smem_raw + sm.tb2);
     const size_t lbase = static_cast<size_t>(b) * gp.n + gp.coff[l];
-    const int roff = clay::rank_off(S, C, q), cnt = clay::owned_count(S, C, q);
+    const int roff = clay::rank_off(S, C, gp.ctail, q), cnt = clay::owned_count(S, C, gp.ctail, q);
     const size_t vbase = lbase + roff;  // this rank's block of every coefficient-domain vector
     const int tid = threadIdx.x;
     const int slots = gp.L * C;  // dot partial slots per iteration
@@ -868,7 +902,7 @@ __device__ __forceinline__ void inv_phase(const GeoParams& gp, const Bufs<T>& bf
     int outP = P;
     const T* out = cdwt_inverse<T, FLEN>(gp, p, z, x0, x1, aw, tb, tb2, P, &outP);
     stamp(gp, 9);
-    const int R = clay::band_rows(S, C, q), r0 = clay::band_row0(S, C, q);
+    const int R = clay::band_rows(S, C, gp.ctail, q), r0 = clay::band_row0(S, C, gp.ctail, q);
     T* __restrict__ phi = bf.phi + lbase + static_cast<size_t>(r0) * S;
     for (int e = tid; e < R * S; e += blockDim.x) phi[e] = out[(e >> p.lsS) * outP + (e & (S - 1))];
     if (p.nlev > 0) cl_wait();  // no rank exits while its level outputs may still be read
@@ -908,9 +942,9 @@ __device__ __forceinline__ void fwd_phase(const GeoParams& gp, const Bufs<T>& bf
     __shared__ double s_ad[16];  // alpha d_{l,scale} (operators.hpp:307-332)
     __shared__ int s_off[2 * (kMaxLev + 1)];
     const int S = gp.side[l];
-    const LPlan p = make_plan(S, C, q, 0, s_off);
+    const LPlan p = make_plan(S, C, gp.ctail, q, 0, s_off);
     const int nthr = blockDim.x, tid = threadIdx.x;
-    const clay::FwdSmem sm = clay::fwd_smem(gp.maxside, C, FLEN, static_cast<int>(sizeof(T)));
+    const clay::FwdSmem sm = clay::fwd_smem(gp.maxside, C, gp.ctail, FLEN, static_cast<int>(sizeof(T)));
     const int P = gp.maxside + 1;
     T* x0 = reinterpret_cast<T*>(smem_raw + sm.x0);
     T* e0 = reinterpret_cast<T*>(smem_raw + sm.e0);
@@ -919,9 +953,9 @@ __device__ __forceinline__ void fwd_phase(const GeoParams& gp, const Bufs<T>& bf
     T* f = reinterpret_cast<T*>(smem_raw + sm.f);
     T* tb = reinterpret_cast<T*>(smem_raw + sm.tb);
     T* tb2 = reinterpret_cast<T*>(smem_raw + sm.tb2);
-    const int R = clay::band_rows(S, C, q), r0 = clay::band_row0(S, C, q);
+    const int R = clay::band_rows(S, C, gp.ctail, q), r0 = clay::band_row0(S, C, gp.ctail, q);
     const size_t lbase = static_cast<size_t>(b) * gp.n + gp.coff[l];
-    const int roff = clay::rank_off(S, C, q), cnt = clay::owned_count(S, C, q);
+    const int roff = clay::rank_off(S, C, gp.ctail, q), cnt = clay::owned_count(S, C, gp.ctail, q);
     const size_t vbase = lbase + roff;
     stamp(gp, 0);
     double my_ad = 0.0;

@@ -61,6 +61,7 @@ struct GeoParams {
     int tt_stride_l, tt_stride_d, tt_off_d;  // byte stride per tile (layer / DM screens), DM base
     // v2 cluster path
     int ccl;          // CTAs per layer cluster
+    int ctail;        // tail size D of distributed layers (clayout.hpp)
     int gather_km;    // max gather taps per layer row/column
     int o_bs;         // [((w*L+l)*kMaxGU + u)*4] psi source block {ilo, ihi, jlo, jhi} of each gather row group
     int bd_rows_max, bd_cols_max;

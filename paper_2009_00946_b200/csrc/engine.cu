@@ -69,12 +69,12 @@ struct Plan {
 // rank_off(q), in the order the kernels' for_owned() visits it.
 std::vector<int> coeff_perm(const GeoParams& gp) {
     std::vector<int> perm(static_cast<size_t>(gp.n), -1);
-    const int C = gp.ccl;
+    const int C = gp.ccl, D = gp.ctail;
     for (int l = 0; l < gp.L; ++l) {
         const int S = gp.side[l], base = gp.coff[l];
         for (int q = 0; q < C; ++q) {
-            int o = base + clay::rank_off(S, C, q);
-            for (int lv = 0; lv < clay::nlev(S, C); ++lv) {
+            int o = base + clay::rank_off(S, C, D, q);
+            for (int lv = 0; lv < clay::nlev(S, C, D); ++lv) {
                 const int s = S >> lv, h = s / 2, k = h / C, m0 = q * k;
                 for (int i = 0; i < k; ++i)
                     for (int c = 0; c < h; ++c) perm[static_cast<size_t>(base + (m0 + i) * S + h + c)] = o++;
@@ -82,11 +82,11 @@ std::vector<int> coeff_perm(const GeoParams& gp) {
                     for (int c = 0; c < s; ++c) perm[static_cast<size_t>(base + (h + m0 + i) * S + c)] = o++;
             }
             if (q == 0) {
-                const int T = clay::tail(S, C);
+                const int T = clay::tail(S, C, D);
                 for (int i = 0; i < T; ++i)
                     for (int j = 0; j < T; ++j) perm[static_cast<size_t>(base + i * S + j)] = o++;
             }
-            if (o != base + clay::rank_off(S, C, q) + clay::owned_count(S, C, q))
+            if (o != base + clay::rank_off(S, C, D, q) + clay::owned_count(S, C, D, q))
                 throw std::logic_error("coefficient layout: rank block size mismatch");
         }
     }
@@ -340,6 +340,26 @@ Plan build_plan(const Geometry& g, int elem_bytes, int wa = 0, int wb = -1) {
         const int R = std::min(16, pl.maxside);
         gp.ccl = pl.maxside / R;
         if (gp.ccl > kMaxC) throw ConfigError("invalid geometry: layer side exceeds the cluster transform");
+        // tail size: D = 2C (measured best at the ELT scale), else 4C, else C -- the first whose layer kernels fit the sm_100 opt-in
+        // shared memory (227 KB less static) in fp64 -- fp32 engines use the same layout, so
+        // their fp64 preconditioner probes share the coefficient permutation
+        {
+            constexpr int kSmemBudget = 227 * 1024 - 2048;
+            const int flen = 2 * g.wavelet_order, C = gp.ccl;
+            gp.ctail = C;
+            for (int D : {2 * C, 4 * C}) {
+                if (D > pl.maxside / 2) continue;
+                if (clay::inv_smem(pl.maxside, C, D, flen, 8).total <= kSmemBudget &&
+                    clay::fwd_smem(pl.maxside, C, D, flen, 8).total <= kSmemBudget) {
+                    gp.ctail = D;
+                    break;
+                }
+            }
+            if (const char* v = std::getenv("FEWHA_TAIL")) {  // profiling override (power of two in [C, maxside/2])
+                const int D = std::atoi(v);
+                if (D >= C && D <= std::max(C, pl.maxside / 2) && (D & (D - 1)) == 0) gp.ctail = D;
+            }
+        }
         // gather tables: per (w,l) and axis, for every layer node the (source, weight) list,
         // ascending source (operators.hpp:129-135 weights as bilinear_stencil assigns them)
         struct Entry { int src; double w; };
@@ -682,10 +702,10 @@ struct Launch {
     static size_t a16(size_t v) { return (v + 15) & ~size_t(15); }
     // shared-memory maps: clayout.hpp (the kernels derive the same offsets)
     static size_t inv_cl_smem(const GeoParams& gp, int flen) {
-        return static_cast<size_t>(clay::inv_smem(gp.maxside, gp.ccl, flen, static_cast<int>(sizeof(T))).total);
+        return static_cast<size_t>(clay::inv_smem(gp.maxside, gp.ccl, gp.ctail, flen, static_cast<int>(sizeof(T))).total);
     }
     static size_t fwd_cl_smem(const GeoParams& gp, int flen) {
-        return static_cast<size_t>(clay::fwd_smem(gp.maxside, gp.ccl, flen, static_cast<int>(sizeof(T))).total);
+        return static_cast<size_t>(clay::fwd_smem(gp.maxside, gp.ccl, gp.ctail, flen, static_cast<int>(sizeof(T))).total);
     }
 
 #define FEWHA_FLEN_SWITCH(flen, CALL)          \

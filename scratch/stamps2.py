@@ -9,7 +9,7 @@ rec.phase_stamps(enable_only=True)
 for _ in range(3): prof = rec.profile_step()
 st = rec.phase_stamps()
 kinds = [k for k, _ in prof if k not in ("fit_control",)]
-for slot, kind in enumerate(kinds[:6]):
+for slot, kind in enumerate(kinds[:9]):
     a = st[slot].astype(np.int64); used = a[:, 0] > 0; a = a[used]; t0 = a[:, 0].min()
     rel = np.where(a > 0, a - t0, -1)
     cols = [k for k in range(16) if (rel[:, k] >= 0).any()]
