@@ -683,6 +683,7 @@ __global__ void __launch_bounds__(256, 2) k_gather(const GeoParams gp, const Buf
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ GDesc s_desc[kMaxW];
     __shared__ unsigned long long s_mbar;
+    pdl_launch_dependents();  // the forward kernel's prologue may start (it waits before reading y)
     const int u = blockIdx.x, l = blockIdx.y, b = blockIdx.z;
     const int side = gp.side[l];
     const int R = side < kGatherRows ? side : kGatherRows;
@@ -790,8 +791,10 @@ __device__ __forceinline__ void inv_phase(const GeoParams& gp, const Bufs<T>& bf
     prefetch_block(bf.jinv + gp.coff[l] + roff, sj, mode == kPlain ? 0 : cnt, &s_mbar, 0);  // constant
     Carry cin{};
     const int ci = b * (gp.iters + 1) + upd - 1;
+    // nothing the frame writes may be read before this point: with programmatic launch
+    // every kernel of the chain can be resident before its predecessors finish
+    pdl_wait();  // the predecessor's outputs (r, c, p, q, Mz, dot partials, carry) are complete
     if (may_update && tid == 0) cin = bf.carry[ci];
-    pdl_wait();  // the predecessor's outputs (r, c, p, q, Mz, dot partials) are complete
     // thread 0 issues every block and arrives at once (misaligned blocks: cooperative copies)
     if (mode == kPlain) {
         prefetch_block(bf.in + vbase, sr, cnt, &s_mbar, 0);
