@@ -150,6 +150,26 @@ int fewha_gpu_sh_transpose(fewha_gpu_t h, const double* meas, double* wf, int co
  * a may be NULL (no correction).  layers: nodal [count][n]. */
 int fewha_gpu_forward_slopes(fewha_gpu_t h, const double* layers, const double* a, double* meas, int count);
 
+/* --- StepTelemetry (reconstructor.hpp:94-102; bench.hpp:214-228 CSV schema) ---
+ * Opt-in: enabling re-captures the frame graph with an event-record node around
+ * every launch (which also serialises programmatic launch overlap, so frames
+ * run a few microseconds slower while it is on).  After a frame,
+ * fewha_gpu_last_telemetry waits for it and fills the device-timed stages:
+ *   stage1_us  W^-1 kernels (reference: per-layer W^-1 kernels)
+ *   stage2_us  per-WFS Gamma/P/C^-1/Gamma^T kernels incl. the RHS
+ *   stage3_us  P^T / W / alpha D kernels incl. the RHS
+ *   pcg_us     the PCG iterations (first W^-1 .. last W)
+ *   fit_us     fitting W^-1 (with the fused last update) + fit + control
+ *   total_us   the whole frame
+ * rho is returned by fewha_gpu_step (rho_out). */
+typedef struct {
+    long long step; /* frames run by this handle (StepTelemetry::step) */
+    int valid;      /* 0: telemetry off, or no frame since it was enabled */
+    double stage1_us, stage2_us, stage3_us, pcg_us, fit_us, total_us;
+} fewha_gpu_telemetry_t;
+int fewha_gpu_enable_telemetry(fewha_gpu_t h, int on);
+int fewha_gpu_last_telemetry(fewha_gpu_t h, fewha_gpu_telemetry_t* out);
+
 /* --- per-WFS sharding (the north star's multi-GPU split) -------
  * Shard `rank` of `world` owns a contiguous WFS range, balanced by wavefront
  * nodes: its WFS kernels (Gamma, C^-1, P) run only those WFS and its adjoint

@@ -35,7 +35,7 @@ EXPORTS = (
     "fewha_gpu_build_rhs", "fewha_gpu_add_dm_slopes", "fewha_gpu_fit_to_mirrors", "fewha_gpu_wavelet",
     "fewha_gpu_propagate", "fewha_gpu_propagate_transpose", "fewha_gpu_sh", "fewha_gpu_sh_transpose",
     "fewha_gpu_forward_slopes", "fewha_gpu_shard_range", "fewha_gpu_nccl_unique_id", "fewha_gpu_shard",
-    "fewha_gpu_shard_wfs", "fewha_gpu_group_step_device",
+    "fewha_gpu_shard_wfs", "fewha_gpu_group_step_device", "fewha_gpu_enable_telemetry", "fewha_gpu_last_telemetry",
 )
 
 
@@ -70,6 +70,11 @@ class _State(C.Structure):
     _fields_ = [("c", C.POINTER(C.c_double)), ("b", C.POINTER(C.c_double)), ("r", C.POINTER(C.c_double)),
                 ("p", C.POINTER(C.c_double)), ("q", C.POINTER(C.c_double)), ("scalars", C.c_double * 3),
                 ("a_prev2", C.POINTER(C.c_double)), ("a_prev", C.POINTER(C.c_double))]
+
+
+class _Telemetry(C.Structure):
+    _fields_ = [("step", C.c_longlong), ("valid", C.c_int), ("stage1_us", C.c_double), ("stage2_us", C.c_double),
+                ("stage3_us", C.c_double), ("pcg_us", C.c_double), ("fit_us", C.c_double), ("total_us", C.c_double)]
 
 
 class _DevBufs(C.Structure):
@@ -132,6 +137,8 @@ def lib() -> C.CDLL:
         L.fewha_gpu_shard.argtypes = [vp, C.c_int, C.c_int, C.c_char_p]
         L.fewha_gpu_shard_wfs.argtypes = [vp, ip, ip]
         L.fewha_gpu_group_step_device.argtypes = [C.POINTER(vp), C.c_int]
+        L.fewha_gpu_enable_telemetry.argtypes = [vp, C.c_int]
+        L.fewha_gpu_last_telemetry.argtypes = [vp, C.POINTER(_Telemetry)]
         _lib_handle = L
     return _lib_handle
 
@@ -354,6 +361,19 @@ class Reconstructor:
         return out if count == 1 else out.reshape(count, self.dims.S)
 
     # -- CUDA-resident path -----------------------------------------------------------
+    def enable_telemetry(self, on: bool = True):
+        """StepTelemetry stage timings for every graph frame (opt-in, serialising)."""
+        self._chk(self._L.fewha_gpu_enable_telemetry(self._h, 1 if on else 0))
+
+    def last_telemetry(self) -> dict:
+        """Reconstructor::last_telemetry(): step, stage1/2/3, pcg, fit, total (us), rho."""
+        t = _Telemetry()
+        self._chk(self._L.fewha_gpu_last_telemetry(self._h, C.byref(t)))
+        out = {k: getattr(t, k) for k, _ in _Telemetry._fields_}
+        out["valid"] = bool(out["valid"])
+        out["rho"] = getattr(self, "last_rho", None)
+        return out
+
     def shard(self, rank: int, world: int, nccl_id: bytes | None = None):
         """Own the WFS of shard rank/world.  nccl_id: multi-process
         NCCL exchange of the partial layer sums; None: in-process group member."""

@@ -226,6 +226,23 @@ int fewha_gpu_forward_slopes(fewha_gpu_t h, const double* layers, const double* 
     H_GUARD(h->eng->forward_slopes(layers, a, meas, count))
 }
 
+int fewha_gpu_enable_telemetry(fewha_gpu_t h, int on) { H_GUARD(h->eng->enable_telemetry(on != 0)) }
+
+int fewha_gpu_last_telemetry(fewha_gpu_t h, fewha_gpu_telemetry_t* out) {
+    if (!out) return FEWHA_ARG;
+    H_GUARD({
+        const auto t = h->eng->last_telemetry();
+        out->step = t.step;
+        out->valid = t.valid ? 1 : 0;
+        out->stage1_us = t.stage1_us;
+        out->stage2_us = t.stage2_us;
+        out->stage3_us = t.stage3_us;
+        out->pcg_us = t.pcg_us;
+        out->fit_us = t.fit_us;
+        out->total_us = t.total_us;
+    })
+}
+
 // ---- per-WFS sharding ----
 int fewha_gpu_shard_range(const char* path, int rank, int world, int* wfs_begin, int* wfs_end) {
     if (!path) return FEWHA_ARG;

@@ -800,6 +800,11 @@ struct EngineImpl {
     GeoParams gp{};      // with device table pointers (engine precision)
     GeoParams gp64{};    // fp64 plan for the preconditioner probes (== gp in fp64 engines)
     GeoParams gpf{};     // plan of the frame's per-WFS kernels (== gp unless sharded)
+    // StepTelemetry (reconstructor.hpp:94-102): opt-in event-record nodes in the frame graph
+    bool telemetry_on = false, telem_pending = false;
+    long long step_counter = 0;
+    std::vector<cudaEvent_t> tev;
+    std::vector<int> tkind;
     // per-WFS sharding: this engine owns WFS [gpf.wa, gpf.wb)
     bool sharded = false;
     int shard_rank = 0, shard_world = 1;
@@ -994,7 +999,25 @@ struct EngineImpl {
         if (sharded && !comm) throw ArgError("shard group members step through fewha_gpu_group_step_device");
         cudaGraph_t gr;
         CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
-        launch_frame<T>(stream);
+        if (telemetry_on) {  // event-record nodes around every launch (StepTelemetry)
+            tkind.clear();
+            size_t k = 0;
+            auto rec = [&] {
+                if (k == tev.size()) {
+                    cudaEvent_t e;
+                    CK(cudaEventCreate(&e));
+                    tev.push_back(e);
+                }
+                CK(cudaEventRecordWithFlags(tev[k++], stream, cudaEventRecordExternal));  // a graph node
+            };
+            rec();
+            launch_frame<T>(stream, [&](int kind) {
+                tkind.push_back(kind);
+                rec();
+            });
+        } else {
+            launch_frame<T>(stream);
+        }
         CK(cudaStreamEndCapture(stream, &gr));
         CK(cudaGraphInstantiate(&graph, gr, 0));
         CK(cudaGraphDestroy(gr));
@@ -1212,6 +1235,7 @@ Engine::~Engine() {
     if (!p_) return;
     cudaSetDevice(p_->device);
     p_->invalidate_graph();
+    for (auto ev : p_->tev) cudaEventDestroy(ev);
     if (p_->comm) NcclApi::get().CommDestroy(p_->comm);
     if (p_->own_stream && p_->stream) cudaStreamDestroy(p_->stream);
 }
@@ -1405,6 +1429,8 @@ void Engine::step(const double* slopes, double* coeffs, double* dm, double* rho,
     if (P.precision == 64) P.ensure_graph<double>();
     else P.ensure_graph<float>();
     CK(cudaGraphLaunch(P.graph, st));
+    ++P.step_counter;
+    P.telem_pending = P.telemetry_on;
     std::vector<int> status(B), nl(B);
     const int* dstat = P.precision == 64 ? P.sd.bf.status : P.sf.bf.status;
     const int* dnl = P.precision == 64 ? P.sd.bf.nlog : P.sf.bf.nlog;
@@ -1508,6 +1534,47 @@ void Engine::step_device(const void* d_slopes) {
     if (P.precision == 64) P.ensure_graph<double>();
     else P.ensure_graph<float>();
     CK(cudaGraphLaunch(P.graph, st));
+    ++P.step_counter;
+    P.telem_pending = P.telemetry_on;
+}
+
+void Engine::enable_telemetry(bool on) {
+    auto& P = *p_;
+    if (P.telemetry_on == on) return;
+    P.telemetry_on = on;
+    P.telem_pending = false;
+    P.invalidate_graph();
+}
+
+// StepTelemetry of the last graph frame (reconstructor.hpp:94-102) from the event
+// nodes: stage1 = W^-1 kernels, stage2 = per-WFS kernels (incl. RHS), stage3 =
+// P^T / W / alpha D kernels (incl. RHS), pcg = the fused PCG iterations (first
+// W^-1 through the last W; the last update is fused into the fitting W^-1), fit =
+// fitting W^-1 + fit + control.  Times are in microseconds.
+StepTelemetry Engine::last_telemetry() {
+    auto& P = *p_;
+    StepTelemetry t;
+    t.step = P.step_counter;
+    if (!P.telem_pending) return t;
+    CK(cudaSetDevice(P.device));
+    CK(cudaEventSynchronize(P.tev[P.tkind.size()]));
+    bool in_pcg = false;
+    for (size_t i = 0; i < P.tkind.size(); ++i) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, P.tev[i], P.tev[i + 1]));
+        const double us = 1000.0 * ms;
+        const int k = P.tkind[i];
+        if (k == kKindInvPcg0) in_pcg = true;
+        if (k == kKindInvFit) in_pcg = false;
+        if (k == kKindInvPcg0 || k == kKindInvPcg || k == kKindInvFit) t.stage1_us += us;
+        else if (k == kKindWfsRhs || k == kKindWfs) t.stage2_us += us;
+        else if (k == kKindGather || k == kKindFwdRhs || k == kKindFwdPcg) t.stage3_us += us;
+        if (in_pcg) t.pcg_us += us;
+        if (k == kKindInvFit || k == kKindFit) t.fit_us += us;
+        t.total_us += us;
+    }
+    t.valid = true;
+    return t;
 }
 
 void Engine::load_slopes(const void* src, bool on_device) {

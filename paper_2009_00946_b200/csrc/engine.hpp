@@ -13,6 +13,13 @@ namespace fewha_gpu {
 
 struct EngineImpl;
 
+// StepTelemetry (reconstructor.hpp:94-102), device-timed
+struct StepTelemetry {
+    long long step = 0;
+    bool valid = false;
+    double stage1_us = 0, stage2_us = 0, stage3_us = 0, pcg_us = 0, fit_us = 0, total_us = 0;
+};
+
 class Engine;
 // contiguous WFS range [first, second) of shard `rank` of `world` (balanced by wavefront nodes)
 std::pair<int, int> shard_range(const Geometry& g, int rank, int world);
@@ -48,6 +55,8 @@ public:
     void step_device(const void* d_slopes);
     void load_slopes(const void* src, bool on_device);
     void sync_check();
+    void enable_telemetry(bool on);
+    StepTelemetry last_telemetry();
     int launches_per_step() const;
     int profile_step(float* ms, int* kinds, int max);
     void enable_stamps(bool on);

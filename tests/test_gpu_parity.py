@@ -389,3 +389,28 @@ def test_transforms_mixed_sides_and_orders(case, tmp_path, precision):
             tol_a = max(STEP_TOL[64], 10.0 * sens_a)
             assert rel_err(g.coeffs(), c_o) <= tol_c, ("c", k, rel_err(g.coeffs(), c_o), tol_c)
             assert rel_err(a_g, a_o) <= tol_a, ("a", k, rel_err(a_g, a_o), tol_a)
+
+
+def test_step_telemetry():
+    """StepTelemetry (reconstructor.hpp:94-102): device-timed stages of graph
+    frames; enabling it changes no result bit."""
+    path = preset("elt_mcao84_3dm.json")
+    g0, g1 = fg.Reconstructor(path), fg.Reconstructor(path)
+    g1.enable_telemetry(True)
+    assert not g1.last_telemetry()["valid"]
+    rng = np.random.default_rng(2)
+    for k in range(3):
+        s = rng.standard_normal(g0.dims.S) * 0.01
+        a0, a1 = g0.step(s), g1.step(s)
+        assert np.array_equal(a0, a1)
+        t = g1.last_telemetry()
+        assert t["valid"] and t["step"] == k + 1
+        assert t["total_us"] > 0 and t["pcg_us"] > 0 and t["fit_us"] > 0
+        for key in ("stage1_us", "stage2_us", "stage3_us"):
+            assert t[key] > 0
+        assert t["stage1_us"] + t["stage2_us"] + t["stage3_us"] <= t["total_us"] * (1 + 1e-6)
+        assert t["pcg_us"] < t["total_us"]
+        assert len(t["rho"]) == g1.dims.iters
+    g1.enable_telemetry(False)
+    g1.step(s)
+    assert not g1.last_telemetry()["valid"]
