@@ -127,10 +127,12 @@ FEWHA_HD FwdSmem fwd_smem(int maxside, int C, int D, int flen, int elem) {
 struct InvSmem {
     int v, vstride, z, x0, x1, aw, tb, tb2, total;
 };
-FEWHA_HD InvSmem inv_smem(int maxside, int C, int D, int flen, int elem) {
+// staged = 0: the six vectors are read straight from global memory (batch mode:
+// the smaller footprint doubles the resident clusters per SM)
+FEWHA_HD InvSmem inv_smem(int maxside, int C, int D, int flen, int elem, int staged = 1) {
     InvSmem m{};
     const int P = maxside + 1, R = band_rows(maxside, C, D, 0), H = flen / 2 - 1;
-    m.vstride = a16(compact_size(maxside, C, D, 0) * elem);
+    m.vstride = staged ? a16(compact_size(maxside, C, D, 0) * elem) : 0;
     m.v = 0;
     m.z = 6 * m.vstride;
     m.x0 = m.z + a16(compact_size(maxside, C, D, H) * elem);

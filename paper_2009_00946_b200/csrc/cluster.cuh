@@ -763,12 +763,13 @@ __device__ __forceinline__ void inv_phase(const GeoParams& gp, const Bufs<T>& bf
     constexpr int H = FLEN / 2 - 1;
     __shared__ int s_off[2 * (kMaxLev + 1)];
     const LPlan p = make_plan(S, C, gp.ctail, q, H, s_off);
-    const clay::InvSmem sm = clay::inv_smem(gp.maxside, C, gp.ctail, FLEN, static_cast<int>(sizeof(T)));
+    const bool staged = gp.inv_staged != 0;
+    const clay::InvSmem sm = clay::inv_smem(gp.maxside, C, gp.ctail, FLEN, static_cast<int>(sizeof(T)), gp.inv_staged);
     const int P = gp.maxside + 1;
     T* v[6];
 #pragma unroll
     for (int i = 0; i < 6; ++i) v[i] = reinterpret_cast<T*>(smem_raw + sm.v + i * sm.vstride);
-    T *sr = v[0], *sj = v[1], *sp = v[2], *sq = v[3], *sc = v[4], *sm_ = v[5];
+    T *sr = v[0], *sj = v[1], *sp = v[2], *sq = v[3], *sc = v[4], *sm_ = v[5];  // staged operands
     T* z = reinterpret_cast<T*>(smem_raw + sm.z);
     T* x0 = reinterpret_cast<T*>(smem_raw + sm.x0);
     T* x1 = reinterpret_cast<T*>(smem_raw + sm.x1);
@@ -788,7 +789,7 @@ __device__ __forceinline__ void inv_phase(const GeoParams& gp, const Bufs<T>& bf
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
-    prefetch_block(bf.jinv + gp.coff[l] + roff, sj, mode == kPlain ? 0 : cnt, &s_mbar, 0);  // constant
+    if (staged) prefetch_block(bf.jinv + gp.coff[l] + roff, sj, mode == kPlain ? 0 : cnt, &s_mbar, 0);  // constant
     Carry cin{};
     const int ci = b * (gp.iters + 1) + upd - 1;
     // nothing the frame writes may be read before this point: with programmatic launch
@@ -796,7 +797,15 @@ __device__ __forceinline__ void inv_phase(const GeoParams& gp, const Bufs<T>& bf
     pdl_wait();  // the predecessor's outputs (r, c, p, q, Mz, dot partials, carry) are complete
     if (may_update && tid == 0) cin = bf.carry[ci];
     // thread 0 issues every block and arrives at once (misaligned blocks: cooperative copies)
-    if (mode == kPlain) {
+    if (!staged) {
+        // operands read in place below
+        sr = const_cast<T*>(mode == kPlain ? bf.in + vbase : bf.r + vbase);
+        sj = const_cast<T*>(bf.jinv + gp.coff[l] + roff);
+        sp = bf.p + vbase;
+        sq = bf.q + vbase;
+        sc = bf.c + vbase;
+        sm_ = bf.mz + vbase;
+    } else if (mode == kPlain) {
         prefetch_block(bf.in + vbase, sr, cnt, &s_mbar, 0);
     } else {
         prefetch_block(bf.r + vbase, sr, cnt, &s_mbar, 0);
@@ -839,10 +848,10 @@ __device__ __forceinline__ void inv_phase(const GeoParams& gp, const Bufs<T>& bf
     } else {
         const bool apply = s_apply != 0;
         const T beta = static_cast<T>(s_beta), alpha = static_cast<T>(s_alpha);
-        T* __restrict__ pr = bf.r + vbase;
-        T* __restrict__ pp = bf.p + vbase;
-        T* __restrict__ pq = bf.q + vbase;
-        T* __restrict__ pc = bf.c + vbase;
+        T* pr = bf.r + vbase;  // (alias the operands when they are read in place)
+        T* pp = bf.p + vbase;
+        T* pq = bf.q + vbase;
+        T* pc = bf.c + vbase;
         for_owned(p, [&](int o, int zo, int) {
             T rr = sr[o], cc = sc[o];
             const T ji = sj[o];

@@ -701,8 +701,18 @@ struct Launch {
     }
     static size_t a16(size_t v) { return (v + 15) & ~size_t(15); }
     // shared-memory maps: clayout.hpp (the kernels derive the same offsets)
-    static size_t inv_cl_smem(const GeoParams& gp, int flen) {
-        return static_cast<size_t>(clay::inv_smem(gp.maxside, gp.ccl, gp.ctail, flen, static_cast<int>(sizeof(T))).total);
+    static size_t inv_cl_smem(const GeoParams& gp, int flen, int staged = 1) {
+        return static_cast<size_t>(
+            clay::inv_smem(gp.maxside, gp.ccl, gp.ctail, flen, static_cast<int>(sizeof(T)), staged).total);
+    }
+    // TMA staging of the inverse kernel's operands pays for a single instance (latency);
+    // batches stream them from global memory at twice the residency
+    static int inv_staged_for(int count) {
+        static const int mode = [] {
+            const char* v = std::getenv("FEWHA_INV_STAGE");
+            return v ? std::atoi(v) : -1;
+        }();
+        return mode >= 0 ? (mode ? 1 : 0) : (count <= 2 ? 1 : 0);
     }
     static size_t fwd_cl_smem(const GeoParams& gp, int flen) {
         return static_cast<size_t>(clay::fwd_smem(gp.maxside, gp.ccl, gp.ctail, flen, static_cast<int>(sizeof(T))).total);
@@ -750,8 +760,10 @@ struct Launch {
     // layer kernels: grid (C, L, count), cluster (C,1,1)
     static void cl(int flen, bool inverse, const GeoParams& gp, const Bufs<T>& bf, int mode, int it, int count,
                    cudaStream_t st, int fit_term = 1) {
-        const size_t smem = inverse ? inv_cl_smem(gp, flen) : fwd_cl_smem(gp, flen);
-#define FEWHA_LAUNCH(N) CK((launch_layer_cluster<T, N>(inverse, gp, bf, mode, it, count, st, fit_term, smem)))
+        GeoParams g2 = gp;
+        g2.inv_staged = inv_staged_for(count);
+        const size_t smem = inverse ? inv_cl_smem(g2, flen, g2.inv_staged) : fwd_cl_smem(g2, flen);
+#define FEWHA_LAUNCH(N) CK((launch_layer_cluster<T, N>(inverse, g2, bf, mode, it, count, st, fit_term, smem)))
         FEWHA_FLEN_SWITCH(flen, FEWHA_LAUNCH)
 #undef FEWHA_LAUNCH
     }

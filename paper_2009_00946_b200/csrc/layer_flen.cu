@@ -24,8 +24,8 @@ cudaError_t launch_layer_cluster(bool inverse, const GeoParams& gp, const Bufs<T
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (griddepcontrol in the kernels)
-    const char* pdl = std::getenv("FEWHA_PDL");
-    attr[1].val.programmaticStreamSerializationAllowed = (pdl && pdl[0] == '1') ? 1 : 0;
+    const char* pdl = std::getenv("FEWHA_PDL");  // on unless FEWHA_PDL=0 (as engine.cu pdl_enabled)
+    attr[1].val.programmaticStreamSerializationAllowed = (pdl && pdl[0] == '0') ? 0 : 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
     if (inverse) return cudaLaunchKernelEx(&cfg, k_inv_cluster<T, FLEN>, gp, bf, mode, it);
