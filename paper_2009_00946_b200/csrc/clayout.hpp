@@ -47,7 +47,7 @@ FEWHA_HD int lg2(int v) {
 // the cluster, the D x D tail (levels below) runs on rank 0 inside one CTA --
 // the coarse levels cost a cluster barrier each but almost no arithmetic, so
 // finishing them locally is cheaper.  Layers with S < 2D are tail-only (whole
-// layer on rank 0).  The host picks D = 2C (measured best), else 4C, else C, whose kernels
+// layer on rank 0).  The host picks D = 4C (measured best), else 2C, else C, whose kernels
 // fit in shared memory (GeoParams::ctail).
 FEWHA_HD bool dist(int S, int C, int D) { return S >= 2 * D; }
 FEWHA_HD int tail(int S, int C, int D) { return dist(S, C, D) ? D : S; }
@@ -143,8 +143,14 @@ FEWHA_HD InvSmem inv_smem(int maxside, int C, int D, int flen, int elem, int sta
     // tb2 aliases x1: the tail is finished (and, if its output sits in tb2, consumed
     // by the first distributed level, which writes x0) before x1 is first written
     const int Tb = tail_max(maxside, C, D);
-    m.tb2 = m.x1;
-    m.total = m.tb + a16(Tb * (Tb + 1) * elem);
+    const int tbb = a16(Tb * (Tb + 1) * elem);
+    if (tbb <= a16(R * P * elem)) {
+        m.tb2 = m.x1;
+        m.total = m.tb + tbb;
+    } else {  // tail larger than a band: no aliasing
+        m.tb2 = m.tb + tbb;
+        m.total = m.tb2 + tbb;
+    }
     return m;
 }
 

@@ -290,6 +290,15 @@ __device__ void tail_forward(const GeoParams& gp, const T* src, int ps, int Tt, 
 // out(2m1+u1, 2m2+u2) = sum_{kk2,b2} G_b2 sum_{kk1,b1} G_b1 X(b1 h + m1-kk1, b2 h + m2-kk2),
 // X = previous level output in the LL quadrant, the tail coefficients elsewhere.
 // Returns the buffer holding the T x T output (pitch T+1).
+// The buffer tail_inverse(.., Tt, b0, b1) returns (fused levels alternate b0, b1,
+// starting with b0; the separable levels stay in place).
+template <typename T, int FLEN>
+__device__ __forceinline__ T* tail_buffer(int Tt, T* b0, T* b1) {
+    if (Tt == 1) return b0;
+    const int sf = Tt < kFusedTail ? Tt : kFusedTail;
+    return (ilog2(sf) & 1) ? b0 : b1;
+}
+
 template <typename T, int FLEN>
 __device__ T* tail_inverse(const GeoParams& gp, const T* zt, int Tt, T* b0, T* b1) {
     const int tid = threadIdx.x, nthr = blockDim.x;
@@ -433,21 +442,17 @@ __device__ void cdwt_forward(const GeoParams& gp, const LPlan& p, T* x0, T* x1, 
 // matching arrive follows this rank's last remote read).
 // ---------------------------------------------------------------------------
 template <typename T, int FLEN>
-__device__ T* cdwt_inverse(const GeoParams& gp, const LPlan& p, const T* z, T* x0, T* x1, T* aw, T* tb, T* tb2,
+__device__ T* cdwt_inverse(const GeoParams& gp, const LPlan& p, const T* z, T* x0, T* x1, T* aw, T* tl,
                            int P, int* outP) {
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int S = p.S, C = p.C, q = p.q, H = p.H;
     constexpr int HF = FLEN / 2;
     constexpr int SEGP = 4;  // output pairs per thread item
     const int Tt = p.T;
-    // tail: T x T block (the whole layer when there are no distributed levels)
-    T* tl = tb;
-    if (p.nlev > 0 || q == 0) tl = tail_inverse<T, FLEN>(gp, z + p.offH[p.nlev], Tt, tb, tb2);
-    if (p.nlev == 0) {
-        *outP = Tt + 1;
-        return tl;
-    }
+    // tl: rank 0's T x T tail output (pitch T+1), computed by rank 0 before the
+    // cluster barrier that precedes this call; the first level reads it remotely
     stamp(gp, 4);
+    const T* tl0 = q == 0 ? tl : rmt(tl, 0);
     T* prev = tl;
     T* cur = x0;
     T* other = x1;
@@ -465,7 +470,7 @@ __device__ T* cdwt_inverse(const GeoParams& gp, const LPlan& p, const T* z, T* x
             if (j < h) {
                 const int mm = (m0 - H + i) & (h - 1);
                 if (first) {
-                    v = tl[mm * (Tt + 1) + j];
+                    v = tl0[mm * (Tt + 1) + j];
                 } else {
                     const int own = mm >> lk;
                     const T* src = own == q ? prev : rmt(prev, own);
@@ -880,8 +885,25 @@ __device__ __forceinline__ void inv_phase(const GeoParams& gp, const Bufs<T>& bf
         if (tid == 0) bf.rho_part[(static_cast<size_t>(b) * gp.iters + it) * slots + l * C + q] = t;
     }
     stamp(gp, 2);
-    if (p.nlev > 0) {
-        cl_sync();  // every rank's owned z is complete
+    // rank 0 owns the whole T x T tail of z: it runs the tail levels before the
+    // barrier (the other ranks read the tail output rows remotely at the first
+    // distributed level); tail-only layers end here
+    T* tl = tb;
+    if (q == 0) {
+        __syncthreads();  // z's tail complete
+        tl = tail_inverse<T, FLEN>(gp, z + p.offH[p.nlev], p.T, tb, tb2);
+    }
+    if (p.nlev == 0) {
+        if (q == 0) {
+            T* __restrict__ phi = bf.phi + lbase;
+            for (int e = tid; e < S * S; e += blockDim.x) phi[e] = tl[(e >> p.lsS) * (S + 1) + (e & (S - 1))];
+        }
+        return;
+    }
+    // every rank computes the same tail buffer choice (the tail level count is uniform)
+    tl = tail_buffer<T, FLEN>(p.T, tb, tb2);
+    {
+        cl_sync();  // every rank's owned z is complete, rank 0's tail output too
         stamp(gp, 5);
         const int nthr = blockDim.x;
         for (int lv = 0; lv < p.nlev; ++lv) {
@@ -903,21 +925,16 @@ __device__ __forceinline__ void inv_phase(const GeoParams& gp, const Bufs<T>& bf
                 }
             }
         }
-        if (q != 0) {
-            const int to = p.offH[p.nlev];
-            const T* z0 = rmt(z, 0);
-            for (int e = tid; e < p.T * p.T; e += nthr) z[to + e] = z0[to + e];
-        }
         __syncthreads();
     }
     stamp(gp, 3);
     int outP = P;
-    const T* out = cdwt_inverse<T, FLEN>(gp, p, z, x0, x1, aw, tb, tb2, P, &outP);
+    const T* out = cdwt_inverse<T, FLEN>(gp, p, z, x0, x1, aw, tl, P, &outP);
     stamp(gp, 9);
     const int R = clay::band_rows(S, C, gp.ctail, q), r0 = clay::band_row0(S, C, gp.ctail, q);
     T* __restrict__ phi = bf.phi + lbase + static_cast<size_t>(r0) * S;
     for (int e = tid; e < R * S; e += blockDim.x) phi[e] = out[(e >> p.lsS) * outP + (e & (S - 1))];
-    if (p.nlev > 0) cl_wait();  // no rank exits while its level outputs may still be read
+    cl_wait();  // no rank exits while its level outputs (or rank 0's tail) may still be read
 }
 
 template <typename T, int FLEN>

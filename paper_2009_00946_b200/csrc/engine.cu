@@ -340,14 +340,14 @@ Plan build_plan(const Geometry& g, int elem_bytes, int wa = 0, int wb = -1) {
         const int R = std::min(16, pl.maxside);
         gp.ccl = pl.maxside / R;
         if (gp.ccl > kMaxC) throw ConfigError("invalid geometry: layer side exceeds the cluster transform");
-        // tail size: D = 2C (measured best at the ELT scale), else 4C, else C -- the first whose layer kernels fit the sm_100 opt-in
+        // tail size: D = 4C (measured best at the ELT scale), else 2C, else C -- the first whose layer kernels fit the sm_100 opt-in
         // shared memory (227 KB less static) in fp64 -- fp32 engines use the same layout, so
         // their fp64 preconditioner probes share the coefficient permutation
         {
             constexpr int kSmemBudget = 227 * 1024 - 2048;
             const int flen = 2 * g.wavelet_order, C = gp.ccl;
             gp.ctail = C;
-            for (int D : {2 * C, 4 * C}) {
+            for (int D : {4 * C, 2 * C}) {
                 if (D > pl.maxside / 2) continue;
                 if (clay::inv_smem(pl.maxside, C, D, flen, 8).total <= kSmemBudget &&
                     clay::fwd_smem(pl.maxside, C, D, flen, 8).total <= kSmemBudget) {
