@@ -259,6 +259,7 @@ __device__ void tail_forward(const GeoParams& gp, const T* src, int ps, int Tt, 
         pc = Tt + 1;
         nxt = b1;
     }
+    stamp(gp, 6);
     for (int s = s0; s >= 2; s >>= 1) {
         const int h = s >> 1, ls = ilog2(s);
         for (int e = tid; e < s * s; e += nthr) {
@@ -343,6 +344,7 @@ __device__ T* tail_inverse(const GeoParams& gp, const T* zt, int Tt, T* b0, T* b
         return b0;
     }
     T* buf = const_cast<T*>(cur);  // sf x sf output, pitch Tt+1
+    stamp(gp, 6);
     for (int s = 2 * sf; s <= Tt; s <<= 1) {  // separable levels: columns, then rows (wavelet.hpp:170-196)
         const int h = s >> 1, ls = ilog2(s);
         for (int e = tid; e < s * s; e += nthr) {
@@ -351,8 +353,10 @@ __device__ T* tail_inverse(const GeoParams& gp, const T* zt, int Tt, T* b0, T* b
         }
         __syncthreads();
         synthesis_lines<T, FLEN, true>(buf, Tt + 1, s, s, gp);
+        if (s == Tt) stamp(gp, 7);
         synthesis_lines<T, FLEN, false>(buf, Tt + 1, s, s, gp);
     }
+    stamp(gp, 8);
     return buf;
 }
 
