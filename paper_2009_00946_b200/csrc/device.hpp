@@ -20,6 +20,7 @@ constexpr int kMaxM = 16;
 constexpr int kMaxC = 8;  // CTAs per layer cluster (portable cluster size)
 constexpr int kGatherRows = 4;  // layer rows per CTA of the adjoint-propagation gather
 constexpr int kMaxGU = 32;      // row groups per layer (max side 128 / kGatherRows)
+constexpr int kMaxWtCode = 1024;  // WFS tiles with a constant-bank position code
 
 // Fused-PCG carry (pcg.hpp:32-38 PcgScalars plus per-frame bookkeeping).
 struct Carry {
@@ -56,6 +57,9 @@ struct GeoParams {
     int wt_first[kMaxW + 1];  // first tile of each WFS (prefix), tiles row-major per WFS
     int wt_cols[kMaxW];       // tiles per row of WFS w
     int wa, wb;               // WFS owned by this plan's per-WFS kernels (all unless sharded)
+    // tile -> (w | i0/16 << 8 | j0/16 << 20), so a WFS tile CTA decodes its position from
+    // the constant bank (n_wtiles <= kMaxWtCode; larger geometries search wt_first)
+    unsigned wt_code[kMaxWtCode];
     int wt_base, wt_count;    // their tiles: [wt_base, wt_base + wt_count)
     const unsigned char* tblob;  // per-tile stencil tables [tile][screen][axis][H] idx, then weights
     int tt_stride_l, tt_stride_d, tt_off_d;  // byte stride per tile (layer / DM screens), DM base

@@ -127,7 +127,7 @@ int push_ranges(Plan& pl, const std::vector<Stencil1>& t, int n_target) {
 // wa..wb: the WFS this plan's per-WFS kernels own (all of them unless sharded,
 // SURVEY 8e): the WFS kernels run only those tiles and the adjoint gather sums
 // only those WFS.
-Plan build_plan(const Geometry& g, int elem_bytes, int wa = 0, int wb = -1) {
+Plan build_plan(const Geometry& g, int elem_bytes, int batch, int wa = 0, int wb = -1) {
     Plan pl;
     GeoParams& gp = pl.gp;
     const int L = static_cast<int>(g.layers.size()), W = static_cast<int>(g.wfs.size()),
@@ -293,6 +293,10 @@ Plan build_plan(const Geometry& g, int elem_bytes, int wa = 0, int wb = -1) {
     }
     gp.n_wtiles = static_cast<int>(pl.wtiles.size() / 3);
     gp.wt_first[W] = gp.n_wtiles;
+    for (int t = 0; t < gp.n_wtiles && t < kMaxWtCode; ++t)
+        gp.wt_code[t] = static_cast<unsigned>(pl.wtiles[3 * t]) |
+                        (static_cast<unsigned>(pl.wtiles[3 * t + 1] / gp.wtile) << 8) |
+                        (static_cast<unsigned>(pl.wtiles[3 * t + 2] / gp.wtile) << 20);
     gp.wt_base = gp.wt_first[wa];
     gp.wt_count = gp.wt_first[wb] - gp.wt_first[wa];
     // per-tile stencil tables of the tile's halo rows/columns for every screen, in the
@@ -344,13 +348,18 @@ Plan build_plan(const Geometry& g, int elem_bytes, int wa = 0, int wb = -1) {
         // shared memory (227 KB less static) in fp64 -- fp32 engines use the same layout, so
         // their fp64 preconditioner probes share the coefficient permutation
         {
-            constexpr int kSmemBudget = 227 * 1024 - 2048;
+            // Batches (> 2 instances) instead keep the forward and the streamed-operand
+            // inverse at two CTAs per SM (<= 113 KB each), which the 32^2 tail buffers break.
+            constexpr int kSmemBudget = 227 * 1024 - 2048, kTwoPerSm = 113 * 1024 - 2048;
             const int flen = 2 * g.wavelet_order, C = gp.ccl;
             gp.ctail = C;
             for (int D : {4 * C, 2 * C}) {
                 if (D > pl.maxside / 2) continue;
-                if (clay::inv_smem(pl.maxside, C, D, flen, 8).total <= kSmemBudget &&
-                    clay::fwd_smem(pl.maxside, C, D, flen, 8).total <= kSmemBudget) {
+                const bool fits = clay::inv_smem(pl.maxside, C, D, flen, 8).total <= kSmemBudget &&
+                                  clay::fwd_smem(pl.maxside, C, D, flen, 8).total <= kSmemBudget;
+                const bool two = clay::inv_smem(pl.maxside, C, D, flen, 8, 0).total <= kTwoPerSm &&
+                                 clay::fwd_smem(pl.maxside, C, D, flen, 8).total <= kTwoPerSm;
+                if (fits && (batch <= 2 || two)) {
                     gp.ctail = D;
                     break;
                 }
@@ -1208,12 +1217,12 @@ Engine::Engine(Geometry g, int precision, int batch, int device) : p_(std::make_
             gpx.fhi_f[k] = static_cast<float>(hi);
         }
     };
-    P.plan = build_plan(P.g, precision / 8);
+    P.plan = build_plan(P.g, precision / 8, batch);
     P.plan.gp.piston_exact = precision == 32 ? 1 : 0;
     set_filters(P.plan.gp);
     Plan plan64;
     if (precision == 32) {  // the preconditioner probes run in fp64 with their own tables
-        plan64 = build_plan(P.g, 8);
+        plan64 = build_plan(P.g, 8, batch);
         plan64.gp.piston_exact = 0;
         set_filters(plan64.gp);
     }
@@ -1322,7 +1331,7 @@ void Engine::shard(int rank, int world, const void* nccl_id) {
     P.shard_rank = rank;
     P.shard_world = world;
     P.sharded = world > 1 || nccl_id != nullptr;
-    Plan sp = build_plan(P.g, P.precision / 8, wa, wb);
+    Plan sp = build_plan(P.g, P.precision / 8, P.batch, wa, wb);
     sp.gp.piston_exact = P.gp.piston_exact;
     std::copy(std::begin(P.gp.flo), std::end(P.gp.flo), sp.gp.flo);
     std::copy(std::begin(P.gp.fhi), std::end(P.gp.fhi), sp.gp.fhi);

@@ -281,10 +281,19 @@ template <typename T, bool RHS>
 __device__ __forceinline__ void wfs_tile(const GeoParams& gp, const Bufs<T>& bf, int with_dm, int tile, int b,
                                          unsigned char* smem_raw) {
     constexpr int TS = kWfsTile, H = TS + 2, Q = TS + 1;
-    int w = 0;
-    while (w + 1 < gp.W && tile >= gp.wt_first[w + 1]) ++w;
-    const int local = tile - gp.wt_first[w], trow = local / gp.wt_cols[w];
-    const int i0 = trow * TS, j0 = (local - trow * gp.wt_cols[w]) * TS;
+    int w, i0, j0;
+    if (gp.n_wtiles <= kMaxWtCode) {
+        const unsigned code = gp.wt_code[tile];
+        w = static_cast<int>(code & 0xffu);
+        i0 = static_cast<int>((code >> 8) & 0xfffu) * TS;
+        j0 = static_cast<int>(code >> 20) * TS;
+    } else {
+        w = 0;
+        while (w + 1 < gp.W && tile >= gp.wt_first[w + 1]) ++w;
+        const int local = tile - gp.wt_first[w], trow = local / gp.wt_cols[w];
+        i0 = trow * TS;
+        j0 = (local - trow * gp.wt_cols[w]) * TS;
+    }
     const int ns = gp.ns[w], np = ns + 1;
     const int tid = threadIdx.x, nthr = blockDim.x;
     const bool screens_on = !RHS || with_dm;
