@@ -643,6 +643,7 @@ struct Work {
     T *in = nullptr, *out = nullptr, *a = nullptr;
     double* meas = nullptr;
     double* meas2 = nullptr;
+    size_t frame_out_bytes = 0;  // rho_log | status | nlog block (state workspaces)
     void alloc(const GeoParams& gp, int cnt, DevFree& fr, bool state) {
         count = cnt;
         const size_t n = static_cast<size_t>(gp.n) * cnt;
@@ -680,9 +681,14 @@ struct Work {
             const size_t np = static_cast<size_t>(gp.iters) * gp.L * kMaxC * cnt;
             bf.rho_part = A((double*)nullptr, np);
             bf.mu_part = A((double*)nullptr, np);
-            bf.rho_log = A((double*)nullptr, static_cast<size_t>(gp.iters) * cnt);
-            bf.status = A((int*)nullptr, cnt);
-            bf.nlog = A((int*)nullptr, cnt);
+            // per-frame host outputs in one block (one D2H copy): rho_log [cnt][iters] doubles,
+            // then status [cnt] and nlog [cnt] ints
+            const size_t nr = static_cast<size_t>(gp.iters) * cnt;
+            frame_out_bytes = nr * sizeof(double) + 2 * static_cast<size_t>(cnt) * sizeof(int);
+            auto* blk = A((unsigned char*)nullptr, frame_out_bytes);
+            bf.rho_log = reinterpret_cast<double*>(blk);
+            bf.status = reinterpret_cast<int*>(blk + nr * sizeof(double));
+            bf.nlog = bf.status + cnt;
         }
     }
 };
@@ -827,6 +833,7 @@ struct EngineImpl {
     std::vector<cudaEvent_t> tev;
     std::vector<int> tkind;
     // per-WFS sharding: this engine owns WFS [gpf.wa, gpf.wb)
+    void* host_out = nullptr;  // pinned staging of the per-frame rho/status/nlog block
     bool sharded = false;
     int shard_rank = 0, shard_world = 1;
     std::vector<void*> ypart;  // [iters+1] partial adjoint layer sums [B][n], one per exchange
@@ -1257,6 +1264,7 @@ Engine::~Engine() {
     cudaSetDevice(p_->device);
     p_->invalidate_graph();
     for (auto ev : p_->tev) cudaEventDestroy(ev);
+    if (p_->host_out) cudaFreeHost(p_->host_out);
     if (p_->comm) NcclApi::get().CommDestroy(p_->comm);
     if (p_->own_stream && p_->stream) cudaStreamDestroy(p_->stream);
 }
@@ -1452,13 +1460,12 @@ void Engine::step(const double* slopes, double* coeffs, double* dm, double* rho,
     CK(cudaGraphLaunch(P.graph, st));
     ++P.step_counter;
     P.telem_pending = P.telemetry_on;
-    std::vector<int> status(B), nl(B);
-    const int* dstat = P.precision == 64 ? P.sd.bf.status : P.sf.bf.status;
-    const int* dnl = P.precision == 64 ? P.sd.bf.nlog : P.sf.bf.nlog;
-    const double* drho = P.precision == 64 ? P.sd.bf.rho_log : P.sf.bf.rho_log;
-    CK(cudaMemcpyAsync(status.data(), dstat, B * sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(nl.data(), dnl, B * sizeof(int), cudaMemcpyDeviceToHost, st));
-    if (rho) CK(cudaMemcpyAsync(rho, drho, B * it * sizeof(double), cudaMemcpyDeviceToHost, st));
+    // rho_log | status | nlog in one copy into a pinned staging block
+    const size_t fob = P.precision == 64 ? P.sd.frame_out_bytes : P.sf.frame_out_bytes;
+    const void* dblk = P.precision == 64 ? static_cast<const void*>(P.sd.bf.rho_log)
+                                         : static_cast<const void*>(P.sf.bf.rho_log);
+    if (!P.host_out) CK(cudaMallocHost(&P.host_out, fob));
+    CK(cudaMemcpyAsync(P.host_out, dblk, fob, cudaMemcpyDeviceToHost, st));
     if (P.precision == 64) {
         if (dm) CK(cudaMemcpyAsync(dm, P.sd.bf.a_out, B * A * sizeof(double), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
@@ -1468,7 +1475,11 @@ void Engine::step(const double* slopes, double* coeffs, double* dm, double* rho,
         if (coeffs) d2h_coeff<float>(coeffs, P.sf.bf.c, P.plan.perm, B, st);
         if (dm) d2h_conv<float>(dm, P.sf.bf.a_out, B * A, st);
     }
-    if (n_rho) std::copy(nl.begin(), nl.end(), n_rho);
+    const auto* hrho = static_cast<const double*>(P.host_out);
+    const int* status = reinterpret_cast<const int*>(hrho + B * it);
+    const int* nl = status + B;
+    if (rho) std::copy(hrho, hrho + B * it, rho);
+    if (n_rho) std::copy(nl, nl + B, n_rho);
     for (size_t b = 0; b < B; ++b)
         if (status[b]) throw std::runtime_error("pcg_solve: non-finite scalar (indefinite operator?)");
 }
