@@ -528,7 +528,7 @@ __device__ T* cdwt_inverse(const GeoParams& gp, const LPlan& p, const T* z, T* x
 //   G(i, c)   = sum_q rw(i,q) psi(rs(i,q), c)      rows first, into shared G
 //   y(i, J)  += sum_{c: idx_c in {J-1, J}} w(c, J) G(i, c)   then columns
 // with w(c, J) = 1 - f_c (idx_c == J) or f_c (idx_c == J-1).  One CTA per
-// kGatherRows-row group of a layer (grid (kMaxGU, L, B): 144 CTAs at the ELT
+// gp.grows-row group of a layer (grid (side/grows, L, B): 288 CTAs at the ELT
 // scale).  Staging per chunk of WFS: the tables by one TMA bulk copy and each
 // WFS's psi rows [ilo, ihi) by one bulk copy each, issued by separate threads.
 // All WFS of a chunk are row-contracted in one pass, then column-contracted in
@@ -571,11 +571,11 @@ __device__ __forceinline__ void gather_issue(const GeoParams& gp, const T* psi_b
 }
 
 // Contract the staged row group, chunk by chunk (chunk 0 already issued by the caller).
-template <typename T, int KM>
+template <typename T, int KM, int ROWS>
 __device__ void gather_group(const GeoParams& gp, const T* __restrict__ psi_b, int l, T* __restrict__ y, T* gbuf,
                              unsigned char* stage, const GDesc* desc, unsigned long long* mbar) {
     const int side = gp.side[l];
-    const int R = side < kGatherRows ? side : kGatherRows;
+    const int R = side < ROWS ? side : ROWS;
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int lside = ilog2(side);
     const int groups = min(nthr >> lside, R);  // threads per layer column
@@ -583,13 +583,13 @@ __device__ void gather_group(const GeoParams& gp, const T* __restrict__ psi_b, i
     const int J = tid & (side - 1), grp = tid >> lside;
     const int i0 = grp * rows_pt;
     const bool worker = grp < groups;
-    const int gst = kGatherRows * gp.bd_cols_max;  // G stride per WFS
+    const int gst = ROWS * gp.bd_cols_max;  // G stride per WFS
     const int km = KM > 0 ? KM : gp.gather_km;  // taps per row in the staged tables
     const int o_rw = align16(R * km * 2), o_f = o_rw + align16(R * km * static_cast<int>(sizeof(T)));
     const int o_idx = o_f + align16((side + 3) * 2);
-    T out[kGatherRows];
+    T out[ROWS];
 #pragma unroll
-    for (int k = 0; k < kGatherRows; ++k) out[k] = T(0);
+    for (int k = 0; k < ROWS; ++k) out[k] = T(0);
     for (int k = 0; k < gp.nchunk; ++k) {
         const int w0 = gp.gchunk[k], w1 = gp.gchunk[k + 1];
         if (k > 0 && tid < 32) {
@@ -640,7 +640,7 @@ __device__ void gather_group(const GeoParams& gp, const T* __restrict__ psi_b, i
                 const T* G = gbuf + (w - w0) * gst;
                 const int c0 = first[J], c1 = first[J + 2];
                 if constexpr (KM == 0) {
-                    for (int k2 = 0; k2 < kGatherRows; ++k2) {
+                    for (int k2 = 0; k2 < ROWS; ++k2) {
                         if (k2 >= rows_pt) break;
                         const T* g = G + (i0 + k2) * nc;
                         T s = T(0);
@@ -663,7 +663,7 @@ __device__ void gather_group(const GeoParams& gp, const T* __restrict__ psi_b, i
                     cc[q] = c;
                 }
 #pragma unroll
-                for (int k2 = 0; k2 < kGatherRows; ++k2) {
+                for (int k2 = 0; k2 < ROWS; ++k2) {
                     if (k2 >= rows_pt) break;
                     const T* g = G + (i0 + k2) * nc;
                     T s = T(0);
@@ -677,14 +677,14 @@ __device__ void gather_group(const GeoParams& gp, const T* __restrict__ psi_b, i
     }
     if (worker) {
 #pragma unroll
-        for (int k = 0; k < kGatherRows; ++k) {
+        for (int k = 0; k < ROWS; ++k) {
             if (k >= rows_pt) break;
             y[(i0 + k) * side + J] = out[k];
         }
     }
 }
 
-// grid (kMaxGU, L, B): one CTA per kGatherRows-row group of a layer; y nodal, row-major.
+// grid (side/grows, L, B): one CTA per gp.grows-row group of a layer; y nodal, row-major.
 // Descriptors and chunk 0's tables are requested before the programmatic-launch
 // wait (they are constant), the psi blocks after it.
 template <typename T>
@@ -695,7 +695,7 @@ __global__ void __launch_bounds__(256, 2) k_gather(const GeoParams gp, const Buf
     pdl_launch_dependents();  // the forward kernel's prologue may start (it waits before reading y)
     const int u = blockIdx.x, l = blockIdx.y, b = blockIdx.z;
     const int side = gp.side[l];
-    const int R = side < kGatherRows ? side : kGatherRows;
+    const int R = side < gp.grows ? side : gp.grows;
     if (u * R >= side) return;
     const int tid = threadIdx.x;
     stamp(gp, 0);
@@ -724,13 +724,22 @@ __global__ void __launch_bounds__(256, 2) k_gather(const GeoParams gp, const Buf
     __syncthreads();  // descriptors visible
     stamp(gp, 12);
     T* y = bf.y + static_cast<size_t>(b) * gp.n + gp.coff[l] + static_cast<size_t>(u) * R * side;
-    switch (gp.gather_km) {
-        case 1: gather_group<T, 1>(gp, psi, l, y, gbuf, stage, s_desc, &s_mbar); break;
-        case 2: gather_group<T, 2>(gp, psi, l, y, gbuf, stage, s_desc, &s_mbar); break;
-        case 3: gather_group<T, 3>(gp, psi, l, y, gbuf, stage, s_desc, &s_mbar); break;
-        case 4: gather_group<T, 4>(gp, psi, l, y, gbuf, stage, s_desc, &s_mbar); break;
-        default: gather_group<T, 0>(gp, psi, l, y, gbuf, stage, s_desc, &s_mbar); break;
+#define FEWHA_GATHER_KM(ROWS)                                                                   \
+    switch (gp.gather_km) {                                                                     \
+        case 1: gather_group<T, 1, ROWS>(gp, psi, l, y, gbuf, stage, s_desc, &s_mbar); break;   \
+        case 2: gather_group<T, 2, ROWS>(gp, psi, l, y, gbuf, stage, s_desc, &s_mbar); break;   \
+        case 3: gather_group<T, 3, ROWS>(gp, psi, l, y, gbuf, stage, s_desc, &s_mbar); break;   \
+        case 4: gather_group<T, 4, ROWS>(gp, psi, l, y, gbuf, stage, s_desc, &s_mbar); break;   \
+        default: gather_group<T, 0, ROWS>(gp, psi, l, y, gbuf, stage, s_desc, &s_mbar); break;  \
     }
+    if (gp.grows == 4) {
+        FEWHA_GATHER_KM(4)
+    } else if (gp.grows == 8) {
+        FEWHA_GATHER_KM(8)
+    } else {
+        FEWHA_GATHER_KM(16)
+    }
+#undef FEWHA_GATHER_KM
     stamp(gp, 2);
 }
 

@@ -18,8 +18,7 @@ constexpr int kMaxL = 16;
 constexpr int kMaxW = 16;
 constexpr int kMaxM = 16;
 constexpr int kMaxC = 8;  // CTAs per layer cluster (portable cluster size)
-constexpr int kGatherRows = 4;  // layer rows per CTA of the adjoint-propagation gather
-constexpr int kMaxGU = 32;      // row groups per layer (max side 128 / kGatherRows)
+constexpr int kMaxGU = 32;      // row groups per layer (max side 128 / the smallest row group, 4)
 constexpr int kMaxWtCode = 1024;  // WFS tiles with a constant-bank position code
 
 // Fused-PCG carry (pcg.hpp:32-38 PcgScalars plus per-frame bookkeeping).
@@ -66,6 +65,7 @@ struct GeoParams {
     // v2 cluster path
     int ccl;          // CTAs per layer cluster
     int ctail;        // tail size D of distributed layers (clayout.hpp)
+    int grows;        // layer rows per CTA of the adjoint gather (4: latency, 8/16: batches)
     int inv_staged;   // inverse kernel: operands staged in shared memory by TMA (1) or read from global (0)
     int gather_km;    // max gather taps per layer row/column
     int o_bs;         // [((w*L+l)*kMaxGU + u)*4] psi source block {ilo, ihi, jlo, jhi} of each gather row group
