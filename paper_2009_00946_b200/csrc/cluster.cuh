@@ -600,30 +600,36 @@ __device__ void gather_group(const GeoParams& gp, const T* __restrict__ psi_b, i
         mbar_wait(mbar, static_cast<unsigned>(k & 1));
         stamp(gp, 1);
         const int t0 = desc[w0].toff;
-        // ---- rows: G_w(i, c) for every WFS of the chunk, one pass ----
-        for (int w = w0; w < w1; ++w) {
-            const GDesc d = desc[w];
-            const int nr = d.ihi - d.ilo, np = gp.ns[w] + 1, nc = d.jhi - d.jlo;
-            if (nr <= 0) continue;
-            const unsigned char* tp = stage + (d.toff - t0);
-            const unsigned shift = static_cast<unsigned>(reinterpret_cast<uintptr_t>(psi_b + d.src) & 15u);
-            const T* __restrict__ blk = reinterpret_cast<const T*>(stage + d.soff + shift) + d.jlo;  // blk[r*np + c]
-            const short* __restrict__ rs = reinterpret_cast<const short*>(tp);
-            const T* __restrict__ rw = reinterpret_cast<const T*>(tp + o_rw);
-            T* __restrict__ G = gbuf + (w - w0) * gst;
-            const int lc = 32 - __clz(nc - 1);  // columns padded to a power of two per row
-            const int cp = 1 << lc;
-            for (int e = tid; e < R << lc; e += nthr) {
-                const int i = e >> lc, c = e & (cp - 1);
-                if (c >= nc) continue;
-                T g = T(0);
-                if constexpr (KM > 0) {
+        // ---- rows: G_w(i, c) for every WFS of the chunk, one pass.  Thread =
+        // (WFS group, column): a column's R rows share the thread's index math and
+        // the row taps are warp-uniform (broadcast) loads ----
+        {
+            constexpr int CL = 128;  // columns per thread group
+            const int ng = nthr / CL > 0 ? nthr / CL : 1, gq = tid / CL, lane = tid % CL;
+            for (int w = w0 + gq; w < w1; w += ng) {
+                const GDesc d = desc[w];
+                const int nr = d.ihi - d.ilo, np = gp.ns[w] + 1, nc = d.jhi - d.jlo;
+                if (nr <= 0) continue;
+                const unsigned char* tp = stage + (d.toff - t0);
+                const unsigned shift = static_cast<unsigned>(reinterpret_cast<uintptr_t>(psi_b + d.src) & 15u);
+                const T* __restrict__ blk = reinterpret_cast<const T*>(stage + d.soff + shift) + d.jlo;  // blk[r*np + c]
+                const short* __restrict__ rs = reinterpret_cast<const short*>(tp);
+                const T* __restrict__ rw = reinterpret_cast<const T*>(tp + o_rw);
+                T* __restrict__ G = gbuf + (w - w0) * gst;
+                for (int c = lane; c < nc; c += CL) {
 #pragma unroll
-                    for (int q = 0; q < KM; ++q) g += rw[i * KM + q] * blk[rs[i * KM + q] * np + c];
-                } else {  // dense aperture sampling of a coarse layer: runtime tap count
-                    for (int q = 0; q < km; ++q) g += rw[i * km + q] * blk[rs[i * km + q] * np + c];
+                    for (int i = 0; i < ROWS; ++i) {
+                        if (i >= R) break;
+                        T g = T(0);
+                        if constexpr (KM > 0) {
+#pragma unroll
+                            for (int q = 0; q < KM; ++q) g += rw[i * KM + q] * blk[rs[i * KM + q] * np + c];
+                        } else {  // dense aperture sampling of a coarse layer: runtime tap count
+                            for (int q = 0; q < km; ++q) g += rw[i * km + q] * blk[rs[i * km + q] * np + c];
+                        }
+                        G[i * nc + c] = g;
+                    }
                 }
-                G[i * nc + c] = g;
             }
         }
         __syncthreads();
@@ -734,10 +740,8 @@ __global__ void __launch_bounds__(256, 2) k_gather(const GeoParams gp, const Buf
     }
     if (gp.grows == 4) {
         FEWHA_GATHER_KM(4)
-    } else if (gp.grows == 8) {
-        FEWHA_GATHER_KM(8)
     } else {
-        FEWHA_GATHER_KM(16)
+        FEWHA_GATHER_KM(8)
     }
 #undef FEWHA_GATHER_KM
     stamp(gp, 2);

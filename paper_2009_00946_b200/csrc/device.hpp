@@ -65,7 +65,7 @@ struct GeoParams {
     // v2 cluster path
     int ccl;          // CTAs per layer cluster
     int ctail;        // tail size D of distributed layers (clayout.hpp)
-    int grows;        // layer rows per CTA of the adjoint gather (4: latency, 8/16: batches)
+    int grows;        // layer rows per CTA of the adjoint gather (4: latency, 8: batches)
     int inv_staged;   // inverse kernel: operands staged in shared memory by TMA (1) or read from global (0)
     int gather_km;    // max gather taps per layer row/column
     int o_bs;         // [((w*L+l)*kMaxGU + u)*4] psi source block {ilo, ihi, jlo, jhi} of each gather row group

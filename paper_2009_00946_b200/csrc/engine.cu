@@ -403,7 +403,7 @@ Plan build_plan(const Geometry& g, int elem_bytes, int batch, int wa = 0, int wb
         gp.grows = batch <= 2 ? 4 : 8;
         if (const char* v = std::getenv("FEWHA_GATHER_ROWS")) {
             const int r = std::atoi(v);
-            if (r == 4 || r == 8 || r == 16) gp.grows = r;
+            if (r == 4 || r == 8) gp.grows = r;
         }
         auto grp_rows = [&](int side) { return std::min(gp.grows, side); };
         gp.o_bs = static_cast<int>(pl.ti.size());
