@@ -698,7 +698,6 @@ __global__ void __launch_bounds__(256, 2) k_gather(const GeoParams gp, const Buf
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ GDesc s_desc[kMaxW];
     __shared__ unsigned long long s_mbar;
-    pdl_launch_dependents();  // the forward kernel's prologue may start (it waits before reading y)
     const int u = blockIdx.x, l = blockIdx.y, b = blockIdx.z;
     const int side = gp.side[l];
     const int R = side < gp.grows ? side : gp.grows;
@@ -722,6 +721,7 @@ __global__ void __launch_bounds__(256, 2) k_gather(const GeoParams gp, const Buf
         gather_issue<T>(gp, psi, s_desc, gp.gchunk[0], gp.gchunk[1], stage, &s_mbar, true, false);
     }
     pdl_wait();  // psi of the predecessor is complete
+    pdl_launch_dependents();  // (after the wait: see the protocol in kernels.cuh)
     if (tid < 32) {
         gather_issue<T>(gp, psi, s_desc, gp.gchunk[0], gp.gchunk[1], stage, &s_mbar, false, true);
         __syncwarp();
@@ -812,11 +812,22 @@ __device__ __forceinline__ void inv_phase(const GeoParams& gp, const Bufs<T>& bf
     }
     __syncthreads();
     if (staged) prefetch_block(bf.jinv + gp.coff[l] + roff, sj, mode == kPlain ? 0 : cnt, &s_mbar, 0);  // constant
+    // Before the wait (kernels.cuh protocol): r, c, p, q were last written by the
+    // previous inverse (three launches back) or the previous frame -- except r at
+    // it = 0, which the RHS forward kernel (the predecessor) updates.
+    const bool r_early = mode == kFit || (mode == kPcg && it > 0);
+    if (staged && mode != kPlain) {
+        if (r_early) prefetch_block(bf.r + vbase, sr, cnt, &s_mbar, 0);
+        prefetch_block(bf.c + vbase, sc, cnt, &s_mbar, 0);
+        if (may_update) {
+            prefetch_block(bf.p + vbase, sp, cnt, &s_mbar, 0);
+            prefetch_block(bf.q + vbase, sq, cnt, &s_mbar, 0);
+        }
+    }
     Carry cin{};
     const int ci = b * (gp.iters + 1) + upd - 1;
-    // nothing the frame writes may be read before this point: with programmatic launch
-    // every kernel of the chain can be resident before its predecessors finish
-    pdl_wait();  // the predecessor's outputs (r, c, p, q, Mz, dot partials, carry) are complete
+    pdl_wait();  // the predecessor's outputs (Mz, mu partials; r at it = 0) are complete
+    pdl_launch_dependents();
     if (may_update && tid == 0) cin = bf.carry[ci];
     // thread 0 issues every block and arrives at once (misaligned blocks: cooperative copies)
     if (!staged) {
@@ -830,13 +841,8 @@ __device__ __forceinline__ void inv_phase(const GeoParams& gp, const Bufs<T>& bf
     } else if (mode == kPlain) {
         prefetch_block(bf.in + vbase, sr, cnt, &s_mbar, 0);
     } else {
-        prefetch_block(bf.r + vbase, sr, cnt, &s_mbar, 0);
-        prefetch_block(bf.c + vbase, sc, cnt, &s_mbar, 0);
-        if (may_update) {
-            prefetch_block(bf.p + vbase, sp, cnt, &s_mbar, 0);
-            prefetch_block(bf.q + vbase, sq, cnt, &s_mbar, 0);
-            prefetch_block(bf.mz + vbase, sm_, cnt, &s_mbar, 0);
-        }
+        if (!r_early) prefetch_block(bf.r + vbase, sr, cnt, &s_mbar, 0);
+        if (may_update) prefetch_block(bf.mz + vbase, sm_, cnt, &s_mbar, 0);
     }
     if (tid == 0) mbar_arrive(&s_mbar);
     if (mode != kPlain && tid < 32) {
@@ -958,7 +964,6 @@ template <typename T, int FLEN>
 __global__ void __launch_bounds__(256) k_inv_cluster(const GeoParams gp, const Bufs<T> bf, int mode, int it) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cg::cluster_group cl = cg::this_cluster();
-    pdl_launch_dependents();
     inv_phase<T, FLEN>(gp, bf, mode, it, smem_raw, blockIdx.y, blockIdx.z, static_cast<int>(cl.block_rank()),
                        static_cast<int>(cl.num_blocks()));
     stamp(gp, 11);
@@ -1013,12 +1018,9 @@ __device__ __forceinline__ void fwd_phase(const GeoParams& gp, const Bufs<T>& bf
     }
     __syncthreads();
     if (mode == kPcg) prefetch_block(bf.jinv + gp.coff[l] + roff, e1, cnt, &s_mbar[0], 0);  // constant
-    pdl_wait();  // y / r / b of the predecessor kernels are complete
-    // the band of y (one bulk copy into x1's space, then into the odd-pitch x0); thread 0
-    // issues every block and arrives at once (misaligned blocks: cooperative copies)
-    prefetch_block(bf.y + lbase + static_cast<size_t>(r0) * S, x1, R * S, &s_mbar[1], 0);
-    if (tid == 0) mbar_arrive(&s_mbar[1]);
-    // epilogue operands (this rank's blocks), requested now, consumed after the transform
+    // epilogue operands (this rank's blocks), requested before the wait (kernels.cuh
+    // protocol: r / b / the operator input were written three or more launches back or
+    // before the frame), consumed after the transform
     if (mode == kApply) {
         prefetch_block(bf.in + vbase, e0, cnt, &s_mbar[0], 0);
     } else if (mode == kPcg) {
@@ -1028,6 +1030,12 @@ __device__ __forceinline__ void fwd_phase(const GeoParams& gp, const Bufs<T>& bf
         prefetch_block(bf.b + vbase, e1, cnt, &s_mbar[0], 0);
     }
     if (tid == 0) mbar_arrive(&s_mbar[0]);
+    pdl_wait();  // y of the predecessor (the gather) is complete
+    pdl_launch_dependents();
+    // the band of y (one bulk copy into x1's space, then into the odd-pitch x0); thread 0
+    // issues every block and arrives at once (misaligned blocks: cooperative copies)
+    prefetch_block(bf.y + lbase + static_cast<size_t>(r0) * S, x1, R * S, &s_mbar[1], 0);
+    if (tid == 0) mbar_arrive(&s_mbar[1]);
     if (tid >= 64 && tid < 64 + 16) s_ad[tid - 64] = my_ad;
     __syncthreads();  // s_ad, cooperative copies
     mbar_wait(&s_mbar[1], 0);
@@ -1075,7 +1083,6 @@ __global__ void __launch_bounds__(256) k_fwd_cluster(const GeoParams gp, const B
                                                       int fit_term) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cg::cluster_group cl = cg::this_cluster();
-    pdl_launch_dependents();
     fwd_phase<T, FLEN>(gp, bf, mode, it, fit_term, smem_raw, blockIdx.y, blockIdx.z, static_cast<int>(cl.block_rank()),
                        static_cast<int>(cl.num_blocks()));
     stamp(gp, 11);

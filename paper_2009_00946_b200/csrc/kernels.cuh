@@ -111,6 +111,12 @@ struct Bulk {
 // waits for its predecessor's results only where it first reads them
 // (griddepcontrol.wait): launch latency and constant-table prefetches overlap
 // the previous kernel's tail.  Both are no-ops for non-programmatic launches.
+// Programmatic dependent launch protocol of the frame: every kernel triggers its
+// dependents only AFTER its own griddepcontrol.wait.  A kernel's pre-wait prologue
+// therefore runs while its predecessor (N-1) may still execute, but kernel N-2 and
+// everything before it are complete and visible -- so the prologue may read the
+// outputs of N-2 and older (constant tables, and the PCG vectors the previous
+// inverse wrote), never those of N-1.
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 
@@ -321,9 +327,11 @@ __device__ __forceinline__ void wfs_tile(const GeoParams& gp, const Bufs<T>& bf,
         }
         __syncthreads();
         pdl_wait();
+        pdl_launch_dependents();
         mbar_wait(&s_mbar, 0);
     } else {
         pdl_wait();
+        pdl_launch_dependents();
     }
     __syncthreads();
     wstamp(gp, 1);
@@ -414,7 +422,6 @@ __device__ __forceinline__ void wfs_tile(const GeoParams& gp, const Bufs<T>& bf,
 template <typename T, bool RHS>
 __global__ void __launch_bounds__(512, 2) k_wfs(const GeoParams gp, const Bufs<T> bf, int with_dm) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    pdl_launch_dependents();
     wfs_tile<T, RHS>(gp, bf, with_dm, gp.wt_base + blockIdx.x, blockIdx.y, smem_raw);
 }
 
@@ -472,8 +479,8 @@ __device__ void fit_actuator(const GeoParams& gp, const Bufs<T>& bf, int step, i
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_fit_control(const GeoParams gp, const Bufs<T> bf, int step) {
-    pdl_launch_dependents();
     pdl_wait();
+    pdl_launch_dependents();
     const int b = blockIdx.y;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (step && blockIdx.x == 0 && threadIdx.x == 0) frame_epilogue(gp, bf, b);
