@@ -231,7 +231,10 @@ __device__ __forceinline__ void prefetch_block(const T* src, T* dst, int count, 
 // Forward level s: out(i,j) = sum_t1 F1[t1] sum_t2 F2[t2] x[2m1+t1][2m2+t2]
 // (rows first, as wavelet.hpp:153-168), F = lo for the approximation half.
 // ---------------------------------------------------------------------------
-constexpr int kFusedTail = 8;  // tail levels s <= 8 as fused 2-D passes, larger ones separable
+#ifndef FEWHA_FUSED_TAIL
+#define FEWHA_FUSED_TAIL 16
+#endif
+constexpr int kFusedTail = FEWHA_FUSED_TAIL;  // tail levels s <= this as fused 2-D passes, larger ones separable
 
 template <typename T, int FLEN>
 __device__ void tail_forward(const GeoParams& gp, const T* src, int ps, int Tt, T* b0, T* b1, T* f) {
