@@ -391,6 +391,38 @@ class RefOracle(_Base):
         self._chk(self._lib.ref_record(self.h, seed, k0, frames, _ptr(meas), _ptr(c), _ptr(a), _ptr(rho), _ptr(us)))
         return meas, c, a, rho, us
 
+    def truth_at_step(self, seed, k):
+        out = np.zeros(self.dims.n)
+        self._chk(self._lib.ref_truth_at_step(self.h, C.c_ulonglong(seed), C.c_int(k), _ptr(out)))
+        return out
+
+    def quality(self, layers, dm):
+        """evaluate_quality: (field_rms, layer_rel_err, rms_per_dir)."""
+        out = np.zeros(2 + 4096)
+        lay = np.ascontiguousarray(layers, np.float64)
+        a = np.ascontiguousarray(dm, np.float64)
+        self._chk(self._lib.ref_quality(self.h, _ptr(lay), _ptr(a), _ptr(out)))
+        return out[0], out[1], out[2:]
+
+    def run_closed_loop(self, n_steps, atm=1, noise=2, threads=0):
+        d = self.dims
+        fr, le = np.zeros(n_steps), np.zeros(n_steps)
+        rho = np.zeros((n_steps, d.iters))
+        o2 = np.zeros(2)
+        self._chk(self._lib.ref_run_closed_loop(self.h, C.c_int(n_steps), C.c_ulonglong(atm), C.c_ulonglong(noise),
+                                                C.c_int(threads), _ptr(fr), _ptr(le), _ptr(rho), _ptr(o2)))
+        return {"field_rms": fr, "layer_rel_err": le, "rho": rho, "uncorrected_field_rms": o2[0],
+                "final_field_rms": o2[1]}
+
+    @staticmethod
+    def gauss(seed, count):
+        lib = C.CDLL(REF_SO)
+        out = np.zeros(count)
+        rc = lib.ref_gauss(C.c_ulonglong(seed), C.c_int(count), _ptr(out))
+        if rc:
+            raise OracleError(rc, lib.ref_last_error().decode())
+        return out
+
     def time_steps(self, meas_stream, frames):
         ms = np.ascontiguousarray(meas_stream, np.float64).reshape(-1, self.dims.S)
         us = np.zeros(frames)

@@ -15,6 +15,8 @@
 //   apply_M / build_rhs    reconstructor.hpp:166 / :215
 //   add_dm_slopes / fit    reconstructor.hpp:259 / :284
 //   synthesize_measurements, generate_atmosphere  simulation.hpp:164 / :76
+//   GaussianStream, truth_at_step, evaluate_quality, run_closed_loop
+//                          simulation.hpp:40 / :131 / :228 / :321
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -402,6 +404,67 @@ int ref_time_steps(void* hp, const double* meas_stream, int stream_len, int fram
             const auto t1 = std::chrono::steady_clock::now();
             us_out[f] = std::chrono::duration<double, std::micro>(t1 - t0).count();
         }
+    });
+}
+
+// Gaussian stream of the simulation (simulation.hpp:40-58): the first `count`
+// draws of GaussianStream(seed).
+int ref_gauss(unsigned long long seed, int count, double* out) {
+    return guarded([&] {
+        GaussianStream g(seed);
+        for (int i = 0; i < count; ++i) out[i] = g();
+    });
+}
+
+// truth_at_step(generate_atmosphere(seed), k) (simulation.hpp:131-158), nodal [n].
+int ref_truth_at_step(void* hp, unsigned long long seed, int k, double* layers_out) {
+    auto* h = static_cast<RefHandle*>(hp);
+    return guarded([&] {
+        for (const auto& l : truth_at_step(truth_for(h, seed), h->g, k)) {
+            std::memcpy(layers_out, l.data(), l.size() * sizeof(double));
+            layers_out += l.size();
+        }
+    });
+}
+
+// evaluate_quality(layers, correction, g) (simulation.hpp:228-305): out =
+// [field_rms, layer_rel_err, rms_per_dir...].
+int ref_quality(void* hp, const double* layers, const double* dm_flat, double* out) {
+    auto* h = static_cast<RefHandle*>(hp);
+    return guarded([&] {
+        std::vector<Grid2D> lay;
+        for (const auto& lc : h->g.layers) {
+            Grid2D gl(lc.n_nodes(), lc.n_nodes());
+            std::memcpy(gl.data(), layers, gl.size() * sizeof(double));
+            layers += gl.size();
+            lay.push_back(std::move(gl));
+        }
+        MirrorShapes corr = MirrorShapes::zero(h->g);
+        flat_to_mirrors(dm_flat, corr);
+        const QualityRecord q = evaluate_quality(lay, corr, h->g);
+        out[0] = q.field_rms;
+        out[1] = q.layer_rel_err;
+        for (std::size_t d = 0; d < q.rms_per_dir.size(); ++d) out[2 + d] = q.rms_per_dir[d];
+    });
+}
+
+// run_closed_loop(g, n_steps, {atm, noise}, threads) (simulation.hpp:321-345):
+// per step field_rms, layer_rel_err, rho [iters] (0-padded); scalars out2 =
+// [uncorrected_field_rms, final_field_rms].
+int ref_run_closed_loop(void* hp, int n_steps, unsigned long long atm, unsigned long long noise, int threads,
+                        double* field_rms, double* layer_err, double* rho, double* out2) {
+    auto* h = static_cast<RefHandle*>(hp);
+    const int it = h->g.solver.pcg_max_iter;
+    return guarded([&] {
+        const LoopResult r = run_closed_loop(h->g, n_steps, LoopSeeds{atm, noise}, threads);
+        for (int k = 0; k < n_steps; ++k) {
+            const auto& q = r.records[static_cast<std::size_t>(k)];
+            field_rms[k] = q.field_rms;
+            layer_err[k] = q.layer_rel_err;
+            for (int i = 0; i < it; ++i) rho[k * it + i] = i < static_cast<int>(q.rho.size()) ? q.rho[i] : 0.0;
+        }
+        out2[0] = r.uncorrected_field_rms;
+        out2[1] = r.final_field_rms;
     });
 }
 
