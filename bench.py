@@ -92,6 +92,10 @@ def kernel_bytes(kind, d, b):
         "fwd_pcg": b * (3 * n + n),               # y, r, J -> Mz
         "inv_fit": b * (6 * n + 4 * n + n),       # last update + c -> phi
         "fit_control": b * (n + 5 * A),           # phi, a_prev, a_prev2 -> a_prev2, a_prev, a_out
+        # fused forward + inverse (k_fwd_inv_cluster): Mz / the RHS pass no longer cross memory
+        "fwd_rhs_inv0": b * (4 * n + 3 * n),      # y, r, b, J -> r, b, phi
+        "fwd_inv_pcg": b * (6 * n + 5 * n),       # y, r, J, p, q, c -> p, q, c, r, phi
+        "fwd_inv_fit": b * (6 * n + 5 * n),       # y, r, J, p, q, c -> p, q, c, r, phi
     }[kind]
 
 

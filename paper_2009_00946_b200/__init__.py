@@ -425,7 +425,8 @@ class Reconstructor:
             self._chk(-n)
         return out.reshape(32, 4096, 16)
 
-    KERNEL_KINDS = ("wfs_rhs", "adjoint", "fwd_rhs", "inv_pcg0", "inv_pcg", "wfs", "fwd_pcg", "inv_fit", "fit_control", "gather")
+    KERNEL_KINDS = ("wfs_rhs", "adjoint", "fwd_rhs", "inv_pcg0", "inv_pcg", "wfs", "fwd_pcg", "inv_fit", "fit_control", "gather",
+                    "fwd_rhs_inv0", "fwd_inv_pcg", "fwd_inv_fit")
 
     def profile_step(self):
         """One eager frame with events between launches: [(kind, ms), ...]."""

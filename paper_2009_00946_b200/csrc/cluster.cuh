@@ -1091,4 +1091,51 @@ __global__ void __launch_bounds__(256) k_fwd_cluster(const GeoParams gp, const B
     stamp(gp, 11);
 }
 
+// ---------------------------------------------------------------------------
+// Barrier over the L x C CTAs of one instance (the fused kernel below; the
+// cooperative launch makes them co-resident).  ctr: the instance's monotonic
+// arrival counter, never reset -- arrival k of the e-th barrier on it reads
+// old in [e n, (e+1) n), so the target needs no per-launch state.  Release /
+// acquire at GPU scope order every CTA's global writes (Mz, r, b, mu partials)
+// before the other CTAs' reads; the proxy fences let the inverse phase's TMA
+// bulk copies read them and overwrite shared memory the forward phase used.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void instance_barrier(unsigned long long* ctr, unsigned long long n) {
+    asm volatile("fence.proxy.async.global;\n" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        unsigned long long old, v;
+        asm volatile("atom.add.release.gpu.global.u64 %0, [%1], 1;\n" : "=l"(old) : "l"(ctr) : "memory");
+        const unsigned long long target = (old / n + 1) * n;
+        do {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(ctr) : "memory");
+        } while (v < target);
+        asm volatile("fence.proxy.async.global;\n" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    }
+    __syncthreads();
+}
+
+// Fused forward(k) + inverse(k+1): the W of one apply_M (or of the RHS) and the
+// next W^-1 with the PCG update between them in one launch.  The scalar
+// recurrence needs the global mu = (s, z) of the forward epilogue, so the two
+// phases meet at one barrier over the instance's L x C CTAs instead of a
+// kernel boundary (grid (C, L, B), cluster (C,1,1), cooperative).  Shared
+// memory is the union of the two phases' maps; the forward phase ends after
+// its last cluster barrier, so no rank reads a peer's forward buffers once
+// the instance barrier is passed.
+template <typename T, int FLEN>
+__global__ void __launch_bounds__(256) k_fwd_inv_cluster(const GeoParams gp, const Bufs<T> bf, int fmode, int fit,
+                                                          int imode, int iit, int fit_term,
+                                                          unsigned long long* bar) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cg::cluster_group cl = cg::this_cluster();
+    const int q = static_cast<int>(cl.block_rank()), C = static_cast<int>(cl.num_blocks());
+    fwd_phase<T, FLEN>(gp, bf, fmode, fit, fit_term, smem_raw, blockIdx.y, blockIdx.z, q, C);
+    instance_barrier(bar + blockIdx.z, static_cast<unsigned long long>(gp.L) * C);
+    inv_phase<T, FLEN>(gp, bf, imode, iit, smem_raw, blockIdx.y, blockIdx.z, q, C);
+    stamp(gp, 11);
+}
+
 }  // namespace fewha_gpu

@@ -100,6 +100,10 @@ enum KernelKind : int {
     kKindInvFit = 7,   // k_layer_inverse kFit: last update + W^-1 c
     kKindFit = 8,      // k_fit_control
     kKindGather = 9,   // k_gather: y = sum_w P^T psi_w
+    // k_fwd_inv_cluster (fused forward + inverse, single-instance latency plans)
+    kKindFwdRhsInv0 = 10,  // kRhs forward + kPcg it=0 inverse
+    kKindFwdInvPcg = 11,   // kPcg forward (it k) + kPcg inverse (it k+1)
+    kKindFwdInvFit = 12,   // kPcg forward (last it) + kFit inverse
 };
 
 template <typename T>

@@ -776,8 +776,10 @@ struct Launch {
             CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(m - fa.sharedSizeBytes)));
         };
-        opt_in(k_wfs<T, false>, wfs_smem(gp));
-        opt_in(k_wfs<T, true>, wfs_smem(gp));
+        opt_in(k_wfs<T, false, FEWHA_WFS_MINB_LAT>, wfs_smem(gp));
+        opt_in(k_wfs<T, true, FEWHA_WFS_MINB_LAT>, wfs_smem(gp));
+        opt_in(k_wfs<T, false, FEWHA_WFS_MINB_BATCH>, wfs_smem(gp));
+        opt_in(k_wfs<T, true, FEWHA_WFS_MINB_BATCH>, wfs_smem(gp));
         opt_in(k_gather<T>, gather_smem(gp));
     }
     // layer kernels: grid (C, L, count), cluster (C,1,1)
@@ -789,6 +791,30 @@ struct Launch {
 #define FEWHA_LAUNCH(N) CK((launch_layer_cluster<T, N>(inverse, g2, bf, mode, it, count, st, fit_term, smem)))
         FEWHA_FLEN_SWITCH(flen, FEWHA_LAUNCH)
 #undef FEWHA_LAUNCH
+    }
+    // fused forward (fmode, fit) + inverse (imode, iit): one cooperative cluster launch
+    static void fused(int flen, const GeoParams& gp, const Bufs<T>& bf, int fmode, int fit, int imode, int iit,
+                      int count, cudaStream_t st, unsigned long long* bar) {
+        GeoParams g2 = gp;
+        g2.inv_staged = inv_staged_for(count);
+        const size_t smem = fused_cl_smem(g2, flen, g2.inv_staged);
+#define FEWHA_LAUNCH(N) \
+    CK((launch_fused_cluster<T, N>(g2, bf, fmode, fit, imode, iit, count, st, 1, smem, bar, pdl_enabled() ? 1 : 0)))
+        FEWHA_FLEN_SWITCH(flen, FEWHA_LAUNCH)
+#undef FEWHA_LAUNCH
+    }
+    static size_t fused_cl_smem(const GeoParams& gp, int flen, int staged) {
+        return std::max(inv_cl_smem(gp, flen, staged), fwd_cl_smem(gp, flen));
+    }
+    // clusters of the fused kernel resident at once (0: it does not fit)
+    static int fused_capacity(const GeoParams& gp, int flen, int count) {
+        GeoParams g2 = gp;
+        g2.inv_staged = inv_staged_for(count);
+        int clusters = 0;
+#define FEWHA_CAP(N) CK((fused_cluster_capacity<T, N>(g2, fused_cl_smem(g2, flen, g2.inv_staged), &clusters)))
+        FEWHA_FLEN_SWITCH(flen, FEWHA_CAP)
+#undef FEWHA_CAP
+        return clusters;
     }
     // programmatic dependent launch config (the kernels call griddepcontrol)
     static cudaLaunchConfig_t pdl_cfg(dim3 grid, size_t smem, cudaStream_t st, cudaLaunchAttribute* attr,
@@ -806,9 +832,15 @@ struct Launch {
     }
     static void wfs(bool rhs, const GeoParams& gp, const Bufs<T>& bf, int with_dm, int count, cudaStream_t st) {
         cudaLaunchAttribute attr[1];
-        cudaLaunchConfig_t cfg = pdl_cfg(dim3(gp.wt_count, count), wfs_smem(gp), st, attr, 512);
-        if (rhs) CK(cudaLaunchKernelEx(&cfg, k_wfs<T, true>, gp, bf, with_dm));
-        else CK(cudaLaunchKernelEx(&cfg, k_wfs<T, false>, gp, bf, with_dm));
+        cudaLaunchConfig_t cfg = pdl_cfg(dim3(gp.wt_count, count), wfs_smem(gp), st, attr, kWfsThreads);
+        constexpr int LAT = FEWHA_WFS_MINB_LAT, BAT = FEWHA_WFS_MINB_BATCH;
+        if (count <= 2) {
+            if (rhs) CK(cudaLaunchKernelEx(&cfg, k_wfs<T, true, LAT>, gp, bf, with_dm));
+            else CK(cudaLaunchKernelEx(&cfg, k_wfs<T, false, LAT>, gp, bf, with_dm));
+        } else {
+            if (rhs) CK(cudaLaunchKernelEx(&cfg, k_wfs<T, true, BAT>, gp, bf, with_dm));
+            else CK(cudaLaunchKernelEx(&cfg, k_wfs<T, false, BAT>, gp, bf, with_dm));
+        }
     }
     // y = sum_w P^T psi_w: one CTA per gp.grows rows of every layer
     static void gather(const GeoParams& gp, const Bufs<T>& bf, int count, cudaStream_t st) {
@@ -850,6 +882,12 @@ struct EngineImpl {
     bool own_stream = false;
     cudaGraphExec_t graph = nullptr;
     bool has_precond = false;
+    // fused forward + inverse launches (k_fwd_inv_cluster): opt-in (FEWHA_FUSE=1) when
+    // every instance's L clusters fit the device at once; per-instance
+    // monotonic barrier counters
+    bool fuse_ok = false;
+    unsigned long long* fbar = nullptr;
+    bool fused_frame() const { return fuse_ok && !telemetry_on && !(sharded && !comm); }
     // optional per-phase timestamps of the cluster kernels (profiling only)
     unsigned long long* stamp_buf = nullptr;
     int stamp_slot = -1;  // < 0: stamping off
@@ -944,6 +982,22 @@ struct EngineImpl {
             Launch<T>::wfs(true, gps(), bf, gp.closed, B, st);
             mark(kKindWfsRhs);
             gather();
+            return;
+        }
+        if (fused_frame()) {  // W of the previous gather and the next W^-1 in one launch
+            const int fmode = seg == 1 ? kRhs : kPcg, fit = seg == 1 ? 0 : seg - 2;
+            if (seg <= it) {
+                Launch<T>::fused(flen, gps(), bf, fmode, fit, kPcg, seg - 1, B, st, fbar);
+                mark(seg == 1 ? kKindFwdRhsInv0 : kKindFwdInvPcg);
+                Launch<T>::wfs(false, gps(), bf, 0, B, st);
+                mark(kKindWfs);
+                gather();
+                return;
+            }
+            Launch<T>::fused(flen, gps(), bf, fmode, fit, kFit, 0, B, st, fbar);
+            mark(kKindFwdInvFit);
+            Launch<T>::fit(gpf, bf, 1, B, st);
+            mark(kKindFit);
             return;
         }
         // W of the previous gather: the RHS (r += b1 - b) or PCG iteration seg-2
@@ -1264,6 +1318,18 @@ Engine::Engine(Geometry g, int precision, int batch, int device) : p_(std::make_
     Launch<double>::set_attrs(P.gp64, P.flen);  // probes always fp64
     P.fr.add(P.jac);
     P.fr.add(P.jinv);
+    {
+        // opt-in (FEWHA_FUSE=1): measured slower than the split launches
+        const char* fz = std::getenv("FEWHA_FUSE");
+        if (fz && fz[0] == '1') {
+            const int cap = precision == 64 ? Launch<double>::fused_capacity(P.gp, P.flen, batch)
+                                            : Launch<float>::fused_capacity(P.gp, P.flen, batch);
+            P.fuse_ok = cap >= P.gp.L * batch;
+        }
+        P.fbar = dalloc<unsigned long long>(static_cast<size_t>(batch));
+        P.fr.add(P.fbar);
+        CK(cudaMemset(P.fbar, 0, sizeof(unsigned long long) * static_cast<size_t>(batch)));
+    }
     reset();
 }
 
@@ -1637,7 +1703,10 @@ void Engine::sync_check() {
         if (s) throw std::runtime_error("pcg_solve: non-finite scalar (indefinite operator?)");
 }
 
-int Engine::launches_per_step() const { return 5 + 4 * p_->gp.iters; }
+int Engine::launches_per_step() const {
+    const int it = p_->gp.iters;
+    return p_->fused_frame() ? 4 + 3 * it : 5 + 4 * it;
+}
 
 int Engine::profile_step(float* ms, int* kinds, int max) {
     auto& P = *p_;

@@ -267,7 +267,25 @@ __device__ __forceinline__ void wstamp(const GeoParams& gp, int k) {
     gp.stamps[blk * 16 + k] = t;
 }
 
-constexpr int kWfsTile = 16;  // WFS node tile side (compile-time: index math by constants)
+// WFS tiles: 14 x 14 nodes, (14+2)^2 = 256 wavefront nodes = one per thread of a
+// 256-thread CTA in the dominant phase (16 x 16 tiles on 512 threads left 37 % of
+// the warps waiting at the barrier).  Resident CTAs per SM: 3 for single-instance
+// plans (80 registers, no spills on the latency path), 4 for batches (64 registers,
+// more tiles in flight): measured in DESIGN.md.
+#ifndef FEWHA_WFS_TILE
+#define FEWHA_WFS_TILE 14
+#endif
+#ifndef FEWHA_WFS_THREADS
+#define FEWHA_WFS_THREADS 256
+#endif
+#ifndef FEWHA_WFS_MINB_LAT
+#define FEWHA_WFS_MINB_LAT 3
+#endif
+#ifndef FEWHA_WFS_MINB_BATCH
+#define FEWHA_WFS_MINB_BATCH 4
+#endif
+constexpr int kWfsTile = FEWHA_WFS_TILE;  // WFS node tile side (compile-time: index math by constants)
+constexpr int kWfsThreads = FEWHA_WFS_THREADS;  // threads per WFS tile CTA
 
 // Shared memory of one WFS tile: stencil tables of the tile's halo rows and
 // columns for every screen, then the wavefront, then the two slope grids.
@@ -419,8 +437,8 @@ __device__ __forceinline__ void wfs_tile(const GeoParams& gp, const Bufs<T>& bf,
     wstamp(gp, 4);
 }
 
-template <typename T, bool RHS>
-__global__ void __launch_bounds__(512, 2) k_wfs(const GeoParams gp, const Bufs<T> bf, int with_dm) {
+template <typename T, bool RHS, int MINB>
+__global__ void __launch_bounds__(kWfsThreads, MINB) k_wfs(const GeoParams gp, const Bufs<T> bf, int with_dm) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     wfs_tile<T, RHS>(gp, bf, with_dm, gp.wt_base + blockIdx.x, blockIdx.y, smem_raw);
 }

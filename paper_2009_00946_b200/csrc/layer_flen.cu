@@ -32,6 +32,48 @@ cudaError_t launch_layer_cluster(bool inverse, const GeoParams& gp, const Bufs<T
     return cudaLaunchKernelEx(&cfg, k_fwd_cluster<T, FLEN>, gp, bf, mode, it, fit_term);
 }
 
+// Fused forward + inverse (k_fwd_inv_cluster): the cluster grid launched
+// cooperatively so the instance barrier's CTAs are co-resident.
+template <typename T, int FLEN>
+cudaError_t launch_fused_cluster(const GeoParams& gp, const Bufs<T>& bf, int fmode, int fit, int imode, int iit,
+                                 int count, cudaStream_t st, int fit_term, size_t smem, unsigned long long* bar,
+                                 int pdl) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(gp.ccl, gp.L, count);
+    cfg.blockDim = dim3(256, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[3];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = gp.ccl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeCooperative;
+    attr[1].val.cooperative = 1;
+    attr[2].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[2].val.programmaticStreamSerializationAllowed = pdl;
+    cfg.attrs = attr;
+    cfg.numAttrs = 3;
+    return cudaLaunchKernelEx(&cfg, k_fwd_inv_cluster<T, FLEN>, gp, bf, fmode, fit, imode, iit, fit_term, bar);
+}
+
+// Clusters of the fused kernel that fit the device at once with `smem` bytes.
+template <typename T, int FLEN>
+cudaError_t fused_cluster_capacity(const GeoParams& gp, size_t smem, int* clusters) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(gp.ccl, gp.L, 1);
+    cfg.blockDim = dim3(256, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = gp.ccl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaOccupancyMaxActiveClusters(clusters, k_fwd_inv_cluster<T, FLEN>, &cfg);
+}
+
 // Opt in to the device maximum minus each kernel's static shared memory.
 template <typename K>
 static cudaError_t opt_in_max(K kernel, size_t maxopt) {
@@ -46,12 +88,18 @@ template <typename T, int FLEN>
 cudaError_t set_layer_cluster_attrs(size_t smem_inv, size_t smem_fwd) {
     cudaError_t e = opt_in_max(k_inv_cluster<T, FLEN>, smem_inv);
     if (e != cudaSuccess) return e;
+    e = opt_in_max(k_fwd_inv_cluster<T, FLEN>, smem_fwd);
+    if (e != cudaSuccess) return e;
     return opt_in_max(k_fwd_cluster<T, FLEN>, smem_fwd);
 }
 
 #define FEWHA_INST(T)                                                                                          \
     template cudaError_t launch_layer_cluster<T, FEWHA_FLEN>(bool, const GeoParams&, const Bufs<T>&, int, int, int, \
                                                              cudaStream_t, int, size_t);                        \
+    template cudaError_t launch_fused_cluster<T, FEWHA_FLEN>(const GeoParams&, const Bufs<T>&, int, int, int, int, \
+                                                             int, cudaStream_t, int, size_t, unsigned long long*, \
+                                                             int);                                              \
+    template cudaError_t fused_cluster_capacity<T, FEWHA_FLEN>(const GeoParams&, size_t, int*);                 \
     template cudaError_t set_layer_cluster_attrs<T, FEWHA_FLEN>(size_t, size_t);
 FEWHA_INST(double)
 FEWHA_INST(float)

@@ -436,3 +436,26 @@ def test_back_to_back_frames_are_race_free():
     sa, sb = ga.get_state(), gb.get_state()
     for key in ("c", "r", "p", "q", "a_prev", "a_prev2"):
         assert np.array_equal(sa[key], sb[key]), key
+
+
+@pytest.mark.parametrize("name", ["small_mcao", "elt_mcao84_3dm"])
+def test_fused_forward_inverse_is_bitwise_the_split_frame(name, precision, monkeypatch):
+    """k_fwd_inv_cluster (forward W, instance barrier, PCG update + W^-1 in one
+    cooperative launch) must reproduce the split forward/inverse launches bit for
+    bit over closed-loop frames, including the carried PCG state."""
+    path = preset(name + ".json")
+    monkeypatch.setenv("FEWHA_FUSE", "1")
+    gf = fg.Reconstructor(path, precision=precision)
+    monkeypatch.setenv("FEWHA_FUSE", "0")
+    gs = fg.Reconstructor(path, precision=precision)
+    it = gf.dims.iters
+    assert gf.launches_per_step() == 4 + 3 * it  # the fused plan is the one running
+    assert gs.launches_per_step() == 5 + 4 * it
+    rng = np.random.default_rng(21)
+    for _ in range(4):
+        s = rng.standard_normal(gf.dims.S) * 0.01
+        assert np.array_equal(gf.step(s), gs.step(s))
+        assert np.array_equal(gf.last_rho, gs.last_rho)
+    sf, ss = gf.get_state(), gs.get_state()
+    for key in ("c", "b", "r", "p", "q", "a_prev", "a_prev2"):
+        assert np.array_equal(sf[key], ss[key]), key
