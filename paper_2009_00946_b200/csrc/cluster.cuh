@@ -573,6 +573,13 @@ __device__ __forceinline__ void gather_issue(const GeoParams& gp, const T* psi_b
     }
 }
 
+// Residency of the gather: 2 CTAs per SM with a 110 KB staging budget each for
+// single-instance plans (fewer, larger WFS chunks: shortest chain), 3 per SM with
+// 72 KB for batches (more row groups in flight: -10 % per launch at B = 64, but
+// +3 % on the single frame).  The host splits the WFS into chunks that fit.
+constexpr int kGatherMinbLat = 2, kGatherSmemKbLat = 110;
+constexpr int kGatherMinbBatch = 3, kGatherSmemKbBatch = 72;
+
 // Contract the staged row group, chunk by chunk (chunk 0 already issued by the caller).
 template <typename T, int KM, int ROWS>
 __device__ void gather_group(const GeoParams& gp, const T* __restrict__ psi_b, int l, T* __restrict__ y, T* gbuf,
@@ -696,8 +703,8 @@ __device__ void gather_group(const GeoParams& gp, const T* __restrict__ psi_b, i
 // grid (side/grows, L, B): one CTA per gp.grows-row group of a layer; y nodal, row-major.
 // Descriptors and chunk 0's tables are requested before the programmatic-launch
 // wait (they are constant), the psi blocks after it.
-template <typename T>
-__global__ void __launch_bounds__(256, 2) k_gather(const GeoParams gp, const Bufs<T> bf) {
+template <typename T, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_gather(const GeoParams gp, const Bufs<T> bf) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ GDesc s_desc[kMaxW];
     __shared__ unsigned long long s_mbar;

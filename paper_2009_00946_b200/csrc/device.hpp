@@ -78,6 +78,7 @@ struct GeoParams {
     int gchunk[kMaxW + 1];
     int o_gd;                   // [((l*kMaxGU + u)*kMaxW + w)*8] gather staging descriptors (int4-aligned)
     int gbuf_bytes;   // the gather's double-buffered row-contracted block (see cluster.cuh)
+    int gather_batch; // k_gather residency plan: 0 single instance (2 CTAs/SM), 1 batches (3 CTAs/SM)
 };
 
 enum LayerMode : int {

@@ -470,7 +470,8 @@ Plan build_plan(const Geometry& g, int elem_bytes, int batch, int wa = 0, int wb
         // row-contracted blocks G of every WFS of a chunk (group rows x psi block columns)
         gp.gbuf_bytes = static_cast<int>(a16(static_cast<size_t>(W) * gp.grows * cmax * elem_bytes));
         const size_t fixed = a16(static_cast<size_t>(gp.gbuf_bytes)) + 1024;  // + static shared memory
-        const size_t limit = 110 * 1024;                                      // two CTAs per SM
+        gp.gather_batch = batch > 2 ? 1 : 0;  // residency plan of k_gather (cluster.cuh)
+        const size_t limit = static_cast<size_t>(gp.gather_batch ? kGatherSmemKbBatch : kGatherSmemKbLat) * 1024;
         const size_t budget = limit > fixed ? limit - fixed : 0;
         gp.nchunk = 0;
         gp.gchunk[0] = wa;
@@ -780,7 +781,8 @@ struct Launch {
         opt_in(k_wfs<T, true, FEWHA_WFS_MINB_LAT>, wfs_smem(gp));
         opt_in(k_wfs<T, false, FEWHA_WFS_MINB_BATCH>, wfs_smem(gp));
         opt_in(k_wfs<T, true, FEWHA_WFS_MINB_BATCH>, wfs_smem(gp));
-        opt_in(k_gather<T>, gather_smem(gp));
+        opt_in(k_gather<T, kGatherMinbLat>, gather_smem(gp));
+        opt_in(k_gather<T, kGatherMinbBatch>, gather_smem(gp));
     }
     // layer kernels: grid (C, L, count), cluster (C,1,1)
     static void cl(int flen, bool inverse, const GeoParams& gp, const Bufs<T>& bf, int mode, int it, int count,
@@ -847,7 +849,8 @@ struct Launch {
         cudaLaunchAttribute attr[1];
         const int groups = gp.maxside / std::min(gp.grows, gp.maxside);
         cudaLaunchConfig_t cfg = pdl_cfg(dim3(groups, gp.L, count), gather_smem(gp), st, attr);
-        CK(cudaLaunchKernelEx(&cfg, k_gather<T>, gp, bf));
+        if (gp.gather_batch) CK(cudaLaunchKernelEx(&cfg, k_gather<T, kGatherMinbBatch>, gp, bf));
+        else CK(cudaLaunchKernelEx(&cfg, k_gather<T, kGatherMinbLat>, gp, bf));
     }
     static void fit(const GeoParams& gp, const Bufs<T>& bf, int step, int count, cudaStream_t st) {
         cudaLaunchAttribute attr[1];
