@@ -235,6 +235,10 @@ __device__ __forceinline__ void prefetch_block(const T* src, T* dst, int count, 
 #define FEWHA_FUSED_TAIL 16
 #endif
 constexpr int kFusedTail = FEWHA_FUSED_TAIL;  // tail levels s <= this as fused 2-D passes, larger ones separable
+#ifndef FEWHA_CL_THREADS
+#define FEWHA_CL_THREADS 256
+#endif
+constexpr int kClThreads = FEWHA_CL_THREADS;  // threads per CTA of the cluster layer kernels
 
 template <typename T, int FLEN>
 __device__ void tail_forward(const GeoParams& gp, const T* src, int ps, int Tt, T* b0, T* b1, T* f) {
@@ -577,8 +581,8 @@ __device__ __forceinline__ void gather_issue(const GeoParams& gp, const T* psi_b
 // single-instance plans (fewer, larger WFS chunks: shortest chain), 3 per SM with
 // 72 KB for batches (more row groups in flight: -10 % per launch at B = 64, but
 // +3 % on the single frame).  The host splits the WFS into chunks that fit.
-constexpr int kGatherMinbLat = 2, kGatherSmemKbLat = 110;
-constexpr int kGatherMinbBatch = 3, kGatherSmemKbBatch = 72;
+// Staging budget per CTA of each residency plan.
+__host__ __device__ constexpr int gather_smem_kb(int minb) { return minb >= 4 ? 54 : minb == 3 ? 72 : 110; }
 
 // Contract the staged row group, chunk by chunk (chunk 0 already issued by the caller).
 template <typename T, int KM, int ROWS>
@@ -748,7 +752,9 @@ __global__ void __launch_bounds__(256, MINB) k_gather(const GeoParams gp, const 
         case 4: gather_group<T, 4, ROWS>(gp, psi, l, y, gbuf, stage, s_desc, &s_mbar); break;   \
         default: gather_group<T, 0, ROWS>(gp, psi, l, y, gbuf, stage, s_desc, &s_mbar); break;  \
     }
-    if (gp.grows == 4) {
+    if (gp.grows == 2) {
+        FEWHA_GATHER_KM(2)
+    } else if (gp.grows == 4) {
         FEWHA_GATHER_KM(4)
     } else {
         FEWHA_GATHER_KM(8)
@@ -971,7 +977,7 @@ __device__ __forceinline__ void inv_phase(const GeoParams& gp, const Bufs<T>& bf
 }
 
 template <typename T, int FLEN>
-__global__ void __launch_bounds__(256) k_inv_cluster(const GeoParams gp, const Bufs<T> bf, int mode, int it) {
+__global__ void __launch_bounds__(kClThreads) k_inv_cluster(const GeoParams gp, const Bufs<T> bf, int mode, int it) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cg::cluster_group cl = cg::this_cluster();
     inv_phase<T, FLEN>(gp, bf, mode, it, smem_raw, blockIdx.y, blockIdx.z, static_cast<int>(cl.block_rank()),
@@ -1089,7 +1095,7 @@ __device__ __forceinline__ void fwd_phase(const GeoParams& gp, const Bufs<T>& bf
 }
 
 template <typename T, int FLEN>
-__global__ void __launch_bounds__(256) k_fwd_cluster(const GeoParams gp, const Bufs<T> bf, int mode, int it,
+__global__ void __launch_bounds__(kClThreads) k_fwd_cluster(const GeoParams gp, const Bufs<T> bf, int mode, int it,
                                                       int fit_term) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cg::cluster_group cl = cg::this_cluster();
@@ -1133,7 +1139,7 @@ __device__ __forceinline__ void instance_barrier(unsigned long long* ctr, unsign
 // its last cluster barrier, so no rank reads a peer's forward buffers once
 // the instance barrier is passed.
 template <typename T, int FLEN>
-__global__ void __launch_bounds__(256) k_fwd_inv_cluster(const GeoParams gp, const Bufs<T> bf, int fmode, int fit,
+__global__ void __launch_bounds__(kClThreads) k_fwd_inv_cluster(const GeoParams gp, const Bufs<T> bf, int fmode, int fit,
                                                           int imode, int iit, int fit_term,
                                                           unsigned long long* bar) {
     extern __shared__ __align__(16) unsigned char smem_raw[];

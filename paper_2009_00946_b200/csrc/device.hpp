@@ -18,7 +18,7 @@ constexpr int kMaxL = 16;
 constexpr int kMaxW = 16;
 constexpr int kMaxM = 16;
 constexpr int kMaxC = 8;  // CTAs per layer cluster (portable cluster size)
-constexpr int kMaxGU = 32;      // row groups per layer (max side 128 / the smallest row group, 4)
+constexpr int kMaxGU = 64;      // row groups per layer (max side 128 / the smallest row group, 2)
 constexpr int kMaxWtCode = 1024;  // WFS tiles with a constant-bank position code
 
 // Fused-PCG carry (pcg.hpp:32-38 PcgScalars plus per-frame bookkeeping).
@@ -78,7 +78,7 @@ struct GeoParams {
     int gchunk[kMaxW + 1];
     int o_gd;                   // [((l*kMaxGU + u)*kMaxW + w)*8] gather staging descriptors (int4-aligned)
     int gbuf_bytes;   // the gather's double-buffered row-contracted block (see cluster.cuh)
-    int gather_batch; // k_gather residency plan: 0 single instance (2 CTAs/SM), 1 batches (3 CTAs/SM)
+    int gather_minb;  // k_gather residency plan: resident CTAs per SM (2, 3 or 4; cluster.cuh)
 };
 
 enum LayerMode : int {

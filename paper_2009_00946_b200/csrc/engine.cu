@@ -403,7 +403,7 @@ Plan build_plan(const Geometry& g, int elem_bytes, int batch, int wa = 0, int wb
         gp.grows = batch <= 2 ? 4 : 8;
         if (const char* v = std::getenv("FEWHA_GATHER_ROWS")) {
             const int r = std::atoi(v);
-            if (r == 4 || r == 8) gp.grows = r;
+            if (r == 2 || r == 4 || r == 8) gp.grows = r;
         }
         auto grp_rows = [&](int side) { return std::min(gp.grows, side); };
         gp.o_bs = static_cast<int>(pl.ti.size());
@@ -470,8 +470,14 @@ Plan build_plan(const Geometry& g, int elem_bytes, int batch, int wa = 0, int wb
         // row-contracted blocks G of every WFS of a chunk (group rows x psi block columns)
         gp.gbuf_bytes = static_cast<int>(a16(static_cast<size_t>(W) * gp.grows * cmax * elem_bytes));
         const size_t fixed = a16(static_cast<size_t>(gp.gbuf_bytes)) + 1024;  // + static shared memory
-        gp.gather_batch = batch > 2 ? 1 : 0;  // residency plan of k_gather (cluster.cuh)
-        const size_t limit = static_cast<size_t>(gp.gather_batch ? kGatherSmemKbBatch : kGatherSmemKbLat) * 1024;
+        // residency plan of k_gather (cluster.cuh): 2 CTAs/SM for a single instance, 3 for
+        // batches (FEWHA_GATHER_MINB overrides: 2, 3 or 4)
+        gp.gather_minb = batch > 2 ? 3 : 2;
+        if (const char* v = std::getenv("FEWHA_GATHER_MINB")) {
+            const int m = std::atoi(v);
+            if (m >= 2 && m <= 4) gp.gather_minb = m;
+        }
+        const size_t limit = static_cast<size_t>(gather_smem_kb(gp.gather_minb)) * 1024;
         const size_t budget = limit > fixed ? limit - fixed : 0;
         gp.nchunk = 0;
         gp.gchunk[0] = wa;
@@ -781,8 +787,9 @@ struct Launch {
         opt_in(k_wfs<T, true, FEWHA_WFS_MINB_LAT>, wfs_smem(gp));
         opt_in(k_wfs<T, false, FEWHA_WFS_MINB_BATCH>, wfs_smem(gp));
         opt_in(k_wfs<T, true, FEWHA_WFS_MINB_BATCH>, wfs_smem(gp));
-        opt_in(k_gather<T, kGatherMinbLat>, gather_smem(gp));
-        opt_in(k_gather<T, kGatherMinbBatch>, gather_smem(gp));
+        opt_in(k_gather<T, 2>, gather_smem(gp));
+        opt_in(k_gather<T, 3>, gather_smem(gp));
+        opt_in(k_gather<T, 4>, gather_smem(gp));
     }
     // layer kernels: grid (C, L, count), cluster (C,1,1)
     static void cl(int flen, bool inverse, const GeoParams& gp, const Bufs<T>& bf, int mode, int it, int count,
@@ -849,8 +856,9 @@ struct Launch {
         cudaLaunchAttribute attr[1];
         const int groups = gp.maxside / std::min(gp.grows, gp.maxside);
         cudaLaunchConfig_t cfg = pdl_cfg(dim3(groups, gp.L, count), gather_smem(gp), st, attr);
-        if (gp.gather_batch) CK(cudaLaunchKernelEx(&cfg, k_gather<T, kGatherMinbBatch>, gp, bf));
-        else CK(cudaLaunchKernelEx(&cfg, k_gather<T, kGatherMinbLat>, gp, bf));
+        if (gp.gather_minb == 4) CK(cudaLaunchKernelEx(&cfg, k_gather<T, 4>, gp, bf));
+        else if (gp.gather_minb == 3) CK(cudaLaunchKernelEx(&cfg, k_gather<T, 3>, gp, bf));
+        else CK(cudaLaunchKernelEx(&cfg, k_gather<T, 2>, gp, bf));
     }
     static void fit(const GeoParams& gp, const Bufs<T>& bf, int step, int count, cudaStream_t st) {
         cudaLaunchAttribute attr[1];
@@ -1531,9 +1539,9 @@ void Engine::step(const double* slopes, double* coeffs, double* dm, double* rho,
     const size_t B = P.batch, S = P.gp.S, n = P.gp.n, A = P.gp.A, it = P.gp.iters;
     const cudaStream_t st = P.s();
     double* meas = P.precision == 64 ? P.sd.meas : P.sf.meas;
-    CK(cudaMemcpyAsync(meas, slopes, B * S * sizeof(double), cudaMemcpyHostToDevice, st));
     if (P.precision == 64) P.ensure_graph<double>();
     else P.ensure_graph<float>();
+    CK(cudaMemcpyAsync(meas, slopes, B * S * sizeof(double), cudaMemcpyHostToDevice, st));
     CK(cudaGraphLaunch(P.graph, st));
     ++P.step_counter;
     P.telem_pending = P.telemetry_on;

@@ -15,7 +15,7 @@ cudaError_t launch_layer_cluster(bool inverse, const GeoParams& gp, const Bufs<T
                                  cudaStream_t st, int fit_term, size_t smem) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(gp.ccl, gp.L, count);
-    cfg.blockDim = dim3(256, 1, 1);
+    cfg.blockDim = dim3(kClThreads, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
@@ -40,7 +40,7 @@ cudaError_t launch_fused_cluster(const GeoParams& gp, const Bufs<T>& bf, int fmo
                                  int pdl) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(gp.ccl, gp.L, count);
-    cfg.blockDim = dim3(256, 1, 1);
+    cfg.blockDim = dim3(kClThreads, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[3];
@@ -62,7 +62,7 @@ template <typename T, int FLEN>
 cudaError_t fused_cluster_capacity(const GeoParams& gp, size_t smem, int* clusters) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(gp.ccl, gp.L, 1);
-    cfg.blockDim = dim3(256, 1, 1);
+    cfg.blockDim = dim3(kClThreads, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;

@@ -459,3 +459,21 @@ def test_fused_forward_inverse_is_bitwise_the_split_frame(name, precision, monke
     sf, ss = gf.get_state(), gs.get_state()
     for key in ("c", "b", "r", "p", "q", "a_prev", "a_prev2"):
         assert np.array_equal(sf[key], ss[key]), key
+
+
+@pytest.mark.parametrize("rows,minb", [(2, 4), (4, 3), (8, 2)])
+def test_gather_plans_are_bitwise_equal(rows, minb, monkeypatch):
+    """The adjoint gather's row-group size and residency plan (FEWHA_GATHER_ROWS /
+    FEWHA_GATHER_MINB; defaults 4 rows at 2 CTAs/SM for one instance, 8 at 3 for
+    batches) change only the work split: every layer node still sums its WFS in
+    ascending order, so frames are bitwise equal."""
+    path = preset("elt_mcao84_3dm.json")
+    g0 = fg.Reconstructor(path)
+    monkeypatch.setenv("FEWHA_GATHER_ROWS", str(rows))
+    monkeypatch.setenv("FEWHA_GATHER_MINB", str(minb))
+    g1 = fg.Reconstructor(path)
+    rng = np.random.default_rng(8)
+    for _ in range(3):
+        s = rng.standard_normal(g0.dims.S) * 0.01
+        assert np.array_equal(g0.step(s), g1.step(s))
+        assert np.array_equal(g0.coeffs(), g1.coeffs())
