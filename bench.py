@@ -387,6 +387,43 @@ def run_ours(args):
                       "note": "inputs resident, no flush between steps (working set 64 x ~15 MB > L2)"}
         rb.close()
 
+    # ---- the other BASELINE configs (rank 0, N=1): single-frame latency -------------
+    configs = None
+    if rank == 0 and world == 1 and not shard and args.configs:
+        configs = {}
+        for tag, name in (("1_small_mcao_2dm", "small_mcao_2dm"), ("2_elt_ltao84", "elt_ltao84"),
+                          ("4_elt_moao84", "elt_moao84")):
+            pth = os.path.join(ROOT, "presets", name + ".json")
+            dc = preset_dims(pth)
+            rx = fg.Reconstructor(pth, precision=args.precision, device=local)
+            rx.build_preconditioner()
+            rx.set_stream(st.cuda_stream)
+            sx = torch.from_numpy(slope_stream(rx, pth, 8, seed=rc.seed)).to(dev)
+            for k in range(max(args.warmup, 3)):
+                rx.load_slopes_device(sx[k % 8].data_ptr())
+                rx.step_device(None)
+            rx.sync()
+            KC = min(K, 300)
+            cs = [torch.cuda.Event(enable_timing=True) for _ in range(KC)]
+            ce = [torch.cuda.Event(enable_timing=True) for _ in range(KC)]
+            for k in range(KC):
+                rx.load_slopes_device(sx[k % 8].data_ptr())
+                flush.zero_()
+                cs[k].record(st)
+                rx.step_device(None)
+                ce[k].record(st)
+            torch.cuda.synchronize(dev)
+            rx.sync()
+            cms = np.array([a.elapsed_time(e_) for a, e_ in zip(cs, ce)])
+            c50 = float(np.percentile(cms, 50))
+            fbx = frame_bytes(dc, b)
+            configs[tag] = {"preset": os.path.relpath(pth, ROOT), "n_coeff": dc["n"], "n_slopes": dc["S"],
+                            "n_act": dc["A"], "frames": KC, "p50_ms": round(c50, 5),
+                            "p99_ms": round(float(np.percentile(cms, 99)), 5),
+                            "recon_per_s": round(1000.0 / float(np.mean(cms)), 1),
+                            "frame_roofline_frac_at_p50": round(fbx / (c50 / 1000.0) / 1e9 / peak, 5)}
+            rx.close()
+
     # ---- CPU baseline (rank 0, N=1 only) -------------------------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -436,6 +473,8 @@ def run_ours(args):
             line["cpu_baseline"] = cpu
         if batch_info:
             line["batch64"] = batch_info
+        if configs:
+            line["other_configs"] = configs
         print(json.dumps(line))
     rc.shutdown()
     return 0
@@ -452,6 +491,8 @@ def main():
     ap.add_argument("--cpu-frames", type=int, default=150)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-batch64", dest="batch64", action="store_false")
+    ap.add_argument("--no-configs", dest="configs", action="store_false",
+                    help="skip the single-frame latency of BASELINE configs 1, 2 and 4")
     ap.add_argument("--shard", action="store_true", help="N>1: per-WFS sharding of one frame (NCCL exchange)")
     args = ap.parse_args()
     if args.impl == "reference":
