@@ -461,34 +461,70 @@ __device__ __forceinline__ void frame_epilogue(const GeoParams& gp, const Bufs<T
     bf.carry[b * (gp.iters + 1)] = c;
 }
 
+// One actuator's fit + control.  Everything constant (the DM's layer group, the
+// bilinear stencil of every layer) and the DM history (written by the previous
+// frame, 21 launches back: kernels.cuh protocol) is loaded before the
+// programmatic-launch wait; after it only the phi samples of the group (all in
+// flight together) remain on the critical path.
 template <typename T>
-__device__ void fit_actuator(const GeoParams& gp, const Bufs<T>& bf, int step, int k, int b) {
+__device__ __forceinline__ void fit_actuator(const GeoParams& gp, const Bufs<T>& bf, int step, int k, int b,
+                                             bool live) {
     int m = 0;
     while (m + 1 < gp.M && k >= gp.aoff[m + 1]) ++m;
     const int idx = k - gp.aoff[m], na = gp.nact[m];
     const int i = idx / na, j = idx % na;
+    const size_t g = static_cast<size_t>(b) * gp.A + k;
+    const int ofit = live ? gp.ti[gp.o_fit + m] : -1;
+    // bilinear resampling of each layer of the DM's group (ascending layer order)
+    int src[kMaxL], sd[kMaxL];
+    T fy[kMaxL], fx[kMaxL];
+    int cnt = 0;
+    if (live && ofit >= 0) {
+        const T* tw = weights<T>(gp);
+        cnt = gp.ti[ofit];
+#pragma unroll
+        for (int q = 0; q < kMaxL; ++q) {
+            src[q] = -1;
+            sd[q] = 0;
+            fy[q] = fx[q] = T(0);
+            if (q < cnt) {
+                const int l = gp.ti[ofit + 1 + 3 * q], ox = gp.ti[ofit + 2 + 3 * q], oy = gp.ti[ofit + 3 + 3 * q];
+                const int ii = gp.ti[oy + i], jj = gp.ti[ox + j];
+                if (ii >= 0 && jj >= 0) {  // a projected point off this layer's grid contributes zero
+                    sd[q] = gp.side[l];
+                    src[q] = gp.coff[l] + ii * sd[q] + jj;
+                    fy[q] = tw[oy + i];
+                    fx[q] = tw[ox + j];
+                }
+            }
+        }
+    }
+    T a0 = T(0), a1 = T(0);
+    if (live && step) {
+        a0 = bf.a_prev[g];
+        a1 = bf.a_prev2[g];
+    }
+    pdl_wait();
+    pdl_launch_dependents();
+    if (!live) return;
     const T* phi_b = bf.phi + static_cast<size_t>(b) * gp.n;
-    const int ofit = gp.ti[gp.o_fit + m];
     T at;
     if (ofit < 0) {  // identity pairing, n_act = 2^J (reconstructor.hpp:304-307)
         at = phi_b[gp.coff[m] + i * gp.side[m] + j];
-    } else {  // bilinear resampling of each layer of the DM's group (ascending layer order)
-        const T* tw = weights<T>(gp);
-        const int cnt = gp.ti[ofit];
+    } else {
         at = T(0);
-        for (int q = 0; q < cnt; ++q) {
-            const int l = gp.ti[ofit + 1 + 3 * q], ox = gp.ti[ofit + 2 + 3 * q], oy = gp.ti[ofit + 3 + 3 * q];
-            const int ii = gp.ti[oy + i], jj = gp.ti[ox + j];
-            if (ii < 0 || jj < 0) continue;  // projected point off this layer's grid
-            at += bilinear<T>(phi_b + gp.coff[l], gp.side[l], ii, jj, tw[oy + i], tw[ox + j]);
+#pragma unroll
+        for (int q = 0; q < kMaxL; ++q) {
+            if (q >= cnt) break;
+            if (src[q] < 0) continue;
+            at += bilinear<T>(phi_b + src[q], sd[q], 0, 0, fy[q], fx[q]);
         }
     }
-    const size_t g = static_cast<size_t>(b) * gp.A + k;
     if (!step) {
         bf.a_out[g] = at;
         return;
     }
-    const T a0 = bf.a_prev[g], a1 = bf.a_prev2[g], gain = static_cast<T>(gp.gain);
+    const T gain = static_cast<T>(gp.gain);
     const T an = gp.closed ? a0 + gain * (at - a1) : (T(1) - gain) * a0 + gain * at;
     bf.a_prev2[g] = a0;
     bf.a_prev[g] = an;
@@ -497,12 +533,10 @@ __device__ void fit_actuator(const GeoParams& gp, const Bufs<T>& bf, int step, i
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_fit_control(const GeoParams gp, const Bufs<T> bf, int step) {
-    pdl_wait();
-    pdl_launch_dependents();
     const int b = blockIdx.y;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    fit_actuator(gp, bf, step, k < gp.A ? k : 0, b, k < gp.A);
     if (step && blockIdx.x == 0 && threadIdx.x == 0) frame_epilogue(gp, bf, b);
-    if (k < gp.A) fit_actuator(gp, bf, step, k, b);
 }
 
 // ---------------------------------------------------------------------------
