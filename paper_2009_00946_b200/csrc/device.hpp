@@ -125,6 +125,9 @@ struct Bufs {
     double* rho_log;   // [B][iters]
     int* status;       // [B]
     int* nlog;         // [B]
+    // zero-copy frame outputs (page-locked host memory, written by k_fit_control; null: off)
+    double* a_host;         // a1 [B][A] straight into the caller's buffer
+    unsigned char* frame_host;  // mirror of the rho_log | status | nlog block
 };
 
 }  // namespace fewha_gpu

@@ -960,6 +960,45 @@ struct EngineImpl {
     void invalidate_graph() {
         if (graph) cudaGraphExecDestroy(graph);
         graph = nullptr;
+        if (graph_tmpl) cudaGraphDestroy(graph_tmpl);
+        graph_tmpl = nullptr;
+        fit_node = nullptr;
+        fit_a_host = nullptr;
+    }
+
+    // Zero-copy DM output: when the caller's DM buffer is page-locked, the frame's
+    // fit/control kernel also stores a1 straight into it (posted PCIe writes inside
+    // the kernel instead of a D2H copy after the graph); its `a_host` argument is
+    // repointed per call.
+    cudaGraph_t graph_tmpl = nullptr;   // the captured frame (node handles for updates)
+    cudaGraphNode_t fit_node = nullptr;  // k_fit_control of the frame
+    double* fit_a_host = nullptr;        // what the node currently writes to
+    template <typename T>
+    void find_fit_node() {
+        size_t nn = 0;
+        CK(cudaGraphGetNodes(graph_tmpl, nullptr, &nn));
+        std::vector<cudaGraphNode_t> nodes(nn);
+        CK(cudaGraphGetNodes(graph_tmpl, nodes.data(), &nn));
+        for (auto nd : nodes) {
+            cudaGraphNodeType ty;
+            CK(cudaGraphNodeGetType(nd, &ty));
+            if (ty != cudaGraphNodeTypeKernel) continue;
+            cudaKernelNodeParams kp{};
+            CK(cudaGraphKernelNodeGetParams(nd, &kp));
+            if (kp.func == reinterpret_cast<void*>(k_fit_control<T>)) fit_node = nd;
+        }
+    }
+    template <typename T>
+    void set_fit_a_host(double* a) {
+        if (!fit_node || a == fit_a_host) return;
+        cudaKernelNodeParams kp{};
+        CK(cudaGraphKernelNodeGetParams(fit_node, &kp));
+        Bufs<T> bf = *static_cast<const Bufs<T>*>(kp.kernelParams[1]);
+        bf.a_host = a;
+        void* args[3] = {kp.kernelParams[0], &bf, kp.kernelParams[2]};
+        kp.kernelParams = args;
+        CK(cudaGraphExecKernelNodeSetParams(graph, fit_node, &kp));
+        fit_a_host = a;
     }
 
     // ---- one frame of Reconstructor::step on the state workspace ----------
@@ -975,6 +1014,7 @@ struct EngineImpl {
         Bufs<T> bf = state<T>().bf;
         bf.jac = static_cast<const T*>(jac);
         bf.jinv = static_cast<const T*>(jinv);
+        bf.frame_host = static_cast<unsigned char*>(host_out);  // page-locked mirror (null: copied)
         return bf;
     }
     int n_segments() const { return gp.iters + 2; }
@@ -1121,7 +1161,8 @@ struct EngineImpl {
         }
         CK(cudaStreamEndCapture(stream, &gr));
         CK(cudaGraphInstantiate(&graph, gr, 0));
-        CK(cudaGraphDestroy(gr));
+        graph_tmpl = gr;
+        find_fit_node<T>();
     }
 
     // ---- apply_M on a double workspace (also the preconditioner probes) ----
@@ -1532,6 +1573,21 @@ void group_step_device(const std::vector<Engine*>& members) {
 
 void Engine::build_preconditioner() { p_->build_precond(); }
 
+// Page-locked host memory the device can store to (FEWHA_ZERO_COPY=0: never).
+static bool page_locked(const void* p) {
+    static const bool on = [] {
+        const char* v = std::getenv("FEWHA_ZERO_COPY");
+        return !(v && v[0] == '0');
+    }();
+    if (!on) return false;
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost && at.devicePointer == p;
+}
+
 void Engine::step(const double* slopes, double* coeffs, double* dm, double* rho, int* n_rho) {
     auto& P = *p_;
     CK(cudaSetDevice(P.device));
@@ -1539,26 +1595,28 @@ void Engine::step(const double* slopes, double* coeffs, double* dm, double* rho,
     const size_t B = P.batch, S = P.gp.S, n = P.gp.n, A = P.gp.A, it = P.gp.iters;
     const cudaStream_t st = P.s();
     double* meas = P.precision == 64 ? P.sd.meas : P.sf.meas;
+    const size_t fob = P.precision == 64 ? P.sd.frame_out_bytes : P.sf.frame_out_bytes;
+    if (!P.host_out) {  // page-locked mirror of the rho/status/nlog block, written by the frame itself
+        CK(cudaMallocHost(&P.host_out, fob));
+        P.invalidate_graph();
+    }
     if (P.precision == 64) P.ensure_graph<double>();
     else P.ensure_graph<float>();
+    double* dm_direct = (dm && P.fit_node && page_locked(dm)) ? dm : nullptr;
+    if (P.precision == 64) P.set_fit_a_host<double>(dm_direct);
+    else P.set_fit_a_host<float>(dm_direct);
     CK(cudaMemcpyAsync(meas, slopes, B * S * sizeof(double), cudaMemcpyHostToDevice, st));
     CK(cudaGraphLaunch(P.graph, st));
     ++P.step_counter;
     P.telem_pending = P.telemetry_on;
-    // rho_log | status | nlog in one copy into a pinned staging block
-    const size_t fob = P.precision == 64 ? P.sd.frame_out_bytes : P.sf.frame_out_bytes;
-    const void* dblk = P.precision == 64 ? static_cast<const void*>(P.sd.bf.rho_log)
-                                         : static_cast<const void*>(P.sf.bf.rho_log);
-    if (!P.host_out) CK(cudaMallocHost(&P.host_out, fob));
-    CK(cudaMemcpyAsync(P.host_out, dblk, fob, cudaMemcpyDeviceToHost, st));
     if (P.precision == 64) {
-        if (dm) CK(cudaMemcpyAsync(dm, P.sd.bf.a_out, B * A * sizeof(double), cudaMemcpyDeviceToHost, st));
+        if (dm && !dm_direct) CK(cudaMemcpyAsync(dm, P.sd.bf.a_out, B * A * sizeof(double), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         if (coeffs) d2h_coeff<double>(coeffs, P.sd.bf.c, P.plan.perm, B, st);
     } else {
         CK(cudaStreamSynchronize(st));
         if (coeffs) d2h_coeff<float>(coeffs, P.sf.bf.c, P.plan.perm, B, st);
-        if (dm) d2h_conv<float>(dm, P.sf.bf.a_out, B * A, st);
+        if (dm && !dm_direct) d2h_conv<float>(dm, P.sf.bf.a_out, B * A, st);
     }
     const auto* hrho = static_cast<const double*>(P.host_out);
     const int* status = reinterpret_cast<const int*>(hrho + B * it);

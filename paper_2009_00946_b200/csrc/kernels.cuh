@@ -454,6 +454,14 @@ __device__ __forceinline__ void frame_epilogue(const GeoParams& gp, const Bufs<T
     Carry c = bf.carry[b * (gp.iters + 1) + gp.iters];
     bf.status[b] = c.err;
     bf.nlog[b] = c.nlog;
+    if (bf.frame_host) {  // the host's copy of this instance's rho log, status and count
+        const int B = gridDim.y;
+        double* hr = reinterpret_cast<double*>(bf.frame_host);
+        for (int k = 0; k < gp.iters; ++k) hr[b * gp.iters + k] = bf.rho_log[b * gp.iters + k];
+        int* hs = reinterpret_cast<int*>(hr + static_cast<size_t>(B) * gp.iters);
+        hs[b] = c.err;
+        hs[B + b] = c.nlog;
+    }
     c.done = 0;
     c.err = 0;
     c.nlog = 0;
@@ -529,6 +537,7 @@ __device__ __forceinline__ void fit_actuator(const GeoParams& gp, const Bufs<T>&
     bf.a_prev2[g] = a0;
     bf.a_prev[g] = an;
     bf.a_out[g] = an;
+    if (bf.a_host) bf.a_host[g] = static_cast<double>(an);  // posted PCIe write into the caller's buffer
 }
 
 template <typename T>

@@ -477,3 +477,37 @@ def test_gather_plans_are_bitwise_equal(rows, minb, monkeypatch):
         s = rng.standard_normal(g0.dims.S) * 0.01
         assert np.array_equal(g0.step(s), g1.step(s))
         assert np.array_equal(g0.coeffs(), g1.coeffs())
+
+
+@pytest.mark.parametrize("precision_", [64, 32])
+def test_zero_copy_outputs_match_copied_outputs(precision_):
+    """fewha_gpu_step into a page-locked DM buffer: the frame's fit/control kernel
+    stores a1 straight into it (and the rho/status block always lands in a pinned
+    mirror); pageable buffers are copied after the graph.  Same values either way,
+    and the device-side a_out stays valid for fewha_gpu_device_buffers users."""
+    import ctypes as C
+
+    import torch
+
+    path = preset("elt_mcao84_3dm.json")
+    gz, gc = fg.Reconstructor(path, precision=precision_), fg.Reconstructor(path, precision=precision_)
+    d = gz.dims
+    rng = np.random.default_rng(6)
+    L = fg.lib()
+    dp = C.POINTER(C.c_double)
+    pin_a = torch.zeros(d.A, dtype=torch.float64).pin_memory()
+    pin_r = torch.zeros(d.iters, dtype=torch.float64).pin_memory()
+    for k in range(4):
+        s = rng.standard_normal(d.S) * 0.01
+        nr = (C.c_int * 1)()
+        pin_a.fill_(np.nan)
+        gz._chk(L.fewha_gpu_step(gz._h, s.ctypes.data_as(dp), None, C.cast(pin_a.data_ptr(), dp),
+                                 C.cast(pin_r.data_ptr(), dp), nr))
+        ac = gc.step(s)
+        assert np.array_equal(pin_a.numpy(), ac), k
+        assert nr[0] == len(gc.last_rho) and np.array_equal(pin_r.numpy()[: nr[0]], gc.last_rho), k
+        if k == 2:  # a pageable DM buffer in between: the node goes back to device-only stores
+            assert np.array_equal(gz.step(s), gc.step(s))
+    sz, sc = gz.get_state(), gc.get_state()
+    for key in ("c", "a_prev", "a_prev2"):
+        assert np.array_equal(sz[key], sc[key]), key
