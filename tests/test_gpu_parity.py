@@ -511,3 +511,33 @@ def test_zero_copy_outputs_match_copied_outputs(precision_):
     sz, sc = gz.get_state(), gc.get_state()
     for key in ("c", "a_prev", "a_prev2"):
         assert np.array_equal(sz[key], sc[key]), key
+
+
+def test_pinned_pageable_and_device_slopes_interleaved():
+    """Page-locked and pageable host slopes and device-resident frames interleaved
+    on one engine give the frames of an engine fed pageable slopes only."""
+    import ctypes as C
+
+    import torch
+
+    path = preset("elt_mcao84_3dm.json")
+    gz, gc = fg.Reconstructor(path), fg.Reconstructor(path)
+    d = gz.dims
+    rng = np.random.default_rng(9)
+    L = fg.lib()
+    dp = C.POINTER(C.c_double)
+    pins = [torch.from_numpy(rng.standard_normal(d.S) * 0.01).pin_memory() for _ in range(3)]
+    for k in range(6):
+        s = pins[k % 3]
+        if k == 3:  # pageable in between
+            az = gz.step(s.numpy().copy())
+        elif k == 4:  # device-resident frame in between
+            gz.load_slopes(s.numpy())
+            gz.step_device(None)
+            gz.sync()
+            az = gz.get_state()["a_prev"]
+        else:
+            az = np.zeros(d.A)
+            nr = (C.c_int * 1)()
+            gz._chk(L.fewha_gpu_step(gz._h, C.cast(s.data_ptr(), dp), None, az.ctypes.data_as(dp), None, nr))
+        assert np.array_equal(az, gc.step(s.numpy())), k
