@@ -103,7 +103,8 @@ int fewha_gpu_preconditioner(fewha_gpu_t h, double* out /* n */);
 /* --- the hot path: Reconstructor::step (reconstructor.hpp:310-355) ---------
  * slopes [batch][S] (host, fp64).  Outputs may be NULL:
  *   coeffs_out [batch][n] = st.c after the step; dm_out [batch][A] = a^(1);
- *   rho_out [batch][iters] = last_telemetry().rho; n_rho [batch].  */
+ *   rho_out [batch][iters] = last_telemetry().rho; n_rho [batch].
+ * A page-locked dm_out is written directly by the frame's last kernel (no D2H copy). */
 int fewha_gpu_step(fewha_gpu_t h, const double* slopes, double* coeffs_out, double* dm_out, double* rho_out,
                    int* n_rho);
 /* ReconstructorState::reset (reconstructor.hpp:81-91) on every instance */
