@@ -219,6 +219,31 @@ def cpu_reference_time(preset, stream, frames, threads):
     return us, r.threads
 
 
+def host_slope_ring(frames, torch):
+    """The e2e input ring as an AO real-time host would hold it: the frames in
+    2 MB transparent-huge-page memory registered with CUDA (one DMA translation per
+    2 MB instead of per 4 KB page -- rotating 4 KB-page buffers measured 5-45 us
+    slower per call on these hosts, tools/e2e_break.py); falls back to
+    torch.pin_memory()."""
+    import mmap
+    try:
+        from cuda.bindings import runtime as rt
+        hp = 2 << 20
+        nbytes = frames.nbytes
+        mm = mmap.mmap(-1, nbytes + 2 * hp, flags=mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS)
+        base = np.frombuffer(mm, dtype=np.uint8)
+        off = (-base.ctypes.data) % hp
+        mm.madvise(mmap.MADV_HUGEPAGE, off, nbytes + hp)
+        ring = base[off:off + nbytes].view(np.float64).reshape(frames.shape)
+        ring[:] = frames
+        if rt.cudaHostRegister(ring.ctypes.data, nbytes, rt.cudaHostRegisterDefault)[0] != rt.cudaError_t.cudaSuccess:
+            raise RuntimeError("cudaHostRegister failed")
+        host_slope_ring.keep = (mm, ring)  # lives for the process
+        return torch.from_numpy(ring), "slope ring in 2 MB THP memory registered with cudaHostRegister"
+    except Exception as e:  # noqa: BLE001
+        return torch.from_numpy(frames).pin_memory(), f"slope ring in torch pinned memory ({type(e).__name__})"
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -339,7 +364,7 @@ def run_ours(args):
             traffic = None
 
     # ---- e2e through the C-ABI with pinned host buffers ------------------------------
-    pin_s = torch.from_numpy(stream_host).pin_memory()
+    pin_s, host_note = host_slope_ring(stream_host, torch)
     pin_a = torch.zeros(d["A"], dtype=torch.float64).pin_memory()
     pin_rho = torch.zeros(d["iters"], dtype=torch.float64).pin_memory()
     lib = fg.lib()
@@ -347,6 +372,10 @@ def run_ours(args):
     dp = C.POINTER(C.c_double)
     nr = (C.c_int * 1)()
     e2e_ms = []
+    # real-time hygiene of an AO host loop: no garbage collection inside the frame loop
+    import gc
+    gc_was = gc.isenabled()
+    gc.disable()
     s_ptrs = [C.cast(pin_s[f].data_ptr(), dp) for f in range(F)]  # argument marshalling outside the timing
     a_ptr, r_ptr, step_fn, h = C.cast(pin_a.data_ptr(), dp), C.cast(pin_rho.data_ptr(), dp), lib.fewha_gpu_step, rec._h
     for k in range(max(args.warmup, 3) + min(K, 300)):
@@ -359,6 +388,8 @@ def run_ours(args):
         rec._chk(code)
         if k >= max(args.warmup, 3):
             e2e_ms.append((t1 - t0) * 1000.0)
+    if gc_was:
+        gc.enable()
     e2e_ms = np.array(e2e_ms)
     (e2e_mean,) = rc.max_over_ranks([float(np.mean(e2e_ms))], device=dev)
     e2e_val = 1000.0 / e2e_mean if shard else rc.aggregate_throughput(1, e2e_mean)
@@ -464,7 +495,7 @@ def run_ours(args):
                          "bytes_per_launch": dom_bytes, "launch_ms": round(dom_ms, 5),
                          "share_of_frame": round(share[dom], 3), "peak_source": peak_kind,
                          "kernel_shares": {k: round(v, 3) for k, v in sorted(share.items(), key=lambda x: -x[1])}},
-            "e2e": {"value": round(e2e_val, 3), "unit": UNIT, "h2d_bytes_per_step": S * 8,
+            "e2e": {"value": round(e2e_val, 3), "unit": UNIT, "h2d_bytes_per_step": S * 8, "host_buffers": host_note,
                     "d2h_bytes_per_step": d["A"] * 8 + d["iters"] * 8 + 8,
                     "p50_ms": round(float(np.percentile(e2e_ms, 50)), 5),
                     "p99_ms": round(float(np.percentile(e2e_ms, 99)), 5)},

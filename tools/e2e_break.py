@@ -10,6 +10,12 @@ import sys
 import time
 
 import numpy as np
+
+if os.environ.get("FEWHA_SCHED"):  # experiment: CUDA host-sync scheduling before any context exists
+    from cuda.bindings import runtime as _rt
+    _flag = {"spin": _rt.cudaDeviceScheduleSpin, "yield": _rt.cudaDeviceScheduleYield,
+             "block": _rt.cudaDeviceScheduleBlockingSync}[os.environ["FEWHA_SCHED"]]
+    print("cudaSetDeviceFlags", _rt.cudaSetDeviceFlags(_flag))
 import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -54,6 +60,45 @@ def T(name, f):
 
 
 T("step(dm + rho)", lambda: L.fewha_gpu_step(rec._h, ps, None, pa, pr, nr))
+# the bench's pattern: 16 different page-locked frames in rotation
+ring = torch.from_numpy(np.random.default_rng(1).standard_normal((16, d.S)) * 0.01).pin_memory()
+ring_p = [C.cast(ring[f].data_ptr(), dp) for f in range(16)]
+kk = [0]
+
+
+def rot():
+    kk[0] += 1
+    return L.fewha_gpu_step(rec._h, ring_p[kk[0] % 16], None, pa, pr, nr)
+
+
+T("step(dm + rho), 16-frame ring", rot)
+
+# the same ring in transparent-huge-page-backed memory registered with CUDA
+import mmap  # noqa: E402
+
+from cuda.bindings import runtime as rt  # noqa: E402
+
+HP = 2 << 20
+nbytes = 16 * d.S * 8
+mm = mmap.mmap(-1, nbytes + 2 * HP, flags=mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS)
+base = np.frombuffer(mm, dtype=np.uint8)
+off = (-base.ctypes.data) % HP
+mm.madvise(mmap.MADV_HUGEPAGE, off, nbytes + HP - off if off else nbytes + HP)
+hp = base[off:off + nbytes].view(np.float64).reshape(16, d.S)
+hp[:] = ring.numpy()
+print("thp:", open("/sys/kernel/mm/transparent_hugepage/enabled").read().strip(),
+      "register:", rt.cudaHostRegister(hp.ctypes.data, nbytes, rt.cudaHostRegisterDefault)[0])
+hp_p = [C.cast(hp[f].ctypes.data, dp) for f in range(16)]
+
+
+def rot_hp():
+    kk[0] += 1
+    return L.fewha_gpu_step(rec._h, hp_p[kk[0] % 16], None, pa, pr, nr)
+
+
+T("step(dm + rho), 16-frame THP ring", rot_hp)
+with open("/proc/self/smaps_rollup") as f:
+    print([ln.strip() for ln in f if "AnonHugePages" in ln])
 T("step(dm only)", lambda: L.fewha_gpu_step(rec._h, ps, None, pa, None, None))
 T("step(no outputs)", lambda: L.fewha_gpu_step(rec._h, ps, None, None, None, None))
 T("step_device + sync", lambda: (rec.step_device(None), rec.sync()))
