@@ -1706,8 +1706,14 @@ void Engine::step_device(const void* d_slopes) {
     double* meas = P.precision == 64 ? P.sd.meas : P.sf.meas;
     if (d_slopes && d_slopes != meas)
         CK(cudaMemcpyAsync(meas, d_slopes, sizeof(double) * P.gp.S * P.batch, cudaMemcpyDeviceToDevice, st));
-    if (P.precision == 64) P.ensure_graph<double>();
-    else P.ensure_graph<float>();
+    // device-resident frames never store into a caller's host buffer from an earlier step()
+    if (P.precision == 64) {
+        P.ensure_graph<double>();
+        P.set_fit_a_host<double>(nullptr);
+    } else {
+        P.ensure_graph<float>();
+        P.set_fit_a_host<float>(nullptr);
+    }
     CK(cudaGraphLaunch(P.graph, st));
     ++P.step_counter;
     P.telem_pending = P.telemetry_on;

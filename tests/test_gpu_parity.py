@@ -511,6 +511,12 @@ def test_zero_copy_outputs_match_copied_outputs(precision_):
     sz, sc = gz.get_state(), gc.get_state()
     for key in ("c", "a_prev", "a_prev2"):
         assert np.array_equal(sz[key], sc[key]), key
+    # device-resident frames after a zero-copy step leave the caller's buffer alone
+    before = pin_a.numpy().copy()
+    gz.load_slopes(rng.standard_normal(d.S) * 0.01)
+    gz.step_device(None)
+    gz.sync()
+    assert np.array_equal(pin_a.numpy(), before)
 
 
 def test_pinned_pageable_and_device_slopes_interleaved():
