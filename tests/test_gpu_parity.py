@@ -547,3 +547,31 @@ def test_pinned_pageable_and_device_slopes_interleaved():
             nr = (C.c_int * 1)()
             gz._chk(L.fewha_gpu_step(gz._h, C.cast(s.data_ptr(), dp), None, az.ctypes.data_as(dp), None, nr))
         assert np.array_equal(az, gc.step(s.numpy())), k
+
+
+def test_zero_copy_outputs_batched():
+    """Batched engine, page-locked DM and rho buffers: every instance's a1, rho log and
+    count land where the copied path puts them."""
+    import ctypes as C
+
+    import torch
+
+    path = preset("small_mcao.json")
+    B = 3
+    gz, gc = fg.Reconstructor(path, batch=B), fg.Reconstructor(path, batch=B)
+    d = gz.dims
+    L = fg.lib()
+    dp = C.POINTER(C.c_double)
+    pin_a = torch.zeros(B * d.A, dtype=torch.float64).pin_memory()
+    pin_r = torch.zeros(B * d.iters, dtype=torch.float64).pin_memory()
+    rng = np.random.default_rng(17)
+    for k in range(3):
+        s = rng.standard_normal((B, d.S)) * 0.01
+        nr = (C.c_int * B)()
+        gz._chk(L.fewha_gpu_step(gz._h, np.ascontiguousarray(s).ctypes.data_as(dp), None,
+                                 C.cast(pin_a.data_ptr(), dp), C.cast(pin_r.data_ptr(), dp), nr))
+        ac = gc.step(s)
+        assert np.array_equal(pin_a.numpy().reshape(B, d.A), ac), k
+        rz = pin_r.numpy().reshape(B, d.iters)
+        for b in range(B):
+            assert nr[b] == len(gc.last_rho[b]) and np.array_equal(rz[b, : nr[b]], gc.last_rho[b]), (k, b)
