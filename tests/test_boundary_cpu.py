@@ -134,3 +134,20 @@ def test_no_silent_cpu_fallback():
         pass
     with pytest.raises(fg.FewhaError, match="CUDA"):
         fg.Reconstructor(preset("mini.json"))
+
+
+def test_bench_models_cover_every_kernel_kind():
+    """bench.py's algorithmic-bytes model has an entry for every kernel kind the
+    library's profile reports (the roofline object must never miss a kind), and the
+    frame model matches SURVEY 8(d)'s 71.76 MB at the ELT MCAO-84 scale."""
+    import importlib.util
+
+    import paper_2009_00946_b200 as fg
+
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    d = bench.preset_dims(os.path.join(ROOT, "presets", "elt_mcao84_3dm.json"))
+    for kind in fg.Reconstructor.KERNEL_KINDS:
+        assert bench.kernel_bytes(kind, d, 8) > 0, kind
+    assert abs(bench.frame_bytes(d, 8) - 71.76e6) / 71.76e6 < 1e-3
