@@ -575,3 +575,15 @@ def test_zero_copy_outputs_batched():
         rz = pin_r.numpy().reshape(B, d.iters)
         for b in range(B):
             assert nr[b] == len(gc.last_rho[b]) and np.array_equal(rz[b, : nr[b]], gc.last_rho[b]), (k, b)
+
+
+def test_layer_side_beyond_the_cluster_transform_is_a_config_error(tmp_path):
+    """Layer grids are transformed by one <= 8-CTA cluster of 16-row bands, so
+    2^J <= 128 (J <= 7, the MAORY/ELT presets' order); larger grids are refused up
+    front with the reference's configuration-error class, never run wrongly."""
+    j = json.load(open(preset("small_mcao.json")))
+    j["layers"][0]["grid_order"] = 8
+    p = tmp_path / "j8.json"
+    p.write_text(json.dumps(j))
+    with pytest.raises(fg.ConfigError):
+        fg.Reconstructor(str(p))
