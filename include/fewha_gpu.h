@@ -125,6 +125,16 @@ int fewha_gpu_step_device(fewha_gpu_t h, const void* d_slopes);
 int fewha_gpu_sync(fewha_gpu_t h);
 /* Kernel launches of one step_device frame (for launch accounting). */
 int fewha_gpu_launches_per_step(fewha_gpu_t h);
+/* The execution plan the handle chose for its batch size (DESIGN.md "Batch-mode
+ * choices"): CTAs per layer cluster, tail block side D of the cluster transforms,
+ * adjoint-gather rows per CTA and its resident CTAs per SM, whether the inverse
+ * kernel stages its operands by TMA (1) or streams them (0), resident WFS-tile
+ * CTAs per SM, WFS tiles, kernel launches per frame. */
+typedef struct {
+    int cluster_ctas, tail, gather_rows, gather_ctas_per_sm, inverse_staged, wfs_ctas_per_sm, wfs_tiles,
+        launches_per_step;
+} fewha_gpu_plan_t;
+int fewha_gpu_plan_info(fewha_gpu_t h, fewha_gpu_plan_t* out);
 /* Runs ONE frame eagerly (not from the graph) with a CUDA event after every
  * launch on the handle's stream; writes per-launch device ms and kernel kind
  * (0 wfs_rhs, 1 adjoint, 2 fwd_rhs, 3 inv_pcg0, 4 inv_pcg, 5 wfs, 6 fwd_pcg,
@@ -150,6 +160,15 @@ int fewha_gpu_sh_transpose(fewha_gpu_t h, const double* meas, double* wf, int co
 /* Noise-free forward model s = Gamma (P phi - P_dm a) (simulation.hpp:164-199);
  * a may be NULL (no correction).  layers: nodal [count][n]. */
 int fewha_gpu_forward_slopes(fewha_gpu_t h, const double* layers, const double* a, double* meas, int count);
+
+/* The frame's fused per-WFS kernel (k_wfs) applied on its own, so the hot-path
+ * tile kernel is parity-tested in isolation (wavefronts [count][N_w] out):
+ *   rhs = 0: psi = Gamma^T C^-1 Gamma P in, in = nodal layers [count][n]
+ *            (apply_M stage 2, reconstructor.hpp:182-192)
+ *   rhs = 1: psi = Gamma^T C^-1 (meas + Gamma P_dm in), in = DM commands
+ *            [count][A] or NULL, meas [count][S] (add_dm_slopes :259-280 +
+ *            build_rhs stage 1 :221-231).  The sh_adjoint fault factor applies. */
+int fewha_gpu_wfs_operator(fewha_gpu_t h, int rhs, const double* in, const double* meas, double* psi, int count);
 
 /* --- StepTelemetry (reconstructor.hpp:94-102; bench.hpp:214-228 CSV schema) ---
  * Opt-in: enabling re-captures the frame graph with an event-record node around

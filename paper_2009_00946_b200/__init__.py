@@ -36,6 +36,7 @@ EXPORTS = (
     "fewha_gpu_propagate", "fewha_gpu_propagate_transpose", "fewha_gpu_sh", "fewha_gpu_sh_transpose",
     "fewha_gpu_forward_slopes", "fewha_gpu_shard_range", "fewha_gpu_nccl_unique_id", "fewha_gpu_shard",
     "fewha_gpu_shard_wfs", "fewha_gpu_group_step_device", "fewha_gpu_enable_telemetry", "fewha_gpu_last_telemetry",
+    "fewha_gpu_wfs_operator", "fewha_gpu_plan_info",
 )
 
 
@@ -75,6 +76,11 @@ class _State(C.Structure):
 class _Telemetry(C.Structure):
     _fields_ = [("step", C.c_longlong), ("valid", C.c_int), ("stage1_us", C.c_double), ("stage2_us", C.c_double),
                 ("stage3_us", C.c_double), ("pcg_us", C.c_double), ("fit_us", C.c_double), ("total_us", C.c_double)]
+
+
+class _Plan(C.Structure):
+    _fields_ = [(k, C.c_int) for k in ("cluster_ctas", "tail", "gather_rows", "gather_ctas_per_sm", "inverse_staged",
+                                       "wfs_ctas_per_sm", "wfs_tiles", "launches_per_step")]
 
 
 class _DevBufs(C.Structure):
@@ -131,6 +137,8 @@ def lib() -> C.CDLL:
             getattr(L, "fewha_gpu_" + name).argtypes = [vp, dp, dp, C.c_int]
         L.fewha_gpu_wavelet.argtypes = [vp, C.c_int, dp, C.c_int]
         L.fewha_gpu_forward_slopes.argtypes = [vp, dp, dp, dp, C.c_int]
+        L.fewha_gpu_wfs_operator.argtypes = [vp, C.c_int, dp, dp, dp, C.c_int]
+        L.fewha_gpu_plan_info.argtypes = [vp, C.POINTER(_Plan)]
         ip = C.POINTER(C.c_int)
         L.fewha_gpu_shard_range.argtypes = [C.c_char_p, C.c_int, C.c_int, ip, ip]
         L.fewha_gpu_nccl_unique_id.argtypes = [C.c_char_p]
@@ -360,6 +368,23 @@ class Reconstructor:
         self._chk(self._L.fewha_gpu_forward_slopes(self._h, _dp(x), _dp(None if a is None else _f64(a)), _dp(out), count))
         return out if count == 1 else out.reshape(count, self.dims.S)
 
+    def wfs_operator(self, x=None, meas=None, rhs: bool = False):
+        """The frame's fused per-WFS tile kernel (k_wfs) on its own:
+        rhs=False: psi = Gamma^T C^-1 Gamma P x (x nodal layers [count, n]);
+        rhs=True:  psi = Gamma^T C^-1 (meas + Gamma P_dm x) (x DM commands or None)."""
+        d = self.dims
+        if rhs:
+            m = _f64(meas)
+            count = m.size // d.S
+            a = None if x is None else _f64(x, d.A * count)
+        else:
+            a = _f64(x)
+            count = a.size // d.n
+            m = None
+        out = np.zeros(count * d.Nw)
+        self._chk(self._L.fewha_gpu_wfs_operator(self._h, 1 if rhs else 0, _dp(a), _dp(m), _dp(out), count))
+        return out if count == 1 else out.reshape(count, d.Nw)
+
     # -- CUDA-resident path -----------------------------------------------------------
     def enable_telemetry(self, on: bool = True):
         """StepTelemetry stage timings for every graph frame (opt-in, serialising)."""
@@ -412,6 +437,12 @@ class Reconstructor:
 
     def launches_per_step(self) -> int:
         return int(self._L.fewha_gpu_launches_per_step(self._h))
+
+    def plan_info(self) -> dict:
+        """The execution plan chosen for this handle's batch size (fewha_gpu_plan_info)."""
+        p = _Plan()
+        self._chk(self._L.fewha_gpu_plan_info(self._h, C.byref(p)))
+        return {k: getattr(p, k) for k, _ in _Plan._fields_}
 
     def phase_stamps(self, enable_only=False):
         """Per-phase %globaltimer stamps of the cluster kernels of the last

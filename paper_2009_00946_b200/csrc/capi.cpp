@@ -179,6 +179,20 @@ int fewha_gpu_load_slopes(fewha_gpu_t h, const void* src, int on_device) {
 int fewha_gpu_step_device(fewha_gpu_t h, const void* d_slopes) { H_GUARD(h->eng->step_device(d_slopes)) }
 int fewha_gpu_sync(fewha_gpu_t h) { H_GUARD(h->eng->sync_check()) }
 int fewha_gpu_launches_per_step(fewha_gpu_t h) { return h ? h->eng->launches_per_step() : -1; }
+int fewha_gpu_plan_info(fewha_gpu_t h, fewha_gpu_plan_t* out) {
+    if (!out) return FEWHA_ARG;
+    H_GUARD({
+        const auto pi = h->eng->plan_info();
+        out->cluster_ctas = pi.cluster_ctas;
+        out->tail = pi.tail;
+        out->gather_rows = pi.gather_rows;
+        out->gather_ctas_per_sm = pi.gather_ctas_per_sm;
+        out->inverse_staged = pi.inverse_staged;
+        out->wfs_ctas_per_sm = pi.wfs_ctas_per_sm;
+        out->wfs_tiles = pi.wfs_tiles;
+        out->launches_per_step = pi.launches_per_step;
+    })
+}
 float fewha_gpu_debug_bench_dwt(fewha_gpu_t h, int variant, int inverse, int reps, int threads) {
     float ms = -1.f;
     if (!h) return ms;
@@ -224,6 +238,13 @@ int fewha_gpu_sh_transpose(fewha_gpu_t h, const double* meas, double* wf, int co
 }
 int fewha_gpu_forward_slopes(fewha_gpu_t h, const double* layers, const double* a, double* meas, int count) {
     H_GUARD(h->eng->forward_slopes(layers, a, meas, count))
+}
+
+int fewha_gpu_wfs_operator(fewha_gpu_t h, int rhs, const double* in, const double* meas, double* psi, int count) {
+    H_GUARD({
+        if (rhs ? !meas : !in) throw ArgError("wfs_operator: null input");
+        h->eng->wfs_operator(rhs, in, meas, psi, count);
+    })
 }
 
 int fewha_gpu_enable_telemetry(fewha_gpu_t h, int on) { H_GUARD(h->eng->enable_telemetry(on != 0)) }

@@ -705,6 +705,7 @@ struct Work {
             bf.status = reinterpret_cast<int*>(blk + nr * sizeof(double));
             bf.nlog = bf.status + cnt;
         }
+        CK(cudaDeviceSynchronize());  // the zero fills (legacy stream) land before stream work uses the buffers
     }
 };
 
@@ -738,10 +739,8 @@ struct Launch {
     // TMA staging of the inverse kernel's operands pays for a single instance (latency);
     // batches stream them from global memory at twice the residency
     static int inv_staged_for(int count) {
-        static const int mode = [] {
-            const char* v = std::getenv("FEWHA_INV_STAGE");
-            return v ? std::atoi(v) : -1;
-        }();
+        const char* v = std::getenv("FEWHA_INV_STAGE");  // read per plan (tests switch it between engines)
+        const int mode = v ? std::atoi(v) : -1;
         return mode >= 0 ? (mode ? 1 : 0) : (count <= 2 ? 1 : 0);
     }
     static size_t fwd_cl_smem(const GeoParams& gp, int flen) {
@@ -1250,13 +1249,19 @@ struct EngineImpl {
             inv[static_cast<size_t>(plan.perm[k])] = 1.0 / diag[k];
         }
         diag.swap(dperm);
+        // uploads ordered on the frame stream (non-blocking: it does not wait for the
+        // legacy stream), complete before the first frame can read them
+        const cudaStream_t fs = s();
+        CK(cudaStreamSynchronize(fs));
         if (precision == 64) {
-            CK(cudaMemcpy(jac, diag.data(), n * sizeof(double), cudaMemcpyHostToDevice));
-            CK(cudaMemcpy(jinv, inv.data(), n * sizeof(double), cudaMemcpyHostToDevice));
+            CK(cudaMemcpyAsync(jac, diag.data(), n * sizeof(double), cudaMemcpyHostToDevice, fs));
+            CK(cudaMemcpyAsync(jinv, inv.data(), n * sizeof(double), cudaMemcpyHostToDevice, fs));
+            CK(cudaStreamSynchronize(fs));
         } else {
             std::vector<float> f(diag.begin(), diag.end()), fi(inv.begin(), inv.end());
-            CK(cudaMemcpy(jac, f.data(), n * sizeof(float), cudaMemcpyHostToDevice));
-            CK(cudaMemcpy(jinv, fi.data(), n * sizeof(float), cudaMemcpyHostToDevice));
+            CK(cudaMemcpyAsync(jac, f.data(), n * sizeof(float), cudaMemcpyHostToDevice, fs));
+            CK(cudaMemcpyAsync(jinv, fi.data(), n * sizeof(float), cudaMemcpyHostToDevice, fs));
+            CK(cudaStreamSynchronize(fs));
         }
         has_precond = true;
     }
@@ -1382,6 +1387,9 @@ Engine::Engine(Geometry g, int precision, int batch, int device) : p_(std::make_
         P.fr.add(P.fbar);
         CK(cudaMemset(P.fbar, 0, sizeof(unsigned long long) * static_cast<size_t>(batch)));
     }
+    // the table uploads and zero fills above ran on the legacy stream: let them land
+    // before anything is issued on the (non-blocking) frame stream
+    CK(cudaDeviceSynchronize());
     reset();
 }
 
@@ -1490,6 +1498,7 @@ void Engine::shard(int rank, int world, const void* nccl_id) {
         const auto& api = NcclApi::get();
         api.check(api.CommInitRank(&P.comm, world, id, rank), "ncclCommInitRank");
     }
+    CK(cudaDeviceSynchronize());  // shard table uploads (legacy stream) land before the frame stream reads them
     P.invalidate_graph();
 }
 
@@ -1631,13 +1640,20 @@ void Engine::reset() {
     auto& P = *p_;
     CK(cudaSetDevice(P.device));
     const size_t B = P.batch, n = P.gp.n, A = P.gp.A;
+    // Frames run on a non-blocking stream (the engine's or the caller's), which does
+    // not order against the legacy default stream: finish any frame in flight, zero
+    // the state on the frame stream and return only when it has landed.
+    const cudaStream_t st = P.s();
+    CK(cudaStreamSynchronize(st));
     auto zero_state = [&](auto& w, size_t es) {
         for (void* ptr : {(void*)w.bf.c, (void*)w.bf.b, (void*)w.bf.r, (void*)w.bf.p, (void*)w.bf.q, (void*)w.bf.mz})
-            CK(cudaMemset(ptr, 0, B * n * es));
-        for (void* ptr : {(void*)w.bf.a_prev2, (void*)w.bf.a_prev, (void*)w.bf.a_out}) CK(cudaMemset(ptr, 0, B * A * es));
+            CK(cudaMemsetAsync(ptr, 0, B * n * es, st));
+        for (void* ptr : {(void*)w.bf.a_prev2, (void*)w.bf.a_prev, (void*)w.bf.a_out})
+            CK(cudaMemsetAsync(ptr, 0, B * A * es, st));
         std::vector<Carry> c(B * (P.gp.iters + 1));
         for (auto& x : c) x = Carry{0.0, 0.0, 0.0, 1, 0, 0, 0};  // PcgScalars{} : fresh
-        CK(cudaMemcpy(w.bf.carry, c.data(), c.size() * sizeof(Carry), cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(w.bf.carry, c.data(), c.size() * sizeof(Carry), cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));
     };
     if (P.precision == 64) zero_state(P.sd, sizeof(double));
     else zero_state(P.sf, sizeof(float));
@@ -1661,7 +1677,8 @@ void Engine::get_state(int inst, double* c, double* b, double* r, double* p, dou
         d2h_conv<T>(a_prev2, w.bf.a_prev2 + inst * A, A, st);
         d2h_conv<T>(a_prev, w.bf.a_prev + inst * A, A, st);
         Carry cr;
-        CK(cudaMemcpy(&cr, w.bf.carry + inst * (P.gp.iters + 1), sizeof(Carry), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpyAsync(&cr, w.bf.carry + inst * (P.gp.iters + 1), sizeof(Carry), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
         sc[0] = cr.rho_old;
         sc[1] = cr.alpha;
         sc[2] = cr.fresh ? 1.0 : 0.0;
@@ -1688,7 +1705,8 @@ void Engine::set_state(int inst, const double* c, const double* b, const double*
         h2d_conv<T>(w.bf.a_prev2 + inst * A, a_prev2, A, st);
         h2d_conv<T>(w.bf.a_prev + inst * A, a_prev, A, st);
         Carry cr{sc[0], sc[1], 0.0, sc[2] != 0.0 ? 1 : 0, 0, 0, 0};
-        CK(cudaMemcpy(w.bf.carry + inst * (P.gp.iters + 1), &cr, sizeof(Carry), cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(w.bf.carry + inst * (P.gp.iters + 1), &cr, sizeof(Carry), cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));
     };
     if (P.precision == 64) set(P.sd);
     else set(P.sf);
@@ -1776,6 +1794,20 @@ void Engine::sync_check() {
     CK(cudaStreamSynchronize(st));
     for (int s : status)
         if (s) throw std::runtime_error("pcg_solve: non-finite scalar (indefinite operator?)");
+}
+
+PlanInfo Engine::plan_info() const {
+    const auto& P = *p_;
+    PlanInfo pi;
+    pi.cluster_ctas = P.gp.ccl;
+    pi.tail = P.gp.ctail;
+    pi.gather_rows = P.gp.grows;
+    pi.gather_ctas_per_sm = P.gp.gather_minb;
+    pi.inverse_staged = P.precision == 64 ? Launch<double>::inv_staged_for(P.batch) : Launch<float>::inv_staged_for(P.batch);
+    pi.wfs_ctas_per_sm = P.batch <= 2 ? FEWHA_WFS_MINB_LAT : FEWHA_WFS_MINB_BATCH;
+    pi.wfs_tiles = P.gp.wt_count;
+    pi.launches_per_step = launches_per_step();
+    return pi;
 }
 
 int Engine::launches_per_step() const {
@@ -1898,7 +1930,7 @@ void Engine::build_rhs(const double* meas, double* out, int count) {
     auto& P = *p_;
     FEWHA_DISPATCH({
         with_ops<T>(P, count, [&](Work<T>& w) {
-            CK(cudaMemcpy(w.meas, meas, sizeof(double) * P.gp.S * count, cudaMemcpyHostToDevice));
+            CK(cudaMemcpyAsync(w.meas, meas, sizeof(double) * P.gp.S * count, cudaMemcpyHostToDevice, P.stream));
             Bufs<T> bf = w.bf;
             Launch<T>::wfs(true, P.gp, bf, 0, count, P.stream);
             Launch<T>::gather(P.gp, bf, count, P.stream);
@@ -1913,7 +1945,7 @@ void Engine::add_dm_slopes(const double* a, double* meas, int count) {
     FEWHA_DISPATCH({
         with_ops<T>(P, count, [&](Work<T>& w) {
             h2d_conv<T>(w.a, a, static_cast<size_t>(P.gp.A) * count, P.stream);
-            CK(cudaMemcpy(w.meas, meas, sizeof(double) * P.gp.S * count, cudaMemcpyHostToDevice));
+            CK(cudaMemcpyAsync(w.meas, meas, sizeof(double) * P.gp.S * count, cudaMemcpyHostToDevice, P.stream));
             const int sub = P.gp.S / 2;
             k_slopes<T><<<dim3((sub + 255) / 256, count), 256, 0, P.stream>>>(P.gp, nullptr, nullptr, w.a, T(1),
                                                                                w.meas, w.meas2, count);
@@ -1968,6 +2000,31 @@ void Engine::wavelet(int inverse, double* data, int count) {
     })
 }
 
+// The frame's fused per-WFS kernel (k_wfs, kernels.cuh wfs_tile) as an operator:
+//   rhs = 0: psi = Gamma^T C^-1 Gamma P phi          (apply_M stage 2, reconstructor.hpp:182-192)
+//   rhs = 1: psi = Gamma^T C^-1 (s + Gamma P_dm a)   (add_dm_slopes :259-280 + build_rhs :221-231;
+//            a == null: psi = Gamma^T C^-1 s)
+void Engine::wfs_operator(int rhs, const double* in, const double* meas, double* psi, int count) {
+    auto& P = *p_;
+    FEWHA_DISPATCH({
+        with_ops<T>(P, count, [&](Work<T>& w) {
+            Bufs<T> bf = w.bf;
+            int with_dm = 0;
+            if (rhs) {
+                if (in) {
+                    h2d_conv<T>(w.a, in, static_cast<size_t>(P.gp.A) * count, P.stream);
+                    with_dm = 1;
+                }
+                CK(cudaMemcpyAsync(w.meas, meas, sizeof(double) * P.gp.S * count, cudaMemcpyHostToDevice, P.stream));
+            } else {
+                h2d_conv<T>(bf.phi, in, static_cast<size_t>(P.gp.n) * count, P.stream);
+            }
+            Launch<T>::wfs(rhs != 0, P.gp, bf, with_dm, count, P.stream);
+            d2h_conv<T>(psi, bf.psi, static_cast<size_t>(P.gp.Nw) * count, P.stream);
+        });
+    })
+}
+
 void Engine::propagate(const double* layers, double* wf, int count) {
     auto& P = *p_;
     FEWHA_DISPATCH({
@@ -2007,7 +2064,7 @@ void Engine::sh_transpose(const double* meas, double* wf, int count) {
     auto& P = *p_;
     FEWHA_DISPATCH({
         with_ops<T>(P, count, [&](Work<T>& w) {
-            CK(cudaMemcpy(w.meas, meas, sizeof(double) * P.gp.S * count, cudaMemcpyHostToDevice));
+            CK(cudaMemcpyAsync(w.meas, meas, sizeof(double) * P.gp.S * count, cudaMemcpyHostToDevice, P.stream));
             k_sh_transpose<T><<<dim3((P.gp.Nw + 255) / 256, count), 256, 0, P.stream>>>(P.gp, w.meas, w.bf.psi, count);
             d2h_conv<T>(wf, w.bf.psi, static_cast<size_t>(P.gp.Nw) * count, P.stream);
         });

@@ -20,6 +20,12 @@ struct StepTelemetry {
     double stage1_us = 0, stage2_us = 0, stage3_us = 0, pcg_us = 0, fit_us = 0, total_us = 0;
 };
 
+// Execution plan an engine chose for its batch size (engine.cu build_plan / Launch)
+struct PlanInfo {
+    int cluster_ctas = 0, tail = 0, gather_rows = 0, gather_ctas_per_sm = 0, inverse_staged = 0, wfs_ctas_per_sm = 0,
+        wfs_tiles = 0, launches_per_step = 0;
+};
+
 class Engine;
 // contiguous WFS range [first, second) of shard `rank` of `world` (balanced by wavefront nodes)
 std::pair<int, int> shard_range(const Geometry& g, int rank, int world);
@@ -58,6 +64,7 @@ public:
     void enable_telemetry(bool on);
     StepTelemetry last_telemetry();
     int launches_per_step() const;
+    PlanInfo plan_info() const;
     int profile_step(float* ms, int* kinds, int max);
     void enable_stamps(bool on);
     float bench_dwt(int variant, int inverse, int reps, int threads);
@@ -83,6 +90,7 @@ public:
     void sh(const double* wf, double* meas, int count);
     void sh_transpose(const double* meas, double* wf, int count);
     void forward_slopes(const double* layers, const double* a, double* meas, int count);
+    void wfs_operator(int rhs, const double* in, const double* meas, double* psi, int count);
 
 private:
     std::unique_ptr<EngineImpl> p_;

@@ -515,6 +515,11 @@ __device__ __forceinline__ void fit_actuator(const GeoParams& gp, const Bufs<T>&
     pdl_wait();
     pdl_launch_dependents();
     if (!live) return;
+    // A non-finite PCG scalar makes the reference throw from pcg_solve before
+    // fit_to_mirrors and the history rotation (reconstructor.hpp:325-351): no
+    // command is produced and a^(-1), a^(0) stay as they were.  (The flag is read
+    // alongside the phi samples below; only the stores wait for it.)
+    const bool failed = step && bf.carry[b * (gp.iters + 1) + gp.iters].err != 0;
     const T* phi_b = bf.phi + static_cast<size_t>(b) * gp.n;
     T at;
     if (ofit < 0) {  // identity pairing, n_act = 2^J (reconstructor.hpp:304-307)
@@ -532,6 +537,7 @@ __device__ __forceinline__ void fit_actuator(const GeoParams& gp, const Bufs<T>&
         bf.a_out[g] = at;
         return;
     }
+    if (failed) return;
     const T gain = static_cast<T>(gp.gain);
     const T an = gp.closed ? a0 + gain * (at - a1) : (T(1) - gain) * a0 + gain * at;
     bf.a_prev2[g] = a0;

@@ -223,3 +223,38 @@ def test_lnem_projection_restates_reference_sampling():
     o_proj = Oracle(jp)
     x = np.random.default_rng(2).standard_normal(o_ref.dims.n)
     assert rel_err(o_proj.fit(x), o_ref.fit(x)) == 0.0
+
+
+@pytest.mark.slow
+def test_fp32_reference_conditioning():
+    """Why the GPU fp32 free-running window is finite (tests/test_gpu_plans.py):
+    the reference algorithm itself, with only its carried state (c, b, r, p, q,
+    a^(-1), a^(0)) and the slopes rounded to fp32 between frames and every
+    operation in fp64, leaves 1e-4 of its own fp64 loop within 30 ELT frames
+    (measured: c 3.7e-4 and rho 3.9e-3 by frame 28), and 1e-15 slope jitter moves
+    its rho by ~1e-9.  An fp32 engine rounds every operation, so no fp32
+    implementation can track the fp64 loop for longer than the reference's own
+    warm-restarted PCG (pcg.hpp:80-99) allows."""
+    import sys
+
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from test_gpu_parity import noisy_slopes, smooth_layers
+
+    f32 = lambda x: np.asarray(x, np.float32).astype(np.float64)  # noqa: E731
+    name = preset("elt_mcao84.json")
+    o, o32 = Oracle(name), Oracle(name)
+    o.build_preconditioner()
+    o32.build_preconditioner()
+    lay = smooth_layers(o, 3)
+    errs = []
+    for k in range(30):
+        s = noisy_slopes(o, lay, 100 + k, o.get_state()["a_prev2"])
+        c_o, _, _ = o.step(s)
+        st = o32.get_state()
+        for key in ("c", "b", "r", "p", "q", "a_prev2", "a_prev"):
+            st[key] = f32(st[key])
+        o32.set_state(st)
+        c_r, _, _ = o32.step(f32(s))
+        errs.append(rel_err(c_r, c_o))
+    assert max(errs[:10]) < 1e-5  # well conditioned early on
+    assert max(errs) > 1e-4       # ... and past 1e-4 within 30 frames
