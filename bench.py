@@ -14,14 +14,21 @@ shadow of the same preset (same layers, WFS and PCG; 9 identity-fitted DMs).
 
   value      reconstructions/s over all ranks, slopes resident in HBM, timed with
              CUDA events around each frame's graph launch; L2 flushed (256 MiB
-             write) before every timed frame.
-  e2e        the same metric through the C-ABI fewha_gpu_step with pinned HOST
-             buffers: H2D of the frame's slopes + D2H of a^(1), rho and status
-             inside the timed region.
-  roofline   dominant kernel (largest share of the frame in a per-launch event
-             profile): algorithmic bytes per launch / its mean event duration.
+             write) before every timed frame.  `latency`: a separate >= 1000-frame
+             sample of the same (p50/p99 need it whatever --steps is).
+  e2e        the same metric through the C-ABI fewha_gpu_step with HOST buffers
+             (H2D of the frame's slopes + a^(1), rho and status back inside the
+             timed region): a registered slope ring (headline) and, beside it,
+             ordinary pageable arrays (the reference's calling convention).
+  roofline   the dominant kernel FUNCTION (largest share of the frame, its launch
+             kinds summed), timed by event-record nodes between the launches of the
+             captured frame graph: algorithmic bytes per launch / its mean launch
+             time; `traffic` = its ncu DRAM bytes per launch (profiles/dram_traffic.json).
   cpu_baseline  the reference solver (oracle/_ref, compiled from the unmodified
-             reference) timed on this host's cores on a bounded frame sample.
+             reference) timed on this host's cores on a bounded frame sample, with
+             the CPU model.
+  shard      (N > 1) the per-WFS split of one instance's frame over the N ranks
+             (the north star's partition), next to the replicas value.
 
 --impl reference runs the reference CPU solver alone (rank 0), with every
 host thread, on the same config and slope stream.
@@ -273,6 +280,7 @@ def run_reference(args):
                                "(L=M shadow of the 3-DM preset: the reference supports only L=M)",
                    "preset": os.path.relpath(args.preset, ROOT), "threads": r.threads},
         "cpu_baseline": {"value": round(val, 3), "unit": UNIT, "cores": r.threads, "kind": "reference",
+                         "cpu_model": cpu_model(), "nproc": os.cpu_count(),
                          "sample": f"{args.steps} frames of Reconstructor::step after {max(args.warmup,1)} warm-up, "
                                    f"{r.threads} pool threads on {os.cpu_count()} host cpus"},
         "e2e": {"value": round(val, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -281,17 +289,116 @@ def run_reference(args):
     return 0
 
 
+# kernel kind (fewha_gpu_profile_step / last_launch_times) -> kernel function
+FUNC = {"wfs_rhs": "k_wfs", "wfs": "k_wfs", "gather": "k_gather", "adjoint": "k_gather",
+        "fwd_rhs": "k_fwd_cluster", "fwd_pcg": "k_fwd_cluster",
+        "inv_pcg0": "k_inv_cluster", "inv_pcg": "k_inv_cluster", "inv_fit": "k_inv_cluster",
+        "fit_control": "k_fit_control",
+        "fwd_rhs_inv0": "k_fwd_inv_cluster", "fwd_inv_pcg": "k_fwd_inv_cluster", "fwd_inv_fit": "k_fwd_inv_cluster"}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def graph_function_profile(rec, frames, before, d, b, batch=1):
+    """Per-kernel-function device times inside the captured frame graph: the
+    telemetry event-record nodes between launches (fewha_gpu_last_launch_times).
+    before(f) runs ahead of frame f (slope load, L2 flush).  Returns
+    {function: {launches, ms_per_frame, bytes_per_frame, ...}} and the frame ms."""
+    rec.enable_telemetry(True)
+    acc, frame_ms = {}, []
+    for f in range(frames + 2):
+        before(f)
+        rec.step_device(None)
+        lt = rec.last_launch_times()
+        if f < 2:
+            continue  # the first telemetry frames re-capture the graph
+        frame_ms.append(sum(t for _, t in lt))
+        for kind, t in lt:
+            fn = FUNC[kind]
+            e = acc.setdefault(fn, {"launches": 0, "ms": 0.0, "bytes": 0})
+            e["launches"] += 1
+            e["ms"] += t
+            e["bytes"] += kernel_bytes(kind, d, b) * batch
+    rec.enable_telemetry(False)
+    rec.sync()
+    tot = sum(frame_ms)
+    out = {}
+    for fn, e in acc.items():
+        out[fn] = {"launches_per_frame": e["launches"] // frames, "ms_per_frame": e["ms"] / frames,
+                   "launch_ms": e["ms"] / e["launches"], "bytes_per_launch": e["bytes"] / e["launches"],
+                   "share": e["ms"] / tot, "achieved_gbs": e["bytes"] / (e["ms"] / 1000.0) / 1e9}
+    return out, float(np.mean(frame_ms))
+
+
+def roofline_object(prof, peak, peak_kind, traffic_key, note):
+    dom = max(prof, key=lambda k: prof[k]["share"])
+    e = prof[dom]
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "dram_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = load_json(tpath).get(traffic_key, {}).get(dom)
+        except Exception:
+            traffic = None
+    return {"bound": "hbm", "kernel": dom, "achieved": round(e["achieved_gbs"], 2), "peak": peak, "unit": "GB/s",
+            "frac": round(e["achieved_gbs"] / peak, 4), "traffic": traffic,
+            "bytes_per_launch": int(e["bytes_per_launch"]), "launch_ms": round(e["launch_ms"], 5),
+            "launches_per_frame": e["launches_per_frame"], "share_of_frame": round(e["share"], 3),
+            "peak_source": peak_kind, "timing": note,
+            "functions": {k: {"share": round(v["share"], 3), "launch_ms": round(v["launch_ms"], 5),
+                              "frac": round(v["achieved_gbs"] / peak, 4)}
+                          for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["share"])}}
+
+
+def e2e_loop(rec, lib, slopes_ptrs, a_ptr, r_ptr, frames, warm, flush, dev, torch):
+    """fewha_gpu_step through the C-ABI with host buffers: per-call wall ms."""
+    import ctypes as C
+    import gc
+    nr = (C.c_int * 1)()
+    step_fn, h = lib.fewha_gpu_step, rec._h
+    gc_was = gc.isenabled()
+    gc.disable()  # real-time hygiene of an AO host loop
+    out = []
+    try:
+        for k in range(warm + frames):
+            sp = slopes_ptrs[k % len(slopes_ptrs)]
+            flush.zero_()
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            code = step_fn(h, sp, None, a_ptr, r_ptr, nr)
+            t1 = time.perf_counter()
+            rec._chk(code)
+            if k >= warm:
+                out.append((t1 - t0) * 1000.0)
+    finally:
+        if gc_was:
+            gc.enable()
+    return np.array(out)
+
+
 def run_ours(args):
     import torch
     import paper_2009_00946_b200 as fg
 
     from paper_2009_00946_b200.replicas import init_replicas
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # init log: communicator size of the per-WFS split
     rc = init_replicas()
     world, rank, local = rc.world, rc.rank, rc.local_rank
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     d = preset_dims(args.preset)
     b = args.precision // 8
+    peak, peak_kind = peaks()
 
     rec = fg.Reconstructor(args.preset, precision=args.precision, batch=1, device=local)
     shard = args.shard and world > 1
@@ -310,89 +417,120 @@ def run_ours(args):
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     S = d["S"]
 
-    def load(k):
+    def load(k, r=rec):
         # slopes for frame k into the library's resident slot (outside timing)
-        rec.load_slopes_device(stream[k % F].data_ptr())
+        r.load_slopes_device(stream[k % F].data_ptr())
 
     for k in range(max(args.warmup, 3)):
         load(k)
         rec.step_device(None)
     rec.sync()
 
-    # ---- device-resident timed region -------------------------------------------
+    def timed_frames(r, K):
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+        for k in range(K):
+            load(k, r)
+            flush.zero_()
+            starts[k].record(st)
+            r.step_device(None)
+            ends[k].record(st)
+        torch.cuda.synchronize(dev)
+        r.sync()
+        return np.array([s_.elapsed_time(e_) for s_, e_ in zip(starts, ends)])
+
+    # ---- device-resident timed region (exactly K frames) ----------------------------
     K = args.steps
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     rc.barrier()
     torch.cuda.synchronize(dev)
     with Clocks(local) as clk:
-        for k in range(K):
-            load(k)
-            flush.zero_()
-            starts[k].record(st)
-            rec.step_device(None)
-            ends[k].record(st)
-        torch.cuda.synchronize(dev)
-    rec.sync()
+        ms = timed_frames(rec, K)
     rc.barrier()
-    ms = np.array([s.elapsed_time(e) for s, e in zip(starts, ends)])
     total_ms = float(ms.sum())
     p50, p99 = float(np.percentile(ms, 50)), float(np.percentile(ms, 99))
     total_ms, p50, p99 = rc.max_over_ranks([total_ms, p50, p99], device=dev)
     value = K / (total_ms / 1000.0) if shard else rc.aggregate_throughput(K, total_ms)
 
-    # ---- per-launch profile (events between launches on the launching stream) ----
-    prof = {}
-    for _ in range(20):
-        load(0)
-        flush.zero_()
-        for kind, t in rec.profile_step():
-            prof.setdefault(kind, []).append(t)
-    frame_prof_ms = sum(sum(v) for v in prof.values()) / 20.0
-    share = {k: sum(v) / 20.0 / frame_prof_ms for k, v in prof.items()}
-    dom = max(share, key=share.get)
-    dom_ms = float(np.mean(prof[dom]))
-    dom_bytes = kernel_bytes(dom, d, b)
-    peak, peak_kind = peaks()
-    achieved = dom_bytes / (dom_ms / 1000.0) / 1e9
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "dram_traffic.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = load_json(tpath).get(f"fp{args.precision}", {}).get(dom)
-        except Exception:
-            traffic = None
+    # ---- latency distribution: >= 1000 frames whatever --steps is (p99 needs them) ----
+    NL = max(1000, K)
+    lms = timed_frames(rec, NL)
+    l50, l99, lmax = rc.max_over_ranks([float(np.percentile(lms, 50)), float(np.percentile(lms, 99)),
+                                        float(lms.max())], device=dev)
+    latency = {"frames": NL, "p50_ms": round(l50, 5), "p99_ms": round(l99, 5), "max_ms": round(lmax, 5),
+               "recon_per_s_p50": round(1000.0 / l50, 1), "l2": "flushed before every frame",
+               "note": "separate sample after the timed region, same method; max over ranks"}
 
-    # ---- e2e through the C-ABI with pinned host buffers ------------------------------
+    # ---- per-function kernel times inside the frame graph (event nodes) -------------
+    def before(f):
+        load(f)
+        flush.zero_()
+
+    prof, prof_frame_ms = graph_function_profile(rec, 30, before, d, b)
+    roof = roofline_object(prof, peak, peak_kind, f"fp{args.precision}",
+                           "event-record nodes between the frame graph's launches (telemetry graph, L2 flushed "
+                           f"before each frame, 30 frames).  The event nodes serialise the programmatic-launch "
+                           f"overlap ({prof_frame_ms:.4f} ms per telemetry frame vs {l50:.4f} ms p50), so shares "
+                           "hold and per-launch times are upper bounds")
+
+    # ---- e2e through the C-ABI with host buffers -------------------------------------
+    import ctypes as C
+    lib = fg.lib()
+    dp = C.POINTER(C.c_double)
     pin_s, host_note = host_slope_ring(stream_host, torch)
     pin_a = torch.zeros(d["A"], dtype=torch.float64).pin_memory()
     pin_rho = torch.zeros(d["iters"], dtype=torch.float64).pin_memory()
-    lib = fg.lib()
-    import ctypes as C
-    dp = C.POINTER(C.c_double)
-    nr = (C.c_int * 1)()
-    e2e_ms = []
-    # real-time hygiene of an AO host loop: no garbage collection inside the frame loop
-    import gc
-    gc_was = gc.isenabled()
-    gc.disable()
-    s_ptrs = [C.cast(pin_s[f].data_ptr(), dp) for f in range(F)]  # argument marshalling outside the timing
-    a_ptr, r_ptr, step_fn, h = C.cast(pin_a.data_ptr(), dp), C.cast(pin_rho.data_ptr(), dp), lib.fewha_gpu_step, rec._h
-    for k in range(max(args.warmup, 3) + min(K, 300)):
-        sp = s_ptrs[k % F]
-        flush.zero_()
+    a_ptr, r_ptr = C.cast(pin_a.data_ptr(), dp), C.cast(pin_rho.data_ptr(), dp)
+    NE = max(1000, min(K, 5000))
+    warm_e = max(args.warmup, 3)
+    e2e_ms = e2e_loop(rec, lib, [C.cast(pin_s[f].data_ptr(), dp) for f in range(F)], a_ptr, r_ptr, NE, warm_e,
+                      flush, dev, torch)
+    # the reference's calling convention: slopes in an ordinary (pageable) vector, a^(1) into one
+    page_s = np.ascontiguousarray(stream_host.copy())
+    page_a, page_r = np.zeros(d["A"]), np.zeros(d["iters"])
+    e2e_pg = e2e_loop(rec, lib, [page_s[f].ctypes.data_as(dp) for f in range(F)], page_a.ctypes.data_as(dp),
+                      page_r.ctypes.data_as(dp), NE, warm_e, flush, dev, torch)
+    e_mean, e_pg_mean, e50, e99, g50, g99 = rc.max_over_ranks(
+        [float(np.mean(e2e_ms)), float(np.mean(e2e_pg)), float(np.percentile(e2e_ms, 50)),
+         float(np.percentile(e2e_ms, 99)), float(np.percentile(e2e_pg, 50)), float(np.percentile(e2e_pg, 99))],
+        device=dev)
+    e2e_val = 1000.0 / e_mean if shard else rc.aggregate_throughput(1, e_mean)
+    e2e_pg_val = 1000.0 / e_pg_mean if shard else rc.aggregate_throughput(1, e_pg_mean)
+
+    # ---- the north-star per-WFS split at N > 1 (always reported beside the replicas) ---
+    shard_info = None
+    if world > 1 and not shard:
+        from paper_2009_00946_b200.replicas import shard_frame
+        rs = fg.Reconstructor(args.preset, precision=args.precision, batch=1, device=local)
+        wfs = shard_frame(rs, rc)
+        rs.build_preconditioner()
+        rs.set_stream(st.cuda_stream)
+        shared = torch.from_numpy(slope_stream(rs, args.preset, F, seed=1)).to(dev)  # one common frame stream
+        for k in range(5):
+            rs.load_slopes_device(shared[k % F].data_ptr())
+            rs.step_device(None)
+        rs.sync()
+        rc.barrier()
+        KS = max(K, 200)
+        s0 = [torch.cuda.Event(enable_timing=True) for _ in range(KS)]
+        s1 = [torch.cuda.Event(enable_timing=True) for _ in range(KS)]
+        for k in range(KS):
+            rs.load_slopes_device(shared[k % F].data_ptr())
+            flush.zero_()
+            s0[k].record(st)
+            rs.step_device(None)
+            s1[k].record(st)
         torch.cuda.synchronize(dev)
-        t0 = time.perf_counter()
-        code = step_fn(h, sp, None, a_ptr, r_ptr, nr)
-        t1 = time.perf_counter()
-        rec._chk(code)
-        if k >= max(args.warmup, 3):
-            e2e_ms.append((t1 - t0) * 1000.0)
-    if gc_was:
-        gc.enable()
-    e2e_ms = np.array(e2e_ms)
-    (e2e_mean,) = rc.max_over_ranks([float(np.mean(e2e_ms))], device=dev)
-    e2e_val = 1000.0 / e2e_mean if shard else rc.aggregate_throughput(1, e2e_mean)
+        rs.sync()
+        sms = np.array([x.elapsed_time(y) for x, y in zip(s0, s1)])
+        sp50, sp99, smean = rc.max_over_ranks([float(np.percentile(sms, 50)), float(np.percentile(sms, 99)),
+                                               float(sms.mean())], device=dev)
+        shard_info = {"world": world, "rank0_wfs": list(wfs), "frames": KS, "p50_ms": round(sp50, 5),
+                      "p99_ms": round(sp99, 5), "recon_per_s": round(1000.0 / smean, 1),
+                      "single_gpu_p50_ms": round(l50, 5), "p99_vs_single_gpu": round(sp99 / l99, 3),
+                      "kept": bool(sp99 < l99), "exchange": "ncclAllReduce of the partial adjoint layer sums, "
+                                                          "5 per frame, captured in the frame graph",
+                      "note": "one instance's frame split by WFS over all ranks (SURVEY 8e); max over ranks"}
+        rs.close()
 
     # ---- batch-64 throughput (HBM-bound regime) ----------------
     batch_info = None
@@ -430,12 +568,10 @@ def run_ours(args):
                 st.wait_event(ev)
             e1.record(st)
             torch.cuda.synchronize(dev)
-            prof_b = {}
-            if parts == 1:  # per-kernel HBM roofline in the regime where the working set exceeds L2
+            prof_b = None
+            if parts == 1:  # per-function HBM roofline where the working set exceeds L2
                 engs[0][0].set_stream(st.cuda_stream)
-                for _ in range(3):
-                    for kind, t in engs[0][0].profile_step():
-                        prof_b.setdefault(kind, []).append(t)
+                prof_b, _ = graph_function_profile(engs[0][0], 3, lambda f: None, d, b, batch=B)
             for r_, _, _ in engs:
                 r_.sync()
                 r_.close()
@@ -444,16 +580,8 @@ def run_ours(args):
         one, prof_b = time_split(1)
         two, _ = time_split(2)
         bms = min(one, two)
-        tot_b = sum(sum(v) for v in prof_b.values())
-        dom_b = max(prof_b, key=lambda k: sum(prof_b[k]))
-        dms_b = float(np.mean(prof_b[dom_b]))
-        ach_b = kernel_bytes(dom_b, d, b) * B / (dms_b / 1000.0) / 1e9
-        roof_b = {"bound": "hbm", "kernel": dom_b, "achieved": round(ach_b, 1), "peak": peak, "unit": "GB/s",
-                  "frac": round(ach_b / peak, 4), "launch_ms": round(dms_b, 4),
-                  "bytes_per_launch": kernel_bytes(dom_b, d, b) * B,
-                  "share_of_step": round(sum(prof_b[dom_b]) / tot_b, 3),
-                  "kernel_fracs": {k: round(kernel_bytes(k, d, b) * B / (float(np.mean(v)) / 1000.0) / 1e9 / peak, 4)
-                                   for k, v in sorted(prof_b.items(), key=lambda kv: -sum(kv[1]))}}
+        roof_b = roofline_object(prof_b, peak, peak_kind, f"fp{args.precision}_b64",
+                                 "event-record nodes of the 64-instance frame graph (3 frames, working set > L2)")
         batch_info = {"batch": B, "ms_per_step": round(bms, 4), "recon_per_s": round(B * 1000.0 / bms, 1),
                       "roofline_frac_frame_model": round(fb / (bms / 1000.0) / 1e9 / peak, 4),
                       "engines": 1 if one <= two else 2,
@@ -479,7 +607,7 @@ def run_ours(args):
                 rx.load_slopes_device(sx[k % 8].data_ptr())
                 rx.step_device(None)
             rx.sync()
-            KC = min(K, 300)
+            KC = 1000
             cs = [torch.cuda.Event(enable_timing=True) for _ in range(KC)]
             ce = [torch.cuda.Event(enable_timing=True) for _ in range(KC)]
             for k in range(KC):
@@ -511,9 +639,11 @@ def run_ours(args):
             us, thr = cpu_reference_time(args.preset, stream_host, frames, threads)
             cms = us / 1000.0
             cpu = {"value": round(1000.0 / float(np.mean(cms)), 3), "unit": UNIT, "cores": thr, "kind": "reference",
-                   "sample": f"{frames} frames of the reference Reconstructor::step (oracle/_ref, L=M shadow preset) on this slope stream, "
-                             f"{thr} pool threads (min(max(L,W), nproc)), {os.cpu_count()} host cpus; "
-                             f"p50 {np.percentile(cms, 50):.2f} ms p99 {np.percentile(cms, 99):.2f} ms"}
+                   "cpu_model": cpu_model(), "nproc": os.cpu_count(),
+                   "sample": f"{frames} frames of the reference Reconstructor::step (oracle/_ref, L=M shadow preset) "
+                             f"on this slope stream, {thr} pool threads (min(max(L,W), nproc)), {os.cpu_count()} host "
+                             f"cpus ({cpu_model()}); p50 {np.percentile(cms, 50):.2f} ms p99 "
+                             f"{np.percentile(cms, 99):.2f} ms"}
 
     if rank == 0:
         fb = frame_bytes(d, b)
@@ -530,21 +660,23 @@ def run_ours(args):
                        "n_act": d["A"], "l2": "flushed (256 MiB write) before every timed frame",
                        "parallelism": (f"wfs-shard x{world} (rank 0 owns WFS {shard_wfs})" if shard
                                        else f"replicas x{world}")},
-            "frame_roofline": {"bytes_per_frame": fb, "achieved_gbs": round(fb / (p50 / 1000.0) / 1e9, 2),
-                               "frac_at_p50": round(fb / (p50 / 1000.0) / 1e9 / peak, 5),
+            "latency": latency,
+            "frame_roofline": {"bytes_per_frame": fb, "achieved_gbs": round(fb / (l50 / 1000.0) / 1e9, 2),
+                               "frac_at_p50": round(fb / (l50 / 1000.0) / 1e9 / peak, 5),
                                "roofline_us": round(fb / (peak * 1e9) * 1e6, 3)},
-            "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 2), "peak": peak,
-                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                         "bytes_per_launch": dom_bytes, "launch_ms": round(dom_ms, 5),
-                         "share_of_frame": round(share[dom], 3), "peak_source": peak_kind,
-                         "kernel_shares": {k: round(v, 3) for k, v in sorted(share.items(), key=lambda x: -x[1])}},
+            "roofline": roof,
             "e2e": {"value": round(e2e_val, 3), "unit": UNIT, "h2d_bytes_per_step": S * 8, "host_buffers": host_note,
-                    "d2h_bytes_per_step": d["A"] * 8 + d["iters"] * 8 + 8,
-                    "p50_ms": round(float(np.percentile(e2e_ms, 50)), 5),
-                    "p99_ms": round(float(np.percentile(e2e_ms, 99)), 5)},
+                    "d2h_bytes_per_step": d["A"] * 8 + d["iters"] * 8 + 8, "frames": NE,
+                    "p50_ms": round(e50, 5), "p99_ms": round(e99, 5),
+                    "pageable": {"value": round(e2e_pg_val, 3), "unit": UNIT, "p50_ms": round(g50, 5),
+                                 "p99_ms": round(g99, 5),
+                                 "host_buffers": "ordinary numpy arrays (pageable), as the reference's "
+                                                 "span<const double> over a std::vector"}},
             "gpu_launches": launches * K,
             "clocks": clk.summary(),
         }
+        if shard_info:
+            line["shard"] = shard_info
         if cpu:
             line["cpu_baseline"] = cpu
         if batch_info:

@@ -189,6 +189,10 @@ typedef struct {
 } fewha_gpu_telemetry_t;
 int fewha_gpu_enable_telemetry(fewha_gpu_t h, int on);
 int fewha_gpu_last_telemetry(fewha_gpu_t h, fewha_gpu_telemetry_t* out);
+/* Per-launch device times (ms) and kernel kinds (as fewha_gpu_profile_step) of
+ * the last graph frame, from the same event nodes.  Returns the launch count
+ * (0: telemetry off or no frame since), < 0 on error. */
+int fewha_gpu_last_launch_times(fewha_gpu_t h, float* ms, int* kinds, int max);
 
 /* --- per-WFS sharding (the north star's multi-GPU split) -------
  * Shard `rank` of `world` owns a contiguous WFS range, balanced by wavefront

@@ -36,7 +36,7 @@ EXPORTS = (
     "fewha_gpu_propagate", "fewha_gpu_propagate_transpose", "fewha_gpu_sh", "fewha_gpu_sh_transpose",
     "fewha_gpu_forward_slopes", "fewha_gpu_shard_range", "fewha_gpu_nccl_unique_id", "fewha_gpu_shard",
     "fewha_gpu_shard_wfs", "fewha_gpu_group_step_device", "fewha_gpu_enable_telemetry", "fewha_gpu_last_telemetry",
-    "fewha_gpu_wfs_operator", "fewha_gpu_plan_info",
+    "fewha_gpu_wfs_operator", "fewha_gpu_plan_info", "fewha_gpu_last_launch_times",
 )
 
 
@@ -139,6 +139,7 @@ def lib() -> C.CDLL:
         L.fewha_gpu_forward_slopes.argtypes = [vp, dp, dp, dp, C.c_int]
         L.fewha_gpu_wfs_operator.argtypes = [vp, C.c_int, dp, dp, dp, C.c_int]
         L.fewha_gpu_plan_info.argtypes = [vp, C.POINTER(_Plan)]
+        L.fewha_gpu_last_launch_times.argtypes = [vp, C.POINTER(C.c_float), C.POINTER(C.c_int), C.c_int]
         ip = C.POINTER(C.c_int)
         L.fewha_gpu_shard_range.argtypes = [C.c_char_p, C.c_int, C.c_int, ip, ip]
         L.fewha_gpu_nccl_unique_id.argtypes = [C.c_char_p]
@@ -398,6 +399,15 @@ class Reconstructor:
         out["valid"] = bool(out["valid"])
         out["rho"] = getattr(self, "last_rho", None)
         return out
+
+    def last_launch_times(self):
+        """[(kind, ms), ...] of the last graph frame (telemetry event nodes)."""
+        ms = (C.c_float * 256)()
+        kinds = (C.c_int * 256)()
+        n = self._L.fewha_gpu_last_launch_times(self._h, ms, kinds, 256)
+        if n < 0:
+            self._chk(-n)
+        return [(self.KERNEL_KINDS[kinds[i]], float(ms[i])) for i in range(n)]
 
     def shard(self, rank: int, world: int, nccl_id: bytes | None = None):
         """Own the WFS of shard rank/world.  nccl_id: multi-process

@@ -264,6 +264,13 @@ int fewha_gpu_last_telemetry(fewha_gpu_t h, fewha_gpu_telemetry_t* out) {
     })
 }
 
+int fewha_gpu_last_launch_times(fewha_gpu_t h, float* ms, int* kinds, int max) {
+    if (!h || !ms || !kinds) return -FEWHA_ARG;
+    int n = 0;
+    const int rc = guard(h->err, [&] { n = h->eng->last_launch_times(ms, kinds, max); });
+    return rc ? -rc : n;
+}
+
 // ---- per-WFS sharding ----
 int fewha_gpu_shard_range(const char* path, int rank, int world, int* wfs_begin, int* wfs_end) {
     if (!path) return FEWHA_ARG;

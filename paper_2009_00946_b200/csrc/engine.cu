@@ -1776,6 +1776,21 @@ StepTelemetry Engine::last_telemetry() {
     return t;
 }
 
+// Per-launch device times of the last graph frame from its telemetry event nodes
+// (kinds as profile_step); 0 when telemetry is off or no frame ran since.
+int Engine::last_launch_times(float* ms, int* kinds, int max) {
+    auto& P = *p_;
+    if (!P.telem_pending) return 0;
+    CK(cudaSetDevice(P.device));
+    CK(cudaEventSynchronize(P.tev[P.tkind.size()]));
+    int n = 0;
+    for (size_t i = 0; i < P.tkind.size() && n < max; ++i, ++n) {
+        CK(cudaEventElapsedTime(&ms[n], P.tev[i], P.tev[i + 1]));
+        kinds[n] = P.tkind[i];
+    }
+    return n;
+}
+
 void Engine::load_slopes(const void* src, bool on_device) {
     auto& P = *p_;
     CK(cudaSetDevice(P.device));

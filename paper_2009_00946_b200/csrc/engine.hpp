@@ -63,6 +63,7 @@ public:
     void sync_check();
     void enable_telemetry(bool on);
     StepTelemetry last_telemetry();
+    int last_launch_times(float* ms, int* kinds, int max);
     int launches_per_step() const;
     PlanInfo plan_info() const;
     int profile_step(float* ms, int* kinds, int max);

@@ -151,3 +151,24 @@ def test_bench_models_cover_every_kernel_kind():
     for kind in fg.Reconstructor.KERNEL_KINDS:
         assert bench.kernel_bytes(kind, d, 8) > 0, kind
     assert abs(bench.frame_bytes(d, 8) - 71.76e6) / 71.76e6 < 1e-3
+
+
+def test_bench_roofline_names_the_dominant_function():
+    """The roofline object sums a kernel function's launch kinds (k_inv_cluster =
+    inv_pcg0 + inv_pcg + inv_fit) before taking the largest share, and every kind
+    maps to a kernel function."""
+    import importlib.util
+
+    import paper_2009_00946_b200 as fg
+
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    for kind in fg.Reconstructor.KERNEL_KINDS:
+        assert kind in bench.FUNC, kind
+    prof = {"k_inv_cluster": {"share": 0.31, "achieved_gbs": 578.0, "bytes_per_launch": 1.1e7, "launch_ms": 0.019,
+                              "launches_per_frame": 5},
+            "k_gather": {"share": 0.21, "achieved_gbs": 116.0, "bytes_per_launch": 1.5e6, "launch_ms": 0.013,
+                         "launches_per_frame": 5}}
+    r = bench.roofline_object(prof, 6548.2, "measured", "fp64", "test")
+    assert r["kernel"] == "k_inv_cluster" and abs(r["frac"] - 578.0 / 6548.2) < 1e-4
