@@ -109,6 +109,7 @@ int fewha_gpu_step(fewha_gpu_t h, const double* slopes, double* coeffs_out, doub
                    int* n_rho);
 /* ReconstructorState::reset (reconstructor.hpp:81-91) on every instance */
 int fewha_gpu_reset(fewha_gpu_t h);
+/* get_state: any vector pointer of *st may be NULL (not copied); scalars always are */
 int fewha_gpu_get_state(fewha_gpu_t h, int instance, fewha_gpu_state_t* st);
 int fewha_gpu_set_state(fewha_gpu_t h, int instance, const fewha_gpu_state_t* st);
 

@@ -1669,13 +1669,14 @@ void Engine::get_state(int inst, double* c, double* b, double* r, double* p, dou
         using T = std::remove_pointer_t<decltype(w.bf.c)>;
         const cudaStream_t st = P.s();
         CK(cudaStreamSynchronize(st));
-        d2h_coeff<T>(c, w.bf.c + inst * n, P.plan.perm, 1, st);
-        d2h_coeff<T>(b, w.bf.b + inst * n, P.plan.perm, 1, st);
-        d2h_coeff<T>(r, w.bf.r + inst * n, P.plan.perm, 1, st);
-        d2h_coeff<T>(p, w.bf.p + inst * n, P.plan.perm, 1, st);
-        d2h_coeff<T>(q, w.bf.q + inst * n, P.plan.perm, 1, st);
-        d2h_conv<T>(a_prev2, w.bf.a_prev2 + inst * A, A, st);
-        d2h_conv<T>(a_prev, w.bf.a_prev + inst * A, A, st);
+        // any output may be null (skipped): e.g. the scalars alone after every step
+        if (c) d2h_coeff<T>(c, w.bf.c + inst * n, P.plan.perm, 1, st);
+        if (b) d2h_coeff<T>(b, w.bf.b + inst * n, P.plan.perm, 1, st);
+        if (r) d2h_coeff<T>(r, w.bf.r + inst * n, P.plan.perm, 1, st);
+        if (p) d2h_coeff<T>(p, w.bf.p + inst * n, P.plan.perm, 1, st);
+        if (q) d2h_coeff<T>(q, w.bf.q + inst * n, P.plan.perm, 1, st);
+        if (a_prev2) d2h_conv<T>(a_prev2, w.bf.a_prev2 + inst * A, A, st);
+        if (a_prev) d2h_conv<T>(a_prev, w.bf.a_prev + inst * A, A, st);
         Carry cr;
         CK(cudaMemcpyAsync(&cr, w.bf.carry + inst * (P.gp.iters + 1), sizeof(Carry), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));

@@ -172,3 +172,16 @@ def test_bench_roofline_names_the_dominant_function():
                          "launches_per_frame": 5}}
     r = bench.roofline_object(prof, 6548.2, "measured", "fp64", "test")
     assert r["kernel"] == "k_inv_cluster" and abs(r["frac"] - 578.0 / 6548.2) < 1e-4
+
+
+@pytest.mark.skipif(not os.path.isdir("/root/reference/proj/include"), reason="reference headers absent")
+def test_cpp_dropin_builds_against_the_reference_headers():
+    """include/fewha_gpu_reconstructor.hpp compiles against the unmodified reference
+    headers and links the in-tree library (tests/cpp/Makefile); the GPU test runs it."""
+    import subprocess
+
+    out = subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp")], capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout + out.stderr
+    binp = os.path.join(ROOT, "tests", "cpp", "_build", "test_dropin")
+    ldd = subprocess.run(["ldd", binp], capture_output=True, text=True).stdout
+    assert "libfewha_gpu.so" in ldd and "not found" not in ldd.split("libfewha_gpu.so")[1].splitlines()[0]
