@@ -195,6 +195,32 @@ int fewha_gpu_last_telemetry(fewha_gpu_t h, fewha_gpu_telemetry_t* out);
  * (0: telemetry off or no frame since), < 0 on error. */
 int fewha_gpu_last_launch_times(fewha_gpu_t h, float* ms, int* kinds, int max);
 
+/* --- closed-loop simulation harness on the device -----------
+ * The reference's simulation layer (simulation.hpp) restated in CUDA, so long
+ * closed loops run with no per-frame host transfer: GaussianStream (mt19937_64 +
+ * Box-Muller, :40-58, one warp per stream), generate_atmosphere (:76-127, inverse
+ * 2-D DFT on the device), truth_at_step (:131-158), synthesize_measurements
+ * (:164-212: the device forward model + the noise stream), evaluate_quality
+ * (:228-305).  Quality records: [0] field_rms, [1] layer_rel_err (NaN without an
+ * L = M pairing), [2..] rms_per_dir; their length is fewha_gpu_sim_quality_size. */
+int fewha_gpu_sim_quality_size(fewha_gpu_t h);
+/* GaussianStream(seed): `count` (even) standard normals drawn on `device` (no handle;
+ * errors via fewha_gpu_create_error) */
+int fewha_gpu_sim_gauss(int device, unsigned long long seed, int count, double* out);
+/* truth_at_step(generate_atmosphere(g, seed), g, step) -> layers [n] (nodal) */
+int fewha_gpu_sim_atmosphere(fewha_gpu_t h, unsigned long long seed, int step, double* layers);
+/* synthesize_measurements(layers, a or none, g, noise_seed) -> meas [S] */
+int fewha_gpu_sim_synthesize(fewha_gpu_t h, const double* layers, const double* a, unsigned long long noise_seed,
+                             double* meas);
+/* evaluate_quality(layers, a, g) -> rec [fewha_gpu_sim_quality_size] */
+int fewha_gpu_sim_quality(fewha_gpu_t h, const double* layers, const double* a, double* rec);
+/* run_closed_loop(g, n_steps, {atmosphere_seed, noise_seed}) (simulation.hpp:321-345) on
+ * this handle (batch 1; its state is reset first, as a fresh Reconstructor): rec
+ * [n_steps][quality size], rho [n_steps][iters] (may be NULL), unc_final {uncorrected
+ * field RMS of the last step's truth, final field RMS} (may be NULL). */
+int fewha_gpu_run_closed_loop(fewha_gpu_t h, int n_steps, unsigned long long atmosphere_seed,
+                              unsigned long long noise_seed, double* rec, double* rho, double* unc_final);
+
 /* --- per-WFS sharding (the north star's multi-GPU split) -------
  * Shard `rank` of `world` owns a contiguous WFS range, balanced by wavefront
  * nodes: its WFS kernels (Gamma, C^-1, P) run only those WFS and its adjoint

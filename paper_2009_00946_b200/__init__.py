@@ -37,6 +37,8 @@ EXPORTS = (
     "fewha_gpu_forward_slopes", "fewha_gpu_shard_range", "fewha_gpu_nccl_unique_id", "fewha_gpu_shard",
     "fewha_gpu_shard_wfs", "fewha_gpu_group_step_device", "fewha_gpu_enable_telemetry", "fewha_gpu_last_telemetry",
     "fewha_gpu_wfs_operator", "fewha_gpu_plan_info", "fewha_gpu_last_launch_times",
+    "fewha_gpu_sim_quality_size", "fewha_gpu_sim_atmosphere", "fewha_gpu_sim_synthesize", "fewha_gpu_sim_quality",
+    "fewha_gpu_run_closed_loop", "fewha_gpu_sim_gauss",
 )
 
 
@@ -140,6 +142,13 @@ def lib() -> C.CDLL:
         L.fewha_gpu_wfs_operator.argtypes = [vp, C.c_int, dp, dp, dp, C.c_int]
         L.fewha_gpu_plan_info.argtypes = [vp, C.POINTER(_Plan)]
         L.fewha_gpu_last_launch_times.argtypes = [vp, C.POINTER(C.c_float), C.POINTER(C.c_int), C.c_int]
+        u64 = C.c_ulonglong
+        L.fewha_gpu_sim_quality_size.argtypes = [vp]
+        L.fewha_gpu_sim_gauss.argtypes = [C.c_int, u64, C.c_int, dp]
+        L.fewha_gpu_sim_atmosphere.argtypes = [vp, u64, C.c_int, dp]
+        L.fewha_gpu_sim_synthesize.argtypes = [vp, dp, dp, u64, dp]
+        L.fewha_gpu_sim_quality.argtypes = [vp, dp, dp, dp]
+        L.fewha_gpu_run_closed_loop.argtypes = [vp, C.c_int, u64, u64, dp, dp, dp]
         ip = C.POINTER(C.c_int)
         L.fewha_gpu_shard_range.argtypes = [C.c_char_p, C.c_int, C.c_int, ip, ip]
         L.fewha_gpu_nccl_unique_id.argtypes = [C.c_char_p]

@@ -271,6 +271,44 @@ int fewha_gpu_last_launch_times(fewha_gpu_t h, float* ms, int* kinds, int max) {
     return rc ? -rc : n;
 }
 
+// ---- closed-loop simulation harness on the device ----
+int fewha_gpu_sim_gauss(int device, unsigned long long seed, int count, double* out) {
+    if (!out || count < 0) return FEWHA_ARG;
+    return guard(g_create_error, [&] { fewha_gpu::sim_gauss_stream(device, seed, count, out); });
+}
+int fewha_gpu_sim_quality_size(fewha_gpu_t h) {
+    if (!h) return -FEWHA_ARG;
+    int n = 0;
+    const int rc = guard(h->err, [&] { n = h->eng->sim_quality_size(); });
+    return rc ? -rc : n;
+}
+int fewha_gpu_sim_atmosphere(fewha_gpu_t h, unsigned long long seed, int step, double* layers) {
+    H_GUARD({
+        if (!layers || step < 0) throw ArgError("sim_atmosphere: null output or negative step");
+        h->eng->sim_atmosphere(seed, step, layers);
+    })
+}
+int fewha_gpu_sim_synthesize(fewha_gpu_t h, const double* layers, const double* a, unsigned long long noise_seed,
+                             double* meas) {
+    H_GUARD({
+        if (!layers || !meas) throw ArgError("sim_synthesize: null argument");
+        h->eng->sim_synthesize(layers, a, noise_seed, meas);
+    })
+}
+int fewha_gpu_sim_quality(fewha_gpu_t h, const double* layers, const double* a, double* rec) {
+    H_GUARD({
+        if (!layers || !a || !rec) throw ArgError("sim_quality: null argument");
+        h->eng->sim_quality(layers, a, rec);
+    })
+}
+int fewha_gpu_run_closed_loop(fewha_gpu_t h, int n_steps, unsigned long long atmosphere_seed,
+                              unsigned long long noise_seed, double* rec, double* rho, double* unc_final) {
+    H_GUARD({
+        if (!rec) throw ArgError("run_closed_loop: null record buffer");
+        h->eng->run_closed_loop(n_steps, atmosphere_seed, noise_seed, rec, rho, unc_final);
+    })
+}
+
 // ---- per-WFS sharding ----
 int fewha_gpu_shard_range(const char* path, int rank, int world, int* wfs_begin, int* wfs_end) {
     if (!path) return FEWHA_ARG;

@@ -20,6 +20,7 @@
 #include "clayout.hpp"
 #include "launch.hpp"
 #include "nccl_dl.hpp"
+#include "sim_kernels.cuh"
 
 namespace fewha_gpu {
 
@@ -910,6 +911,7 @@ struct EngineImpl {
         return g2;
     }
     std::vector<double> precond;
+    std::unique_ptr<struct SimState> sim;  // closed-loop simulation harness, built on first use
     void* jac = nullptr;
     void* jinv = nullptr;  // 1/J
     // state (precision T) -- one of the two is used
@@ -2085,6 +2087,415 @@ void Engine::sh_transpose(const double* meas, double* wf, int count) {
             d2h_conv<T>(wf, w.bf.psi, static_cast<size_t>(P.gp.Nw) * count, P.stream);
         });
     })
+}
+
+
+// ---------------------------------------------------------------------------
+// Closed-loop simulation harness on the device (reference
+// simulation.hpp:40-345).  Host code only builds tables and issues launches:
+// a run_closed_loop moves no data between host and device per frame.
+// ---------------------------------------------------------------------------
+namespace {
+std::uint64_t splitmix64(std::uint64_t x) {  // simulation.hpp:31-36
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+constexpr double kPi = 3.14159265358979323846;
+}  // namespace
+
+struct SimState {
+    DevFree fr;
+    int n = 0, S = 0, A = 0, L = 0, M = 0, pairs = 0, n_dir = 0, nodes = 0;
+    bool paired = false, wind = false;
+    sim::AtmParams ap{};
+    sim::QualParams qp{};
+    sim::LerrParams lp{};
+    std::vector<std::pair<double, double>> wind_sp;  // per layer (row, column) node shift per step
+    double *truth = nullptr, *layers = nullptr, *cplx = nullptr, *cplx2 = nullptr, *z_atm = nullptr;
+    double *noise = nullptr, *dm = nullptr, *zero_dm = nullptr, *var = nullptr, *part = nullptr;
+    int *nx = nullptr, *ny = nullptr;
+    double* sig = nullptr;
+    unsigned long long* seeds = nullptr;  // device seed slots
+    int seed_cap = 0;
+    double* z = nullptr;                   // noise normals [chunk][2 pairs]
+    int z_cap = 0;
+    template <typename T>
+    T* alloc(size_t k) {
+        T* p = dalloc<T>(k);
+        fr.add(p);
+        return p;
+    }
+};
+
+namespace {
+SimState& sim_state(EngineImpl& P) {
+    if (P.sim) return *P.sim;
+    CK(cudaSetDevice(P.device));
+    auto st = std::make_unique<SimState>();
+    SimState& S = *st;
+    const Geometry& g = P.g;
+    S.n = P.gp.n;
+    S.S = P.gp.S;
+    S.A = P.gp.A;
+    S.L = P.gp.L;
+    S.M = P.gp.M;
+    S.paired = !g.projection && g.layers.size() == g.dms.size();
+    // atmosphere: per layer side, nodal offset, normals offset, period, target variance
+    S.ap.L = S.L;
+    S.ap.kappa0 = 2.0 * kPi / g.outer_scale;
+    for (int l = 0; l < S.L; ++l) {
+        const int nl = g.layers[l].side();
+        S.ap.lay[l] = {nl, P.gp.coff[l], 2 * P.gp.coff[l], g.layers[l].extent / (nl - 1) * nl,
+                       g.layers[l].strength * g.truth_strength};
+    }
+    S.wind = !g.wind.empty();
+    for (int l = 0; S.wind && l < S.L; ++l) {
+        const double sp = g.layers[l].extent / (g.layers[l].side() - 1);
+        S.wind_sp.push_back({g.wind[l].second / sp, g.wind[l].first / sp});
+    }
+    S.truth = S.alloc<double>(S.n);
+    S.layers = S.alloc<double>(S.n);
+    S.cplx = S.alloc<double>(2 * static_cast<size_t>(S.n));
+    S.cplx2 = S.alloc<double>(2 * static_cast<size_t>(S.n));
+    S.z_atm = S.alloc<double>(2 * static_cast<size_t>(S.n));
+    S.noise = S.alloc<double>(S.S);
+    S.dm = S.alloc<double>(std::max(S.A, 1));
+    S.zero_dm = S.alloc<double>(std::max(S.A, 1));
+    // noise scatter table: active subapertures, WFS then row-major (simulation.hpp:196-207)
+    std::vector<int> ix, iy;
+    std::vector<double> sg;
+    for (size_t w = 0; w < g.wfs.size(); ++w) {
+        const int ns = g.wfs[w].n_subap;
+        const double sigma = std::sqrt(g.wfs[w].noise_variance);
+        for (int k = 0; k < ns * ns; ++k)
+            if (g.wfs[w].mask[static_cast<size_t>(k)]) {
+                ix.push_back(P.gp.moff[w] + k);
+                iy.push_back(P.gp.moff[w] + ns * ns + k);
+                sg.push_back(sigma);
+            }
+    }
+    S.pairs = static_cast<int>(ix.size());
+    S.nx = S.alloc<int>(ix.size());
+    S.ny = S.alloc<int>(iy.size());
+    S.sig = S.alloc<double>(sg.size());
+    CK(cudaMemcpy(S.nx, ix.data(), ix.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(S.ny, iy.data(), iy.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(S.sig, sg.data(), sg.size() * sizeof(double), cudaMemcpyHostToDevice));
+    // quality: annular-pupil nodes of the finest WFS grid and per (direction, screen)
+    // stencil tables (evaluate_quality, simulation.hpp:228-269)
+    int n_sub = 0;
+    for (const auto& w : g.wfs) n_sub = std::max(n_sub, w.n_subap);
+    const int nq = n_sub + 1;
+    const double d = g.diameter / (nq - 1), r_out = g.r_out(), r_in = g.r_in();
+    std::vector<int> nodes;
+    for (int i = 0; i < nq; ++i)
+        for (int j = 0; j < nq; ++j) {
+            const double x = -r_out + j * d, y = -r_out + i * d, r2 = x * x + y * y;
+            if (r2 <= r_out * r_out * (1.0 + 1e-12) && r2 >= r_in * r_in * (1.0 - 1e-12)) nodes.push_back(i * nq + j);
+        }
+    std::vector<std::pair<double, double>> dirs;  // EvaluationConfig::directions (geometry.hpp:122-133)
+    const int nps = g.eval_n_per_side;
+    for (int i = 0; i < nps; ++i)
+        for (int j = 0; j < nps; ++j) {
+            const double fy = nps == 1 ? 0.0 : -1.0 + 2.0 * i / (nps - 1);
+            const double fx = nps == 1 ? 0.0 : -1.0 + 2.0 * j / (nps - 1);
+            dirs.push_back({fx * g.eval_half_width, fy * g.eval_half_width});
+        }
+    S.n_dir = static_cast<int>(dirs.size());
+    S.nodes = static_cast<int>(nodes.size());
+    const int NS = S.L + S.M;
+    std::vector<int> tix(static_cast<size_t>(S.n_dir) * NS * 2 * nq);
+    std::vector<double> tw(tix.size());
+    for (int dd = 0; dd < S.n_dir; ++dd)
+        for (int sc = 0; sc < NS; ++sc) {
+            const bool lay = sc < S.L;
+            const int side = lay ? g.layers[sc].side() : g.dms[sc - S.L].n_act;
+            const double ext = lay ? g.layers[sc].extent : g.dms[sc - S.L].extent;
+            const double h = lay ? g.layers[sc].height : g.dms[sc - S.L].height;
+            for (int axis = 0; axis < 2; ++axis)
+                for (int k = 0; k < nq; ++k) {
+                    const double p = -r_out + k * d + (axis ? dirs[dd].second : dirs[dd].first) * h;
+                    const Stencil1 st1 = stencil1(side, ext, p);
+                    const size_t o = ((static_cast<size_t>(dd) * NS + sc) * 2 + axis) * nq + k;
+                    tix[o] = st1.idx;
+                    tw[o] = st1.f;
+                }
+        }
+    int* dnode = S.alloc<int>(nodes.size());
+    int* dtix = S.alloc<int>(tix.size());
+    double* dtw = S.alloc<double>(tw.size());
+    CK(cudaMemcpy(dnode, nodes.data(), nodes.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dtix, tix.data(), tix.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dtw, tw.data(), tw.size() * sizeof(double), cudaMemcpyHostToDevice));
+    S.qp.L = S.L;
+    S.qp.M = S.M;
+    S.qp.n = nq;
+    S.qp.n_nodes = S.nodes;
+    S.qp.n_dir = S.n_dir;
+    for (int l = 0; l < S.L; ++l) {
+        S.qp.side[l] = P.gp.side[l];
+        S.qp.loff[l] = P.gp.coff[l];
+    }
+    for (int m = 0; m < S.M; ++m) {
+        S.qp.nact[m] = P.gp.nact[m];
+        S.qp.aoff[m] = P.gp.aoff[m];
+    }
+    S.qp.node = dnode;
+    S.qp.tidx = dtix;
+    S.qp.tw = dtw;
+    S.var = S.alloc<double>(std::max(S.n_dir, 1));
+    S.part = S.alloc<double>(2 * static_cast<size_t>(std::max(S.L, 1)));
+    if (S.paired) {  // layer_rel_err tables: DM l on layer l's nodes with the layer extent
+        std::vector<int> li;
+        std::vector<double> lw;
+        S.lp.L = S.L;
+        for (int l = 0; l < S.L; ++l) {
+            const int nl = g.layers[l].side(), na = g.dms[l].n_act;
+            const double ext = g.layers[l].extent, dl = ext / (nl - 1);
+            S.lp.side[l] = nl;
+            S.lp.loff[l] = P.gp.coff[l];
+            S.lp.nact[l] = na;
+            S.lp.aoff[l] = P.gp.aoff[l];
+            S.lp.toff[l] = static_cast<int>(li.size());
+            for (int k = 0; k < nl; ++k) {
+                const Stencil1 st1 = stencil1(na, ext, -ext / 2.0 + k * dl);
+                li.push_back(st1.idx);
+                lw.push_back(st1.f);
+            }
+        }
+        int* dli = S.alloc<int>(li.size());
+        double* dlw = S.alloc<double>(lw.size());
+        CK(cudaMemcpy(dli, li.data(), li.size() * sizeof(int), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dlw, lw.data(), lw.size() * sizeof(double), cudaMemcpyHostToDevice));
+        S.lp.tidx = dli;
+        S.lp.tw = dlw;
+    }
+    CK(cudaFuncSetAttribute(sim::k_quality_dir, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(std::max<size_t>(S.nodes * sizeof(double), 1))));
+    CK(cudaDeviceSynchronize());
+    P.sim = std::move(st);
+    return *P.sim;
+}
+
+// normals of `streams` GaussianStreams (seeds on the host) -> S.z [stream][count]
+void sim_normals(EngineImpl& P, SimState& S, const std::vector<unsigned long long>& seeds, int count, double* out,
+                 cudaStream_t st) {
+    if (static_cast<int>(seeds.size()) > S.seed_cap) {
+        S.seed_cap = static_cast<int>(seeds.size());
+        S.seeds = S.alloc<unsigned long long>(seeds.size());
+    }
+    CK(cudaMemcpyAsync(S.seeds, seeds.data(), seeds.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice, st));
+    sim::k_gauss<<<static_cast<unsigned>(seeds.size()), 32, 0, st>>>(S.seeds, count, out, count);
+    CK(cudaGetLastError());
+    (void)P;
+}
+
+// generate_atmosphere(g, seed) -> S.truth
+void sim_atmosphere(EngineImpl& P, SimState& S, std::uint64_t seed, cudaStream_t st) {
+    int maxn = 0;
+    for (int l = 0; l < S.L; ++l) maxn = std::max(maxn, S.ap.lay[l].n);
+    // one stream per layer, 2 n^2 normals each, laid out at 2 * coff[l]
+    for (int l = 0; l < S.L; ++l) {
+        const std::vector<unsigned long long> sd{splitmix64(seed ^ (0x51a9e4c7ULL + static_cast<std::uint64_t>(l)))};
+        sim_normals(P, S, sd, 2 * S.ap.lay[l].n * S.ap.lay[l].n, S.z_atm + 2 * static_cast<size_t>(P.gp.coff[l]), st);
+        CK(cudaStreamSynchronize(st));  // the seed slot is reused by the next layer
+    }
+    sim::k_atm_spectrum<<<dim3(maxn, S.L), maxn, 0, st>>>(S.ap, S.z_atm, S.cplx);
+    sim::k_atm_dft<<<dim3(maxn, S.L), maxn, 0, st>>>(S.ap, S.cplx, S.cplx2, 0);
+    sim::k_atm_dft<<<dim3(maxn, S.L), maxn, 0, st>>>(S.ap, S.cplx2, S.cplx, 1);
+    sim::k_atm_finish<<<S.L, 1024, 0, st>>>(S.ap, S.cplx, S.truth);
+    CK(cudaGetLastError());
+}
+
+// truth_at_step(truth, g, step) -> out (the truth itself when there is no wind or step 0)
+const double* sim_truth_at_step(SimState& S, const double* base, int step, double* out, cudaStream_t st) {
+    if (!S.wind || step == 0) return base;
+    sim::FlowParams fp{};
+    fp.L = S.L;
+    int maxnn = 0;
+    for (int l = 0; l < S.L; ++l) {
+        fp.n[l] = S.ap.lay[l].n;
+        fp.off[l] = S.ap.lay[l].off;
+        fp.si[l] = S.wind_sp[static_cast<size_t>(l)].first * step;
+        fp.sj[l] = S.wind_sp[static_cast<size_t>(l)].second * step;
+        maxnn = std::max(maxnn, fp.n[l] * fp.n[l]);
+    }
+    sim::k_frozen_flow<<<dim3((maxnn + 255) / 256, S.L), 256, 0, st>>>(fp, base, out);
+    CK(cudaGetLastError());
+    return out;
+}
+
+// synthesize_measurements(layers, a, g, noise_seed): forward model + the frame's noise
+// (normals z of its stream, or none) -> meas (device)
+void sim_slopes(EngineImpl& P, SimState& S, const double* layers, const double* a, const double* z, double* meas,
+                cudaStream_t st) {
+    const double* noise = nullptr;
+    if (z) {
+        sim::k_noise_scatter<<<(S.pairs + 255) / 256, 256, 0, st>>>(S.nx, S.ny, S.sig, S.pairs, z, S.noise);
+        noise = S.noise;
+    }
+    const int sub = S.S / 2;
+    k_slopes<double><<<dim3((sub + 255) / 256, 1), 256, 0, st>>>(P.gp64, nullptr, layers, a, -1.0, noise, meas, 1);
+    CK(cudaGetLastError());
+}
+
+// evaluate_quality(layers, a, g) -> rec[0] field_rms, rec[1] layer_rel_err, rec[2..] rms_per_dir
+void sim_quality(SimState& S, const double* layers, const double* a, double* rec, cudaStream_t st) {
+    sim::k_quality_dir<<<S.n_dir, 512, S.nodes * sizeof(double), st>>>(S.qp, layers, a, S.var);
+    if (S.paired) sim::k_layer_err<<<S.L, 1024, 0, st>>>(S.lp, layers, a, S.part);
+    sim::k_quality_finish<<<1, 32, 0, st>>>(S.var, S.n_dir, S.part, S.L, S.paired ? 1 : 0, rec);
+    CK(cudaGetLastError());
+}
+
+// the engine's a^(-1) (state a_prev2, instance 0) as doubles
+const double* sim_dm(EngineImpl& P, SimState& S, cudaStream_t st) {
+    if (P.precision == 64) return P.sd.bf.a_prev2;
+    k_convert<float, double><<<(S.A + 255) / 256, 256, 0, st>>>(P.sf.bf.a_prev2, S.dm, static_cast<size_t>(S.A));
+    CK(cudaGetLastError());
+    return S.dm;
+}
+}  // namespace
+
+// A bare GaussianStream on the device (for known-answer tests of k_gauss).
+void sim_gauss_stream(int device, unsigned long long seed, int count, double* out) {
+    CK(cudaSetDevice(device));
+    unsigned long long* ds = dalloc<unsigned long long>(1);
+    double* dz = dalloc<double>(static_cast<size_t>(count));
+    CK(cudaMemcpy(ds, &seed, sizeof(seed), cudaMemcpyHostToDevice));
+    sim::k_gauss<<<1, 32>>>(ds, count, dz, count);
+    const cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) CK(cudaMemcpy(out, dz, sizeof(double) * count, cudaMemcpyDeviceToHost));
+    cudaFree(ds);
+    cudaFree(dz);
+    CK(e);
+}
+
+int Engine::sim_quality_size() {
+    return 2 + sim_state(*p_).n_dir;
+}
+
+void Engine::sim_atmosphere(unsigned long long seed, int step, double* layers_out) {
+    auto& P = *p_;
+    CK(cudaSetDevice(P.device));
+    SimState& S = sim_state(P);
+    const cudaStream_t st = P.stream;
+    fewha_gpu::sim_atmosphere(P, S, seed, st);
+    const double* l = sim_truth_at_step(S, S.truth, step, S.layers, st);
+    CK(cudaMemcpyAsync(layers_out, l, sizeof(double) * S.n, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+}
+
+void Engine::sim_synthesize(const double* layers, const double* a, unsigned long long noise_seed, double* meas) {
+    auto& P = *p_;
+    CK(cudaSetDevice(P.device));
+    SimState& S = sim_state(P);
+    const cudaStream_t st = P.stream;
+    CK(cudaMemcpyAsync(S.layers, layers, sizeof(double) * S.n, cudaMemcpyHostToDevice, st));
+    if (a) CK(cudaMemcpyAsync(S.dm, a, sizeof(double) * S.A, cudaMemcpyHostToDevice, st));
+    double* z = nullptr;
+    if (P.g.sim_noise) {
+        if (S.z_cap < 1) {
+            S.z = S.alloc<double>(2 * static_cast<size_t>(S.pairs));
+            S.z_cap = 1;
+        }
+        sim_normals(P, S, {splitmix64(noise_seed ^ 0x6e0f7a3dULL)}, 2 * S.pairs, S.z, st);
+        z = S.z;
+    }
+    Work<double>& w = P.pd.count ? P.pd : P.od;
+    if (w.count < 1) w.alloc(P.gp64, 1, P.fr, false);
+    sim_slopes(P, S, S.layers, a ? S.dm : nullptr, z, w.meas2, st);
+    CK(cudaMemcpyAsync(meas, w.meas2, sizeof(double) * S.S, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+}
+
+void Engine::sim_quality(const double* layers, const double* a, double* rec) {
+    auto& P = *p_;
+    CK(cudaSetDevice(P.device));
+    SimState& S = sim_state(P);
+    const cudaStream_t st = P.stream;
+    CK(cudaMemcpyAsync(S.layers, layers, sizeof(double) * S.n, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(S.dm, a, sizeof(double) * S.A, cudaMemcpyHostToDevice, st));
+    double* d = S.alloc<double>(2 + S.n_dir);
+    fewha_gpu::sim_quality(S, S.layers, S.dm, d, st);
+    CK(cudaMemcpyAsync(rec, d, sizeof(double) * (2 + S.n_dir), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+}
+
+// run_closed_loop (simulation.hpp:321-345) with every frame on the device: the
+// handle's state is reset (a fresh Reconstructor in the reference), the truth
+// generated once, the noise streams of a chunk of frames generated together, and
+// per frame only kernel launches: frozen flow, slopes into the frame's input
+// slot, quality of a^(-1), the frame graph, its rho log kept on the device.
+// rec: [n_steps][2 + n_dir] (field_rms, layer_rel_err, rms_per_dir); rho
+// [n_steps][iters]; unc_final {uncorrected field RMS, final field RMS}.
+void Engine::run_closed_loop(int n_steps, unsigned long long atm_seed, unsigned long long noise_seed, double* rec,
+                             double* rho, double* unc_final) {
+    auto& P = *p_;
+    if (n_steps < 1) throw ArgError("run_closed_loop: n_steps must be >= 1");
+    if (P.batch != 1 || P.sharded) throw ArgError("run_closed_loop: single-instance, unsharded handles only");
+    CK(cudaSetDevice(P.device));
+    SimState& S = sim_state(P);
+    if (!P.has_precond) P.build_precond();
+    reset();
+    const cudaStream_t st = P.s();
+    fewha_gpu::sim_atmosphere(P, S, atm_seed, st);
+    const int RW = 2 + S.n_dir, it = P.gp.iters;
+    double* drec = S.alloc<double>(static_cast<size_t>(n_steps) * RW);
+    double* drho = S.alloc<double>(static_cast<size_t>(n_steps) * it);
+    double* dunc = S.alloc<double>(static_cast<size_t>(RW));
+    constexpr int kChunk = 128;
+    const int zc = 2 * S.pairs;
+    if (P.g.sim_noise && S.z_cap < kChunk) {
+        S.z = S.alloc<double>(static_cast<size_t>(kChunk) * std::max(zc, 1));
+        S.z_cap = kChunk;
+    }
+    double* meas = P.precision == 64 ? P.sd.meas : P.sf.meas;
+    const double* rho_log = P.precision == 64 ? P.sd.bf.rho_log : P.sf.bf.rho_log;
+    if (P.precision == 64) {
+        P.ensure_graph<double>();
+        P.set_fit_a_host<double>(nullptr);
+    } else {
+        P.ensure_graph<float>();
+        P.set_fit_a_host<float>(nullptr);
+    }
+    const double* lay = S.truth;
+    for (int k0 = 0; k0 < n_steps; k0 += kChunk) {
+        const int nk = std::min(kChunk, n_steps - k0);
+        if (P.g.sim_noise) {  // the chunk's noise streams, one warp each
+            std::vector<unsigned long long> seeds(static_cast<size_t>(nk));
+            for (int k = 0; k < nk; ++k)
+                seeds[static_cast<size_t>(k)] =
+                    splitmix64(splitmix64(noise_seed + static_cast<std::uint64_t>(k0 + k)) ^ 0x6e0f7a3dULL);
+            sim_normals(P, S, seeds, zc, S.z, st);
+        }
+        for (int k = 0; k < nk; ++k) {
+            const int step = k0 + k;
+            lay = sim_truth_at_step(S, S.truth, step, S.layers, st);
+            const double* a2 = sim_dm(P, S, st);
+            sim_slopes(P, S, lay, a2, P.g.sim_noise ? S.z + static_cast<size_t>(k) * zc : nullptr,
+                       meas, st);
+            fewha_gpu::sim_quality(S, lay, a2, drec + static_cast<size_t>(step) * RW, st);
+            CK(cudaGraphLaunch(P.graph, st));
+            CK(cudaMemcpyAsync(drho + static_cast<size_t>(step) * it, rho_log, sizeof(double) * it,
+                               cudaMemcpyDeviceToDevice, st));
+            ++P.step_counter;
+        }
+        CK(cudaStreamSynchronize(st));  // the chunk's normals are consumed before the next chunk
+    }
+    fewha_gpu::sim_quality(S, lay, S.zero_dm, dunc, st);
+    CK(cudaMemcpyAsync(rec, drec, sizeof(double) * static_cast<size_t>(n_steps) * RW, cudaMemcpyDeviceToHost, st));
+    if (rho) CK(cudaMemcpyAsync(rho, drho, sizeof(double) * static_cast<size_t>(n_steps) * it, cudaMemcpyDeviceToHost, st));
+    double unc[2];
+    CK(cudaMemcpyAsync(unc, dunc, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    unc[1] = rec[static_cast<size_t>(n_steps - 1) * RW];
+    if (unc_final) {
+        unc_final[0] = unc[0];
+        unc_final[1] = unc[1];
+    }
+    sync_check();
 }
 
 }  // namespace fewha_gpu

@@ -29,6 +29,8 @@ struct PlanInfo {
 class Engine;
 // contiguous WFS range [first, second) of shard `rank` of `world` (balanced by wavefront nodes)
 std::pair<int, int> shard_range(const Geometry& g, int rank, int world);
+// GaussianStream(seed) (simulation.hpp:40-58) drawn on the device: count normals
+void sim_gauss_stream(int device, unsigned long long seed, int count, double* out);
 // one frame of an in-process shard group, members in rank order
 void group_step_device(const std::vector<Engine*>& members);
 
@@ -92,6 +94,14 @@ public:
     void sh_transpose(const double* meas, double* wf, int count);
     void forward_slopes(const double* layers, const double* a, double* meas, int count);
     void wfs_operator(int rhs, const double* in, const double* meas, double* psi, int count);
+
+    // closed-loop simulation harness on the device (simulation.hpp)
+    int sim_quality_size();  // 2 + probe directions
+    void sim_atmosphere(unsigned long long seed, int step, double* layers_out);
+    void sim_synthesize(const double* layers, const double* a, unsigned long long noise_seed, double* meas);
+    void sim_quality(const double* layers, const double* a, double* rec);
+    void run_closed_loop(int n_steps, unsigned long long atm_seed, unsigned long long noise_seed, double* rec,
+                         double* rho, double* unc_final);
 
 private:
     std::unique_ptr<EngineImpl> p_;
