@@ -102,10 +102,10 @@ FEWHA_HD int tail_max(int maxside, int C, int D) {
     const int Tm = tail(maxside, C, D), tonly = maxside < D ? maxside : D;
     return Tm > tonly ? Tm : tonly;
 }
-FEWHA_HD FwdSmem fwd_smem(int maxside, int C, int D, int flen, int elem) {
+// tonly: the largest tail-only layer side of the geometry (0: none)
+FEWHA_HD FwdSmem fwd_smem(int maxside, int C, int D, int flen, int elem, int tonly) {
     FwdSmem m{};
     const int P = maxside + 1, R = band_rows(maxside, C, D, 0);
-    const int tonly = maxside < D ? maxside : D;
     const int xrows = (R + flen - 2) > tonly ? (R + flen - 2) : tonly;  // tail-only layers use the band too
     const int xb = a16(xrows * P * elem), cb = a16(compact_size(maxside, C, D, 0) * elem);
     m.x0 = 0;

@@ -315,11 +315,28 @@ __device__ T* tail_inverse(const GeoParams& gp, const T* zt, int Tt, T* b0, T* b
     int pc = Tt;
     T* nxt = b0;
     const int sf = Tt < kFusedTail ? Tt : kFusedTail;
+    // the filter taps in registers (compile-time indices): an output's taps depend on its
+    // row / column parity, selected per thread below -- a per-lane parity index into the
+    // parameter bank would serialise the warp's constant loads
+    T flo[FLEN], fhi[FLEN];
+#pragma unroll
+    for (int k = 0; k < FLEN; ++k) {
+        flo[k] = Filt<T>::lo(gp, k);
+        fhi[k] = Filt<T>::hi(gp, k);
+    }
     for (int s = 2; s <= sf; s <<= 1) {
         const int h = s >> 1, ls = ilog2(s);
         for (int e = tid; e < s * s; e += nthr) {
             const int r = e >> ls, c = e & (s - 1);
             const int m1 = r >> 1, u1 = r & 1, m2 = c >> 1, u2 = c & 1;
+            T l1[HF], h1[HF], l2[HF], h2[HF];
+#pragma unroll
+            for (int kk = 0; kk < HF; ++kk) {
+                l1[kk] = u1 ? flo[2 * kk + 1] : flo[2 * kk];
+                h1[kk] = u1 ? fhi[2 * kk + 1] : fhi[2 * kk];
+                l2[kk] = u2 ? flo[2 * kk + 1] : flo[2 * kk];
+                h2[kk] = u2 ? fhi[2 * kk + 1] : fhi[2 * kk];
+            }
             T acc = T(0);
 #pragma unroll
             for (int kk2 = 0; kk2 < HF; ++kk2) {
@@ -329,13 +346,12 @@ __device__ T* tail_inverse(const GeoParams& gp, const T* zt, int Tt, T* b0, T* b
                     T y = T(0);
 #pragma unroll
                     for (int kk1 = 0; kk1 < HF; ++kk1) {
-                        const int k1 = u1 + 2 * kk1, ra = (m1 - kk1) & (h - 1);
+                        const int ra = (m1 - kk1) & (h - 1);
                         const T xa = (cc < h) ? cur[ra * pc + cc] : zt[ra * Tt + cc];
                         const T xd = zt[(h + ra) * Tt + cc];
-                        y += xa * Filt<T>::lo(gp, k1) + xd * Filt<T>::hi(gp, k1);
+                        y += xa * l1[kk1] + xd * h1[kk1];
                     }
-                    const int k2 = u2 + 2 * kk2;
-                    acc += y * (b2 == 0 ? Filt<T>::lo(gp, k2) : Filt<T>::hi(gp, k2));
+                    acc += y * (b2 == 0 ? l2[kk2] : h2[kk2]);
                 }
             }
             nxt[r * (Tt + 1) + c] = acc;
@@ -1011,7 +1027,7 @@ __device__ __forceinline__ void fwd_phase(const GeoParams& gp, const Bufs<T>& bf
     const int S = gp.side[l];
     const LPlan p = make_plan(S, C, gp.ctail, q, 0, s_off);
     const int nthr = blockDim.x, tid = threadIdx.x;
-    const clay::FwdSmem sm = clay::fwd_smem(gp.maxside, C, gp.ctail, FLEN, static_cast<int>(sizeof(T)));
+    const clay::FwdSmem sm = clay::fwd_smem(gp.maxside, C, gp.ctail, FLEN, static_cast<int>(sizeof(T)), gp.tonly);
     const int P = gp.maxside + 1;
     T* x0 = reinterpret_cast<T*>(smem_raw + sm.x0);
     T* e0 = reinterpret_cast<T*>(smem_raw + sm.e0);

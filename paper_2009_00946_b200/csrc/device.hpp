@@ -17,7 +17,7 @@ namespace fewha_gpu {
 constexpr int kMaxL = 16;
 constexpr int kMaxW = 16;
 constexpr int kMaxM = 16;
-constexpr int kMaxC = 8;  // CTAs per layer cluster (portable cluster size)
+constexpr int kMaxC = 16;  // CTAs per layer cluster (8: portable; 16: non-portable opt-in)
 constexpr int kMaxGU = 64;      // row groups per layer (max side 128 / the smallest row group, 2)
 constexpr int kMaxWtCode = 1024;  // WFS tiles with a constant-bank position code
 
@@ -65,6 +65,7 @@ struct GeoParams {
     // v2 cluster path
     int ccl;          // CTAs per layer cluster
     int ctail;        // tail size D of distributed layers (clayout.hpp)
+    int tonly;        // largest tail-only layer side (S < 2D; 0: none) -- sizes the forward band buffer
     int grows;        // layer rows per CTA of the adjoint gather (4: latency, 8: batches)
     int inv_staged;   // inverse kernel: operands staged in shared memory by TMA (1) or read from global (0)
     int gather_km;    // max gather taps per layer row/column

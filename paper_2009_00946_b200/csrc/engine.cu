@@ -340,11 +340,23 @@ Plan build_plan(const Geometry& g, int elem_bytes, int batch, int wa = 0, int wb
         gp.tt_off_d = static_cast<int>(td_.first);
     }
 
-    // ---- cluster path: C = maxside / min(16, maxside) CTAs per layer; band rows per rank: clayout.hpp
+    // ---- cluster path: C = maxside / min(R, maxside) CTAs per layer, R = 16 band rows per rank
+    // (FEWHA_CLUSTER_ROWS = 8: 16-CTA clusters, non-portable); band rows per rank: clayout.hpp
     {
-        const int R = std::min(16, pl.maxside);
+        int band = 16;
+        if (const char* v = std::getenv("FEWHA_CLUSTER_ROWS")) {
+            const int r = std::atoi(v);
+            if (r == 8 || r == 16) band = r;
+        }
+        const int R = std::min(band, pl.maxside);
         gp.ccl = pl.maxside / R;
         if (gp.ccl > kMaxC) throw ConfigError("invalid geometry: layer side exceeds the cluster transform");
+        auto tonly_of = [&](int D) {  // largest tail-only layer side for tail size D
+            int t = 0;
+            for (int l = 0; l < L; ++l)
+                if (!clay::dist(gp.side[l], gp.ccl, D)) t = std::max(t, gp.side[l]);
+            return t;
+        };
         // tail size: D = 4C (measured best at the ELT scale), else 2C, else C -- the first whose layer kernels fit the sm_100 opt-in
         // shared memory (227 KB less static) in fp64 -- fp32 engines use the same layout, so
         // their fp64 preconditioner probes share the coefficient permutation
@@ -354,12 +366,16 @@ Plan build_plan(const Geometry& g, int elem_bytes, int batch, int wa = 0, int wb
             constexpr int kSmemBudget = 227 * 1024 - 2048, kTwoPerSm = 113 * 1024 - 2048;
             const int flen = 2 * g.wavelet_order, C = gp.ccl;
             gp.ctail = C;
-            for (int D : {4 * C, 2 * C}) {
+            // candidates: a 32^2 tail (4C at C = 8, 2C at C = 16; measured best at the ELT
+            // scale), then 2C
+            const int D0 = C <= 8 ? 4 * C : 2 * C;
+            for (int D : {D0, 2 * C}) {
                 if (D > pl.maxside / 2) continue;
+                const int t = tonly_of(D);
                 const bool fits = clay::inv_smem(pl.maxside, C, D, flen, 8).total <= kSmemBudget &&
-                                  clay::fwd_smem(pl.maxside, C, D, flen, 8).total <= kSmemBudget;
+                                  clay::fwd_smem(pl.maxside, C, D, flen, 8, t).total <= kSmemBudget;
                 const bool two = clay::inv_smem(pl.maxside, C, D, flen, 8, 0).total <= kTwoPerSm &&
-                                 clay::fwd_smem(pl.maxside, C, D, flen, 8).total <= kTwoPerSm;
+                                 clay::fwd_smem(pl.maxside, C, D, flen, 8, t).total <= kTwoPerSm;
                 if (fits && (batch <= 2 || two)) {
                     gp.ctail = D;
                     break;
@@ -369,6 +385,7 @@ Plan build_plan(const Geometry& g, int elem_bytes, int batch, int wa = 0, int wb
                 const int D = std::atoi(v);
                 if (D >= C && D <= std::max(C, pl.maxside / 2) && (D & (D - 1)) == 0) gp.ctail = D;
             }
+            gp.tonly = tonly_of(gp.ctail);
         }
         // gather tables: per (w,l) and axis, for every layer node the (source, weight) list,
         // ascending source (operators.hpp:129-135 weights as bilinear_stencil assigns them)
@@ -739,13 +756,16 @@ struct Launch {
     }
     // TMA staging of the inverse kernel's operands pays for a single instance (latency);
     // batches stream them from global memory at twice the residency
-    static int inv_staged_for(int count) {
+    // 16-CTA clusters stream too: a staged inverse (one CTA per SM) would not let
+    // nine 16-CTA clusters be resident at once
+    static int inv_staged_for(const GeoParams& gp, int count) {
         const char* v = std::getenv("FEWHA_INV_STAGE");  // read per plan (tests switch it between engines)
         const int mode = v ? std::atoi(v) : -1;
-        return mode >= 0 ? (mode ? 1 : 0) : (count <= 2 ? 1 : 0);
+        return mode >= 0 ? (mode ? 1 : 0) : (count <= 2 && gp.ccl <= 8 ? 1 : 0);
     }
     static size_t fwd_cl_smem(const GeoParams& gp, int flen) {
-        return static_cast<size_t>(clay::fwd_smem(gp.maxside, gp.ccl, gp.ctail, flen, static_cast<int>(sizeof(T))).total);
+        return static_cast<size_t>(
+            clay::fwd_smem(gp.maxside, gp.ccl, gp.ctail, flen, static_cast<int>(sizeof(T)), gp.tonly).total);
     }
 
 #define FEWHA_FLEN_SWITCH(flen, CALL)          \
@@ -795,7 +815,7 @@ struct Launch {
     static void cl(int flen, bool inverse, const GeoParams& gp, const Bufs<T>& bf, int mode, int it, int count,
                    cudaStream_t st, int fit_term = 1) {
         GeoParams g2 = gp;
-        g2.inv_staged = inv_staged_for(count);
+        g2.inv_staged = inv_staged_for(gp, count);
         const size_t smem = inverse ? inv_cl_smem(g2, flen, g2.inv_staged) : fwd_cl_smem(g2, flen);
 #define FEWHA_LAUNCH(N) CK((launch_layer_cluster<T, N>(inverse, g2, bf, mode, it, count, st, fit_term, smem)))
         FEWHA_FLEN_SWITCH(flen, FEWHA_LAUNCH)
@@ -805,7 +825,7 @@ struct Launch {
     static void fused(int flen, const GeoParams& gp, const Bufs<T>& bf, int fmode, int fit, int imode, int iit,
                       int count, cudaStream_t st, unsigned long long* bar) {
         GeoParams g2 = gp;
-        g2.inv_staged = inv_staged_for(count);
+        g2.inv_staged = inv_staged_for(gp, count);
         const size_t smem = fused_cl_smem(g2, flen, g2.inv_staged);
 #define FEWHA_LAUNCH(N) \
     CK((launch_fused_cluster<T, N>(g2, bf, fmode, fit, imode, iit, count, st, 1, smem, bar, pdl_enabled() ? 1 : 0)))
@@ -818,7 +838,7 @@ struct Launch {
     // clusters of the fused kernel resident at once (0: it does not fit)
     static int fused_capacity(const GeoParams& gp, int flen, int count) {
         GeoParams g2 = gp;
-        g2.inv_staged = inv_staged_for(count);
+        g2.inv_staged = inv_staged_for(gp, count);
         int clusters = 0;
 #define FEWHA_CAP(N) CK((fused_cluster_capacity<T, N>(g2, fused_cl_smem(g2, flen, g2.inv_staged), &clusters)))
         FEWHA_FLEN_SWITCH(flen, FEWHA_CAP)
@@ -1140,6 +1160,17 @@ struct EngineImpl {
         if (graph) return;
         if (sharded && !comm) throw ArgError("shard group members step through fewha_gpu_group_step_device");
         cudaGraph_t gr;
+        // profiling (FEWHA_GRAPH_STAMPS=1 after fewha_gpu_phase_stamps enabled the buffer): the
+        // captured launches record their phase stamps, so the overlapped (PDL) timeline of a
+        // real graph frame can be read back
+        struct Stamps {
+            int& slot;
+            bool on;
+            ~Stamps() {
+                if (on) slot = -1;
+            }
+        } graph_stamps{stamp_slot, stamp_buf != nullptr && std::getenv("FEWHA_GRAPH_STAMPS") != nullptr};
+        if (graph_stamps.on) stamp_slot = 0;
         CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
         if (telemetry_on) {  // event-record nodes around every launch (StepTelemetry)
             tkind.clear();
@@ -1821,7 +1852,7 @@ PlanInfo Engine::plan_info() const {
     pi.tail = P.gp.ctail;
     pi.gather_rows = P.gp.grows;
     pi.gather_ctas_per_sm = P.gp.gather_minb;
-    pi.inverse_staged = P.precision == 64 ? Launch<double>::inv_staged_for(P.batch) : Launch<float>::inv_staged_for(P.batch);
+    pi.inverse_staged = P.precision == 64 ? Launch<double>::inv_staged_for(P.gp, P.batch) : Launch<float>::inv_staged_for(P.gp, P.batch);
     pi.wfs_ctas_per_sm = P.batch <= 2 ? FEWHA_WFS_MINB_LAT : FEWHA_WFS_MINB_BATCH;
     pi.wfs_tiles = P.gp.wt_count;
     pi.launches_per_step = launches_per_step();

@@ -86,6 +86,12 @@ static cudaError_t opt_in_max(K kernel, size_t maxopt) {
 
 template <typename T, int FLEN>
 cudaError_t set_layer_cluster_attrs(size_t smem_inv, size_t smem_fwd) {
+    // 16-CTA clusters (FEWHA_CLUSTER_ROWS=8) are beyond the portable size 8
+    for (const void* k : {(const void*)k_inv_cluster<T, FLEN>, (const void*)k_fwd_cluster<T, FLEN>,
+                          (const void*)k_fwd_inv_cluster<T, FLEN>}) {
+        const cudaError_t a = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (a != cudaSuccess) return a;
+    }
     cudaError_t e = opt_in_max(k_inv_cluster<T, FLEN>, smem_inv);
     if (e != cudaSuccess) return e;
     e = opt_in_max(k_fwd_inv_cluster<T, FLEN>, smem_fwd);
