@@ -80,6 +80,16 @@ typedef struct {
  * as the reference).  */
 int fewha_gpu_create(const char* preset_json_path, int precision, int batch, int device, fewha_gpu_t* out);
 int fewha_gpu_create_from_json(const char* json_text, int precision, int batch, int device, fewha_gpu_t* out);
+/* The SURVEY 8(b) multi-device form: devices[0..n_devices) (repeats allowed).  One
+ * device: the same handle as fewha_gpu_create.  Several: an in-process per-WFS shard
+ * group (fewha_gpu_shard semantics, one shard per listed device, peer access between
+ * them): fewha_gpu_step / _step_device / _load_slopes / _reset / _set_state /
+ * _build_preconditioner / _sync act on every shard and step them together (the
+ * partial adjoint layer sums are summed in rank order from the shards' buffers);
+ * outputs, state reads and the operator entry points come from shard 0 (the
+ * replicated state is bitwise identical on every shard). */
+int fewha_gpu_create_multi(const char* preset_json_path, int precision, int batch, const int* devices, int n_devices,
+                           fewha_gpu_t* out);
 /* loop_mode: -1 keep, 0 closed, 1 open; gain < 0 keeps (test hooks, like editing SystemGeometry) */
 int fewha_gpu_override_loop(fewha_gpu_t h, int loop_mode, double gain);
 const char* fewha_gpu_create_error(void);

@@ -38,7 +38,7 @@ EXPORTS = (
     "fewha_gpu_shard_wfs", "fewha_gpu_group_step_device", "fewha_gpu_enable_telemetry", "fewha_gpu_last_telemetry",
     "fewha_gpu_wfs_operator", "fewha_gpu_plan_info", "fewha_gpu_last_launch_times",
     "fewha_gpu_sim_quality_size", "fewha_gpu_sim_atmosphere", "fewha_gpu_sim_synthesize", "fewha_gpu_sim_quality",
-    "fewha_gpu_run_closed_loop", "fewha_gpu_sim_gauss",
+    "fewha_gpu_run_closed_loop", "fewha_gpu_sim_gauss", "fewha_gpu_create_multi",
 )
 
 
@@ -112,6 +112,7 @@ def lib() -> C.CDLL:
         vp = C.c_void_p
         L.fewha_gpu_create.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]
         L.fewha_gpu_create_from_json.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]
+        L.fewha_gpu_create_multi.argtypes = [C.c_char_p, C.c_int, C.c_int, C.POINTER(C.c_int), C.c_int, C.POINTER(vp)]
         L.fewha_gpu_create_error.restype = C.c_char_p
         L.fewha_gpu_last_error.restype = C.c_char_p
         L.fewha_gpu_last_error.argtypes = [vp]
@@ -220,10 +221,16 @@ class Reconstructor:
     precision: 64 (parity mode, 1e-9) or 32 (1e-4).  batch: independent
     instances stepped together; per-frame arrays are then [batch, ...]."""
 
-    def __init__(self, preset, precision: int = 64, batch: int = 1, device: int = 0, loop_mode=None, gain=None):
+    def __init__(self, preset, precision: int = 64, batch: int = 1, device: int = 0, loop_mode=None, gain=None,
+                 devices=None):
+        """devices: a list of CUDA ordinals (fewha_gpu_create_multi): more than one makes
+        the handle an in-process per-WFS shard group stepped as one reconstructor."""
         L = lib()
         h = C.c_void_p()
-        if isinstance(preset, dict):
+        if devices is not None:
+            arr = (C.c_int * len(devices))(*devices)
+            rc = L.fewha_gpu_create_multi(os.fspath(preset).encode(), precision, batch, arr, len(devices), C.byref(h))
+        elif isinstance(preset, dict):
             import json
             rc = L.fewha_gpu_create_from_json(json.dumps(preset).encode(), precision, batch, device, C.byref(h))
         else:

@@ -17,8 +17,17 @@ using fewha_gpu::ConfigError;
 using fewha_gpu::Engine;
 
 struct fewha_gpu_handle {
-    std::unique_ptr<Engine> eng;
+    std::unique_ptr<Engine> eng;  // the engine (member 0 of a multi-device handle)
+    // fewha_gpu_create_multi with n_devices > 1: shard members 1..n-1 (member 0 is eng)
+    // of an in-process per-WFS group stepped together by fewha_gpu_step
+    std::vector<std::unique_ptr<Engine>> more;
     std::string err;
+    bool group() const { return !more.empty(); }
+    std::vector<Engine*> members() const {
+        std::vector<Engine*> m{eng.get()};
+        for (const auto& e : more) m.push_back(e.get());
+        return m;
+    }
 };
 
 namespace {
@@ -72,6 +81,26 @@ int fewha_gpu_create(const char* path, int precision, int batch, int device, few
 
 int fewha_gpu_create_from_json(const char* text, int precision, int batch, int device, fewha_gpu_t* out) {
     return create(&fewha_gpu::parse_preset_text, text, precision, batch, device, out);
+}
+
+int fewha_gpu_create_multi(const char* path, int precision, int batch, const int* devices, int n_devices,
+                           fewha_gpu_t* out) {
+    if (!out || !path || !devices || n_devices < 1) {
+        g_create_error = "null argument or no device";
+        return FEWHA_ARG;
+    }
+    *out = nullptr;
+    return guard(g_create_error, [&] {
+        const auto g = fewha_gpu::parse_preset_file(path);
+        auto h = std::make_unique<fewha_gpu_handle>();
+        h->eng = std::make_unique<Engine>(g, precision, batch, devices[0]);
+        for (int r = 1; r < n_devices; ++r) h->more.push_back(std::make_unique<Engine>(g, precision, batch, devices[r]));
+        if (n_devices > 1) {  // per-WFS shards of one frame, exchanged by peer loads
+            auto m = h->members();
+            for (int r = 0; r < n_devices; ++r) m[static_cast<size_t>(r)]->shard(r, n_devices, nullptr);
+        }
+        *out = h.release();
+    });
 }
 
 int fewha_gpu_override_loop(fewha_gpu_t h, int loop_mode, double gain) { H_GUARD(h->eng->override_loop(loop_mode, gain)) }
@@ -137,7 +166,9 @@ int fewha_gpu_geometry(fewha_gpu_t h, double* layer_extent, double* dm_extent, u
     })
 }
 
-int fewha_gpu_build_preconditioner(fewha_gpu_t h) { H_GUARD(h->eng->build_preconditioner()) }
+int fewha_gpu_build_preconditioner(fewha_gpu_t h) {
+    H_GUARD(for (auto* m : h->members()) m->build_preconditioner())
+}
 
 int fewha_gpu_preconditioner(fewha_gpu_t h, double* out) {
     H_GUARD({
@@ -150,18 +181,27 @@ int fewha_gpu_preconditioner(fewha_gpu_t h, double* out) {
 int fewha_gpu_step(fewha_gpu_t h, const double* slopes, double* coeffs, double* dm, double* rho, int* n_rho) {
     H_GUARD({
         if (!slopes) throw ArgError("step: null slopes");
-        h->eng->step(slopes, coeffs, dm, rho, n_rho);
+        if (!h->group()) {
+            h->eng->step(slopes, coeffs, dm, rho, n_rho);
+        } else {  // every shard reconstructs the same frame; the replicated outputs are read from member 0
+            const auto m = h->members();
+            for (auto* e : m) e->load_slopes(slopes, false);
+            fewha_gpu::group_step_device(m);
+            for (size_t r = 1; r < m.size(); ++r) m[r]->sync_check();
+            h->eng->read_outputs(coeffs, dm, rho, n_rho);
+        }
     })
 }
 
-int fewha_gpu_reset(fewha_gpu_t h) { H_GUARD(h->eng->reset()) }
+int fewha_gpu_reset(fewha_gpu_t h) { H_GUARD(for (auto* m : h->members()) m->reset()) }
 
 int fewha_gpu_get_state(fewha_gpu_t h, int instance, fewha_gpu_state_t* st) {
     H_GUARD(h->eng->get_state(instance, st->c, st->b, st->r, st->p, st->q, st->scalars, st->a_prev2, st->a_prev))
 }
 
 int fewha_gpu_set_state(fewha_gpu_t h, int instance, const fewha_gpu_state_t* st) {
-    H_GUARD(h->eng->set_state(instance, st->c, st->b, st->r, st->p, st->q, st->scalars, st->a_prev2, st->a_prev))
+    H_GUARD(for (auto* m : h->members())
+                m->set_state(instance, st->c, st->b, st->r, st->p, st->q, st->scalars, st->a_prev2, st->a_prev))
 }
 
 int fewha_gpu_set_stream(fewha_gpu_t h, void* stream) { H_GUARD(h->eng->set_stream(stream)) }
@@ -173,11 +213,22 @@ int fewha_gpu_device_buffers(fewha_gpu_t h, fewha_gpu_device_t* o) {
 int fewha_gpu_load_slopes(fewha_gpu_t h, const void* src, int on_device) {
     H_GUARD({
         if (!src) throw ArgError("load_slopes: null source");
-        h->eng->load_slopes(src, on_device != 0);
+        for (auto* m : h->members()) m->load_slopes(src, on_device != 0);
     })
 }
-int fewha_gpu_step_device(fewha_gpu_t h, const void* d_slopes) { H_GUARD(h->eng->step_device(d_slopes)) }
-int fewha_gpu_sync(fewha_gpu_t h) { H_GUARD(h->eng->sync_check()) }
+int fewha_gpu_step_device(fewha_gpu_t h, const void* d_slopes) {
+    H_GUARD({
+        if (!h->group()) {
+            h->eng->step_device(d_slopes);
+        } else {
+            const auto m = h->members();
+            if (d_slopes)
+                for (auto* e : m) e->load_slopes(d_slopes, true);
+            fewha_gpu::group_step_device(m);
+        }
+    })
+}
+int fewha_gpu_sync(fewha_gpu_t h) { H_GUARD(for (auto* m : h->members()) m->sync_check()) }
 int fewha_gpu_launches_per_step(fewha_gpu_t h) { return h ? h->eng->launches_per_step() : -1; }
 int fewha_gpu_plan_info(fewha_gpu_t h, fewha_gpu_plan_t* out) {
     if (!out) return FEWHA_ARG;

@@ -1833,6 +1833,32 @@ void Engine::load_slopes(const void* src, bool on_device) {
                        on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, P.s()));
 }
 
+// Outputs of the last device frame (any may be null): st.c, a^(1), the rho log
+// and its length; raises on a non-finite PCG scalar like step().
+void Engine::read_outputs(double* coeffs, double* dm, double* rho, int* n_rho) {
+    auto& P = *p_;
+    CK(cudaSetDevice(P.device));
+    const cudaStream_t st = P.s();
+    const size_t B = P.batch, A = P.gp.A, it = P.gp.iters;
+    CK(cudaStreamSynchronize(st));
+    auto rd = [&](auto& w) {
+        using T = std::remove_pointer_t<decltype(w.bf.c)>;
+        if (coeffs) d2h_coeff<T>(coeffs, w.bf.c, P.plan.perm, B, st);
+        if (dm) d2h_conv<T>(dm, w.bf.a_out, B * A, st);
+        std::vector<unsigned char> blk(w.frame_out_bytes);
+        CK(cudaMemcpyAsync(blk.data(), w.bf.rho_log, blk.size(), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        const auto* hr = reinterpret_cast<const double*>(blk.data());
+        const int* status = reinterpret_cast<const int*>(hr + B * it);
+        if (rho) std::copy(hr, hr + B * it, rho);
+        if (n_rho) std::copy(status + B, status + 2 * B, n_rho);
+        for (size_t b = 0; b < B; ++b)
+            if (status[b]) throw std::runtime_error("pcg_solve: non-finite scalar (indefinite operator?)");
+    };
+    if (P.precision == 64) rd(P.sd);
+    else rd(P.sf);
+}
+
 void Engine::sync_check() {
     auto& P = *p_;
     CK(cudaSetDevice(P.device));

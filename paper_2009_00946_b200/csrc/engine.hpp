@@ -63,6 +63,7 @@ public:
     void step_device(const void* d_slopes);
     void load_slopes(const void* src, bool on_device);
     void sync_check();
+    void read_outputs(double* coeffs, double* dm, double* rho, int* n_rho);
     void enable_telemetry(bool on);
     StepTelemetry last_telemetry();
     int last_launch_times(float* ms, int* kinds, int max);

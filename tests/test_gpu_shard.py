@@ -99,3 +99,29 @@ def test_group_member_refuses_standalone_step():
     m = _group(path, 2, 64)[0]
     with pytest.raises(fg.ArgumentError, match="group"):
         m.step(np.zeros(m.dims.S))
+
+
+@pytest.mark.parametrize("devices", [[0], [0, 0], [0, 0, 0]])
+def test_multi_device_handle_steps_like_one_reconstructor(devices):
+    """fewha_gpu_create_multi (SURVEY 8(b)'s devices/n_devices form): one handle over
+    the listed devices -- a per-WFS shard group when there are several -- driven
+    through the ordinary fewha_gpu_step: a^(1), st.c and rho match the oracle at
+    1e-9 over closed-loop frames, and reset / set_state act on every shard."""
+    path = preset("elt_mcao84_3dm.json")
+    o = Oracle(path)
+    o.build_preconditioner()
+    g = fg.Reconstructor(path, devices=devices)
+    lay = smooth_layers(o, 11)
+    for k in range(4):
+        s = noisy_slopes(o, lay, 700 + k, o.get_state()["a_prev2"])
+        c_o, a_o, rho_o = o.step(s)
+        a = g.step(s)
+        assert rel_err(g.coeffs(), c_o) <= 1e-9, ("c", k)
+        assert rel_err(a, a_o) <= 1e-9, ("a", k)
+        assert rel_err(g.last_rho, rho_o) <= 1e-9, ("rho", k)
+    st = o.get_state()
+    g.reset()
+    g.set_state(st)  # every shard restarts from the oracle's state
+    s = noisy_slopes(o, lay, 800, st["a_prev2"])
+    c_o, a_o, _ = o.step(s)
+    assert rel_err(g.step(s), a_o) <= 1e-10
