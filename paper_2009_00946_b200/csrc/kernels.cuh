@@ -1,26 +1,27 @@
-// sm_100a kernels of the FEWHA reconstructor.
+// sm_100a kernels of the FEWHA reconstructor: the per-WFS tile kernel, the
+// fitting/control kernel, the operator-entry kernels and the shared device
+// helpers (TMA bulk copies, programmatic dependent launch, the fused-PCG scalar
+// step).  The cluster-distributed layer transforms and the adjoint gather are in
+// cluster.cuh, the simulation harness in sim_kernels.cuh.
 //
 // Every operator of the reference's hot path (reconstructor.hpp:166-355) is a
-// hand-written kernel here.  No tensor cores: nothing on the path is a dense
-// contraction; the kernels are HBM/L2-bandwidth and latency bound (SURVEY.md
-// 8d).  Design points:
-//   * a whole 2^J x 2^J layer lives in shared memory (odd pitch side+1, so
-//     row-walks and column-walks are both bank-conflict free) while its
-//     multilevel periodic Daubechies transform runs; each pass stages its
-//     outputs in registers across one CTA barrier, so the transform is in
-//     place with no second buffer (128 KiB fp64 at J=7);
-//   * the per-WFS chain Gamma^T C^-1 Gamma P runs on 16x16 node tiles with a
-//     one-node halo: P gather -> slopes -> adjoint slopes all in shared memory;
-//   * the adjoint propagation P^T is an atomic-free separable gather: the
-//     bilinear stencil factorises (x depends only on the column, y only on the
-//     row, operators.hpp:208-210), so per layer tile a psi block is staged and
-//     contracted along columns then rows, WFS in ascending order
-//     (reconstructor.hpp:199-200) -- deterministic, no float atomics;
-//   * PCG dots are per-layer CTA partials written to fixed slots and summed in
-//     fixed order by every consumer (run-to-run bitwise deterministic); the
-//     scalar recurrences (pcg.hpp:80-99) are evaluated redundantly by each
-//     consumer CTA, and the p/q/c/r updates are fused into the next
-//     iteration's W^-1 kernel.
+// hand-written kernel.  No tensor cores: nothing on the path is a dense
+// contraction; the kernels are HBM/L2-bandwidth and latency bound.
+// Design points of this file:
+//   * k_wfs: one CTA per 14 x 14 wavefront-node tile (+1-node halo = 256 nodes,
+//     one per thread) of one WFS and instance.  The tile's stencil tables arrive
+//     by one TMA bulk copy before the programmatic-launch wait; P (9 layers' 36
+//     bilinear loads in flight per node), Gamma, C^-1 and Gamma^T then run in
+//     shared memory, Gamma^T as a gather in the reference's scatter order
+//     (operators.hpp:176-187);
+//   * k_fit_control: one thread per actuator; the DM history and the fitting
+//     stencils are loaded before the programmatic-launch wait; a^(1) is also
+//     stored straight into a page-locked caller buffer (zero-copy output);
+//   * PCG dots are per-CTA partials written to fixed slots and summed in fixed
+//     order by every consumer (run-to-run bitwise deterministic); the scalar
+//     recurrences (pcg.hpp:80-99) are evaluated redundantly by each consumer CTA
+//     (pcg_scalar_from_sums), and the p/q/c/r updates are fused into the next
+//     iteration's W^-1 kernel (cluster.cuh).
 #pragma once
 
 #include <cuda_runtime.h>
