@@ -863,7 +863,11 @@ struct Launch {
         cudaLaunchAttribute attr[1];
         cudaLaunchConfig_t cfg = pdl_cfg(dim3(gp.wt_count, count), wfs_smem(gp), st, attr, kWfsThreads);
         constexpr int LAT = FEWHA_WFS_MINB_LAT, BAT = FEWHA_WFS_MINB_BATCH;
-        if (count <= 2) {
+        static const bool bat_lat = [] {  // profiling: batches on the latency instantiation
+            const char* v = std::getenv("FEWHA_WFS_BATCH_MINB");
+            return v && std::atoi(v) == LAT;
+        }();
+        if (count <= 2 || bat_lat) {
             if (rhs) CK(cudaLaunchKernelEx(&cfg, k_wfs<T, true, LAT>, gp, bf, with_dm));
             else CK(cudaLaunchKernelEx(&cfg, k_wfs<T, false, LAT>, gp, bf, with_dm));
         } else {
