@@ -271,8 +271,7 @@ __device__ __forceinline__ void wstamp(const GeoParams& gp, int k) {
 // WFS tiles: 14 x 14 nodes, (14+2)^2 = 256 wavefront nodes = one per thread of a
 // 256-thread CTA in the dominant phase (16 x 16 tiles on 512 threads left 37 % of
 // the warps waiting at the barrier).  Resident CTAs per SM: 3 for single-instance
-// plans (80 registers, no spills on the latency path), 4 for batches (64 registers,
-// more tiles in flight): measured in DESIGN.md.
+// plans, 4 for batches (more tiles in flight); no spills in either (k_wfs below).
 #ifndef FEWHA_WFS_TILE
 #define FEWHA_WFS_TILE 14
 #endif
@@ -302,7 +301,7 @@ __host__ __device__ constexpr size_t wfs_tile_smem(int screens) {
     return wfs_tile_table_bytes<T>(screens) + static_cast<size_t>(H * H + 2 * Q * Q) * sizeof(T);
 }
 
-template <typename T, bool RHS>
+template <typename T, bool RHS, int G = 9>
 __device__ __forceinline__ void wfs_tile(const GeoParams& gp, const Bufs<T>& bf, int with_dm, int tile, int b,
                                          unsigned char* smem_raw) {
     constexpr int TS = kWfsTile, H = TS + 2, Q = TS + 1;
@@ -363,7 +362,6 @@ __device__ __forceinline__ void wfs_tile(const GeoParams& gp, const Bufs<T>& bf,
         if (screens_on && i >= 0 && i < np && j >= 0 && j < np) {
             // screens in unrolled groups of G: a group's 4G loads are in flight together
             // (padding screens of the last group read a valid node with weight 0)
-            constexpr int G = 9;
             for (int s0 = 0; s0 < NS; s0 += G) {
                 T q00[G], q01[G], q10[G], q11[G], fy[G], fx[G];
 #pragma unroll
@@ -441,7 +439,11 @@ __device__ __forceinline__ void wfs_tile(const GeoParams& gp, const Bufs<T>& bf,
 template <typename T, bool RHS, int MINB>
 __global__ void __launch_bounds__(kWfsThreads, MINB) k_wfs(const GeoParams gp, const Bufs<T> bf, int with_dm) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    wfs_tile<T, RHS>(gp, bf, with_dm, gp.wt_base + blockIdx.x, blockIdx.y, smem_raw);
+    // screens per unrolled load group: 7 for the latency plan (3 CTAs/SM, 72 registers; 9
+    // spilled 16 bytes), 5 for batches (4 CTAs/SM, 56 registers; 9 spilled 44 bytes and
+    // was 5 % slower per launch at B = 64)
+    constexpr int G = (MINB >= 4 && sizeof(T) == 8) ? 5 : 7;
+    wfs_tile<T, RHS, G>(gp, bf, with_dm, gp.wt_base + blockIdx.x, blockIdx.y, smem_raw);
 }
 
 // ---------------------------------------------------------------------------
