@@ -563,21 +563,34 @@ struct GDesc {
     int ilo, ihi, jlo, jhi;  // psi source block of this row group
     int src;                 // psi source element offset (woff + ilo * np)
     int soff;                // psi stage byte offset inside its chunk
-    int toff, tb;            // table byte offset in gblob, table bytes
+    int rtoff, rb;           // row-tap table of (layer, row group, WFS): byte offset in gblob, bytes
+    int ctoff, cb;           // column stencil of (layer, WFS) -- shared by every row group: offset, bytes
+    int pad0, pad1;
 };
+constexpr int kGDescInts = 12;
 
 __device__ __forceinline__ int align16(int v) { return (v + 15) & ~15; }
 
-// Stage WFS [w0, w1) (warp 0 only): the tables by lane 31 (one contiguous copy),
-// psi blocks by lanes 0..n-1.  The caller __syncwarp()s and lane 0 arrives.
+// Stage WFS [w0, w1) (warp 0 only): the chunk's row-tap tables by lane 31 and its
+// column stencils by lane 30 (one contiguous copy each: the row tables are stored per
+// (layer, row group), the column stencils once per layer, WFS ascending), psi blocks
+// by lanes 0..n-1.  The caller __syncwarp()s and lane 0 arrives.
+// Stage layout: [row tables | column stencils | psi blocks].
+__device__ __forceinline__ int gather_row_bytes(const GDesc* desc, int w0, int w1) {
+    return desc[w1 - 1].rtoff + desc[w1 - 1].rb - desc[w0].rtoff;
+}
 template <typename T>
 __device__ __forceinline__ void gather_issue(const GeoParams& gp, const T* psi_b, const GDesc* desc, int w0, int w1,
                                              unsigned char* stage, unsigned long long* mbar, bool tables, bool psi) {
     const int lane = threadIdx.x;
     if (tables && lane == 31) {
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        const unsigned bytes = static_cast<unsigned>(desc[w1 - 1].toff + desc[w1 - 1].tb - desc[w0].toff);
-        bulk_g2s(stage, gp.gblob + desc[w0].toff, bytes, mbar);
+        bulk_g2s(stage, gp.gblob + desc[w0].rtoff, static_cast<unsigned>(gather_row_bytes(desc, w0, w1)), mbar);
+    }
+    if (tables && lane == 30) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        const unsigned bytes = static_cast<unsigned>(desc[w1 - 1].ctoff + desc[w1 - 1].cb - desc[w0].ctoff);
+        bulk_g2s(stage + gather_row_bytes(desc, w0, w1), gp.gblob + desc[w0].ctoff, bytes, mbar);
     }
     if (psi && lane < w1 - w0) {
         const int w = w0 + lane;
@@ -615,8 +628,8 @@ __device__ void gather_group(const GeoParams& gp, const T* __restrict__ psi_b, i
     const bool worker = grp < groups;
     const int gst = ROWS * gp.bd_cols_max;  // G stride per WFS
     const int km = KM > 0 ? KM : gp.gather_km;  // taps per row in the staged tables
-    const int o_rw = align16(R * km * 2), o_f = o_rw + align16(R * km * static_cast<int>(sizeof(T)));
-    const int o_idx = o_f + align16((side + 3) * 2);
+    const int o_rw = align16(R * km * 2);      // row table: [src int16 R x km][weight R x km]
+    const int o_idx = align16((side + 3) * 2);  // column stencil: [first int16 side+3][idx int16 nc][frac nc]
     T out[ROWS];
 #pragma unroll
     for (int k = 0; k < ROWS; ++k) out[k] = T(0);
@@ -629,7 +642,8 @@ __device__ void gather_group(const GeoParams& gp, const T* __restrict__ psi_b, i
         }
         mbar_wait(mbar, static_cast<unsigned>(k & 1));
         stamp(gp, 1);
-        const int t0 = desc[w0].toff;
+        const int rt0 = desc[w0].rtoff, ct0 = desc[w0].ctoff;
+        const unsigned char* cstage = stage + gather_row_bytes(desc, w0, w1);
         // ---- rows: G_w(i, c) for every WFS of the chunk, one pass.  Thread =
         // (WFS group, column): a column's R rows share the thread's index math and
         // the row taps are warp-uniform (broadcast) loads ----
@@ -640,7 +654,7 @@ __device__ void gather_group(const GeoParams& gp, const T* __restrict__ psi_b, i
                 const GDesc d = desc[w];
                 const int nr = d.ihi - d.ilo, np = gp.ns[w] + 1, nc = d.jhi - d.jlo;
                 if (nr <= 0) continue;
-                const unsigned char* tp = stage + (d.toff - t0);
+                const unsigned char* tp = stage + (d.rtoff - rt0);
                 const unsigned shift = static_cast<unsigned>(reinterpret_cast<uintptr_t>(psi_b + d.src) & 15u);
                 const T* __restrict__ blk = reinterpret_cast<const T*>(stage + d.soff + shift) + d.jlo;  // blk[r*np + c]
                 const short* __restrict__ rs = reinterpret_cast<const short*>(tp);
@@ -669,8 +683,8 @@ __device__ void gather_group(const GeoParams& gp, const T* __restrict__ psi_b, i
                 const GDesc d = desc[w];
                 const int nr = d.ihi - d.ilo, nc = d.jhi - d.jlo;
                 if (nr <= 0) continue;
-                const unsigned char* tp = stage + (d.toff - t0);
-                const short* first = reinterpret_cast<const short*>(tp + o_f);
+                const unsigned char* tp = cstage + (d.ctoff - ct0);
+                const short* first = reinterpret_cast<const short*>(tp);
                 const short* cidx = reinterpret_cast<const short*>(tp + o_idx);
                 const T* cfr = reinterpret_cast<const T*>(tp + o_idx + align16(nc * 2));
                 const T* G = gbuf + (w - w0) * gst;
@@ -739,9 +753,9 @@ __global__ void __launch_bounds__(256, MINB) k_gather(const GeoParams gp, const 
     const T* psi = bf.psi + static_cast<size_t>(b) * gp.Nw;
     if (tid < 32) {
         if (tid < gp.W) {
-            const int4* d = reinterpret_cast<const int4*>(gp.ti + gp.o_gd + ((l * kMaxGU + u) * kMaxW + tid) * 8);
-            const int4 a = d[0], c = d[1];
-            s_desc[tid] = GDesc{a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
+            const int4* d = reinterpret_cast<const int4*>(gp.ti + gp.o_gd + ((l * kMaxGU + u) * kMaxW + tid) * kGDescInts);
+            const int4 a = d[0], c = d[1], e = d[2];
+            s_desc[tid] = GDesc{a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w, e.x, e.y, e.z, e.w};
         }
         if (tid == 0) {
             mbar_init(&s_mbar, 1);

@@ -73,7 +73,6 @@ struct GeoParams {
     int bd_rows_max, bd_cols_max;
     unsigned long long* stamps;  // optional phase timestamps [block][16] (nullptr: off)
     const unsigned char* gblob;  // per-(w,l) gather blobs of the engine's precision (see cluster.cuh)
-    int o_gb;                    // [l*kMaxGU + u] byte offset of each row group's table block (into ti)
     int chunk_bytes;  // shared-memory bytes of the largest staged WFS chunk of the gather
     int nchunk;                 // WFS chunks of the gather: [gchunk[k], gchunk[k+1])
     int gchunk[kMaxW + 1];

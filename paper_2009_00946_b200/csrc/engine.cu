@@ -464,11 +464,15 @@ Plan build_plan(const Geometry& g, int elem_bytes, int batch, int wa = 0, int wb
         gp.bd_cols_max = cmax;
         // staged bytes per WFS (mirrors gather_tab_bytes()/psi_bytes() in cluster.cuh)
         auto a16 = [](size_t v) { return (v + 15) & ~size_t(15); };
-        auto tab_bytes = [&](int R, int side, int nc) {
-            return a16(static_cast<size_t>(R) * km * 2) + a16(static_cast<size_t>(R) * km * elem_bytes) +
-                   a16(static_cast<size_t>(side + 3) * 2) + a16(static_cast<size_t>(nc) * 2) +
+        // row-tap table of one (layer, row group, WFS) and column stencil of one (layer, WFS)
+        auto row_bytes = [&](int R) {
+            return a16(static_cast<size_t>(R) * km * 2) + a16(static_cast<size_t>(R) * km * elem_bytes);
+        };
+        auto col_bytes = [&](int side, int nc) {
+            return a16(static_cast<size_t>(side + 3) * 2) + a16(static_cast<size_t>(nc) * 2) +
                    a16(static_cast<size_t>(nc) * elem_bytes);
         };
+        auto tab_bytes = [&](int R, int side, int nc) { return row_bytes(R) + col_bytes(side, nc); };
         // WFS chunks (same for every row group): greedy over w by the worst row group's bytes,
         // within a budget that keeps two gather CTAs per SM
         auto need_of = [&](int w, int l, int u) {
@@ -512,17 +516,17 @@ Plan build_plan(const Geometry& g, int elem_bytes, int batch, int wa = 0, int wb
         }
         gp.gchunk[++gp.nchunk] = wb;
         gp.chunk_bytes = static_cast<int>(chunk_max);
-        // gather tables per (layer, row group), WFS ascending, each WFS 16-byte aligned parts
-        //   [row src int16 R x KM][row w R x KM]                  padded row taps of the group
-        //   [first int16 side+3][col idx int16 nc][col frac nc]   compressed column stencil
-        // (mirrors k_gather() in cluster.cuh).  Row sources are relative to the group's psi
-        // block row ilo (zero-weight padding clamped into the block); column entries are
-        // the psi block columns jlo.. with their layer column idx and bilinear fraction f
-        // (layer column J receives 1-f from idx == J and f from idx == J-1, operators.hpp:
-        // 129-135); first[k] = first block column with idx >= k-1.
-        gp.o_gb = static_cast<int>(pl.ti.size());
-        pl.ti.resize(pl.ti.size() + static_cast<size_t>(L * kMaxGU), 0);
-        pl.td.resize(pl.ti.size(), 0.0);
+        // gather tables (mirrors k_gather() in cluster.cuh), in gblob:
+        //   column stencils, once per (layer, WFS), WFS ascending within a layer:
+        //     [first int16 side+3][col idx int16 nc][col frac nc]
+        //   row-tap tables per (layer, row group), WFS ascending:
+        //     [row src int16 R x KM][row w R x KM]   padded row taps of the group
+        // every part 16-byte aligned.  Row sources are relative to the group's psi block row
+        // ilo (zero-weight padding clamped into the block); column entries are the psi block
+        // columns jlo.. with their layer column idx and bilinear fraction f (layer column J
+        // receives 1-f from idx == J and f from idx == J-1, operators.hpp:129-135);
+        // first[k] = first block column with idx >= k-1.  The column stencil depends on the
+        // WFS and the layer only, so every row group of the layer stages the same copy.
         pl.gblob.clear();
         auto padded = [&](const std::vector<std::vector<Entry>>& tab, std::vector<int>& src, std::vector<double>& wt) {
             const int side = static_cast<int>(tab.size());
@@ -573,11 +577,50 @@ Plan build_plan(const Geometry& g, int elem_bytes, int batch, int wa = 0, int wb
             pl.gblob.insert(pl.gblob.end(), b, b + n);
         };
         auto pad16 = [&](size_t start) { pl.gblob.resize(start + a16(pl.gblob.size() - start), 0); };
+        // column stencils: jlo/jhi of a (w, l) are the same in every row group (bs[2], bs[3])
+        std::vector<size_t> coff_wl(static_cast<size_t>(W * L), 0);
+        for (int l = 0; l < L; ++l)
+            for (int w = 0; w < W; ++w) {
+                const int side = gp.side[l];
+                const int* bs = &pl.ti[static_cast<size_t>(gp.o_bs + ((w * L + l) * kMaxGU + 0) * 4)];
+                const int jlo = bs[2], nc = bs[3] - bs[2];
+                const auto& tx = colst[w * L + l];
+                const size_t start = pl.gblob.size();
+                coff_wl[static_cast<size_t>(w * L + l)] = start;
+                size_t p0 = pl.gblob.size();
+                for (int k = 0; k < side + 3; ++k) {
+                    int f0 = nc;
+                    for (int c = 0; c < nc; ++c)
+                        if (tx[static_cast<size_t>(jlo + c)].idx >= k - 1) { f0 = c; break; }
+                    const short v = static_cast<short>(f0);
+                    put_raw(&v, 2);
+                }
+                pad16(p0);
+                p0 = pl.gblob.size();
+                for (int c = 0; c < nc; ++c) {
+                    const short v = static_cast<short>(tx[static_cast<size_t>(jlo + c)].idx);
+                    put_raw(&v, 2);
+                }
+                pad16(p0);
+                p0 = pl.gblob.size();
+                for (int c = 0; c < nc; ++c) {
+                    const double fr = tx[static_cast<size_t>(jlo + c)].f;
+                    if (elem_bytes == 8) put_raw(&fr, 8);
+                    else {
+                        const float ff = static_cast<float>(fr);
+                        put_raw(&ff, 4);
+                    }
+                }
+                pad16(p0);
+                if (pl.gblob.size() - start != col_bytes(side, nc)) throw std::logic_error("gather tables: size mismatch");
+            }
+        // row-tap tables
+        std::vector<size_t> roff_lu(static_cast<size_t>(L * kMaxGU), 0);
         std::vector<int> rsrc;
         std::vector<double> rwt;
         for (int l = 0; l < L; ++l)
             for (int u = 0; u < gp.side[l] / grp_rows(gp.side[l]); ++u) {
-                pl.ti[static_cast<size_t>(gp.o_gb + l * kMaxGU + u)] = static_cast<int>(pl.gblob.size());
+                roff_lu[static_cast<size_t>(l * kMaxGU + u)] = pl.gblob.size();
                 const int side = gp.side[l];
                 const int Rl = grp_rows(side), I0 = u * Rl;
                 for (int w = 0; w < W; ++w) {
@@ -586,49 +629,20 @@ Plan build_plan(const Geometry& g, int elem_bytes, int batch, int wa = 0, int wb
                     padded(rows[w * L + l], rsrc, rwt);
                     put_i16(rsrc, I0, Rl, bs[0], bs[1] - bs[0]);
                     put_wt(rwt, I0, Rl);
-                    const auto& tx = colst[w * L + l];
-                    const int jlo = bs[2], nc = bs[3] - bs[2];
-                    size_t p0 = pl.gblob.size();
-                    for (int k = 0; k < side + 3; ++k) {
-                        int f0 = nc;
-                        for (int c = 0; c < nc; ++c)
-                            if (tx[static_cast<size_t>(jlo + c)].idx >= k - 1) { f0 = c; break; }
-                        const short v = static_cast<short>(f0);
-                        put_raw(&v, 2);
-                    }
-                    pad16(p0);
-                    p0 = pl.gblob.size();
-                    for (int c = 0; c < nc; ++c) {
-                        const short v = static_cast<short>(tx[static_cast<size_t>(jlo + c)].idx);
-                        put_raw(&v, 2);
-                    }
-                    pad16(p0);
-                    p0 = pl.gblob.size();
-                    for (int c = 0; c < nc; ++c) {
-                        const double fr = tx[static_cast<size_t>(jlo + c)].f;
-                        if (elem_bytes == 8) put_raw(&fr, 8);
-                        else {
-                            const float ff = static_cast<float>(fr);
-                            put_raw(&ff, 4);
-                        }
-                    }
-                    pad16(p0);
-                    if (pl.gblob.size() - start != tab_bytes(Rl, side, nc))
-                        throw std::logic_error("gather tables: size mismatch");
+                    if (pl.gblob.size() - start != row_bytes(Rl)) throw std::logic_error("gather tables: size mismatch");
                 }
             }
-        // staging descriptors per (layer, row group, WFS), 8 ints (mirrors GDesc in cluster.cuh):
+        // staging descriptors per (layer, row group, WFS), kGDescInts ints (mirrors GDesc in cluster.cuh):
         //   ilo ihi jlo jhi | psi source element offset | psi stage byte offset in its chunk |
-        //   table byte offset in gblob | table bytes
-        // In a chunk the tables of its WFS come first (one contiguous copy), then the psi blocks.
+        //   row table offset, bytes | column stencil offset, bytes | pad pad
+        // A chunk stages [its WFS's row tables | their column stencils | psi blocks].
         pl.ti.resize((pl.ti.size() + 3) & ~size_t(3), 0);  // int4-aligned
         gp.o_gd = static_cast<int>(pl.ti.size());
-        pl.ti.resize(pl.ti.size() + static_cast<size_t>(L * kMaxGU * kMaxW * 8), 0);
+        pl.ti.resize(pl.ti.size() + static_cast<size_t>(L * kMaxGU * kMaxW * kGDescInts), 0);
         pl.td.resize(pl.ti.size(), 0.0);
         for (int l = 0; l < L; ++l)
             for (int u = 0; u < gp.side[l] / grp_rows(gp.side[l]); ++u) {
-                size_t toff = static_cast<size_t>(pl.ti[static_cast<size_t>(gp.o_gb + l * kMaxGU + u)]);
-                for (int w = 0; w < wa; ++w) toff += need_of(w, l, u).first;  // tables of WFS this plan skips
+                const int Rl = grp_rows(gp.side[l]);
                 for (int k = 0; k < gp.nchunk; ++k) {
                     size_t tsum = 0;
                     for (int w = gp.gchunk[k]; w < gp.gchunk[k + 1]; ++w) tsum += need_of(w, l, u).first;
@@ -636,14 +650,15 @@ Plan build_plan(const Geometry& g, int elem_bytes, int batch, int wa = 0, int wb
                     for (int w = gp.gchunk[k]; w < gp.gchunk[k + 1]; ++w) {
                         const int* bs = &pl.ti[static_cast<size_t>(gp.o_bs + ((w * L + l) * kMaxGU + u) * 4)];
                         const auto nb = need_of(w, l, u);
-                        int* d = &pl.ti[static_cast<size_t>(gp.o_gd + ((l * kMaxGU + u) * kMaxW + w) * 8)];
+                        int* d = &pl.ti[static_cast<size_t>(gp.o_gd + ((l * kMaxGU + u) * kMaxW + w) * kGDescInts)];
                         d[0] = bs[0]; d[1] = bs[1]; d[2] = bs[2]; d[3] = bs[3];
                         d[4] = gp.woff[w] + bs[0] * (g.wfs[w].n_subap + 1);
                         d[5] = static_cast<int>(poff);
-                        d[6] = static_cast<int>(toff);
-                        d[7] = static_cast<int>(nb.first);
+                        d[6] = static_cast<int>(roff_lu[static_cast<size_t>(l * kMaxGU + u)] + static_cast<size_t>(w) * row_bytes(Rl));
+                        d[7] = static_cast<int>(row_bytes(Rl));
+                        d[8] = static_cast<int>(coff_wl[static_cast<size_t>(w * L + l)]);
+                        d[9] = static_cast<int>(col_bytes(gp.side[l], bs[3] - bs[2]));
                         poff += nb.second;
-                        toff += nb.first;
                     }
                 }
             }
