@@ -1079,8 +1079,19 @@ __device__ __forceinline__ void fwd_phase(const GeoParams& gp, const Bufs<T>& bf
     pdl_wait();  // y of the predecessor (the gather) is complete
     pdl_launch_dependents();
     // the band of y (one bulk copy into x1's space, then into the odd-pitch x0); thread 0
-    // issues every block and arrives at once (misaligned blocks: cooperative copies)
-    prefetch_block(bf.y + lbase + static_cast<size_t>(r0) * S, x1, R * S, &s_mbar[1], 0);
+    // issues every block and arrives at once (misaligned blocks: cooperative copies).
+    // Shard groups: the band is the rank-order sum of the members' partials, read
+    // directly from their buffers (the former k_exchange, fused here).
+    if (bf.nsum > 0) {
+        const size_t off = lbase + static_cast<size_t>(r0) * S;
+        for (int e = tid; e < R * S; e += nthr) {
+            T v = bf.ysum[0][off + e];
+            for (int r = 1; r < bf.nsum; ++r) v += bf.ysum[r][off + e];
+            x1[e] = v;
+        }
+    } else {
+        prefetch_block(bf.y + lbase + static_cast<size_t>(r0) * S, x1, R * S, &s_mbar[1], 0);
+    }
     if (tid == 0) mbar_arrive(&s_mbar[1]);
     if (tid >= 64 && tid < 64 + 16) s_ad[tid - 64] = my_ad;
     __syncthreads();  // s_ad, cooperative copies

@@ -125,6 +125,11 @@ struct Bufs {
     double* rho_log;   // [B][iters]
     int* status;       // [B]
     int* nlog;         // [B]
+    // per-WFS shard groups: the forward kernel stages y = sum_r ysum[r] (the
+    // members' partial adjoint layer sums, rank order; peer loads across devices) instead
+    // of y -- the exchange fused into the band staging (nsum = 0: off)
+    const T* ysum[kMaxW];
+    int nsum;
     // zero-copy frame outputs (page-locked host memory, written by k_fit_control; null: off)
     double* a_host;         // a1 [B][A] straight into the caller's buffer
     unsigned char* frame_host;  // mirror of the rho_log | status | nlog block

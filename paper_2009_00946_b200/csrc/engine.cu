@@ -1059,10 +1059,18 @@ struct EngineImpl {
     }
     int n_segments() const { return gp.iters + 2; }
 
+    // in-process shard group: the members' partial buffers of the previous segment, read
+    // by this member's next forward kernel (set by group_step_device)
+    std::vector<const void*> peer_sum;
+
     template <typename T, typename Mark>
     void launch_segment(int seg, cudaStream_t st, Mark&& mark) {
         Bufs<T> bf = frame_bufs<T>();
         const int B = batch, it = gp.iters;
+        if (seg >= 1 && !peer_sum.empty()) {
+            bf.nsum = static_cast<int>(peer_sum.size());
+            for (size_t r = 0; r < peer_sum.size(); ++r) bf.ysum[r] = static_cast<const T*>(peer_sum[r]);
+        }
         auto gather = [&] {
             Bufs<T> gb = bf;
             if (sharded) gb.y = static_cast<T*>(ypart[static_cast<size_t>(seg)]);  // partial sums
@@ -1563,11 +1571,13 @@ void* Engine::shard_partial(int seg) const {
 }
 
 // In-process shard group (one process driving the members, on one device or on
-// several with peer access): segments in lockstep on every member's stream, the
-// exchange of segment k a fixed-order sum of all members' partials (k_exchange)
-// after every member's segment k (cross-stream events).  Each member's partial
-// buffer of segment k is rewritten only in the next frame, after every member
-// passed exchange k, so no buffer is read and rewritten concurrently.
+// several with peer access): segments in lockstep on every member's stream; the
+// exchange after segment k is fused into every member's next forward kernel, which
+// stages its y band as the rank-order sum of all members' partial buffers of segment
+// k (cluster.cuh fwd_phase; NVLink peer loads across devices) after waiting for every
+// member's segment k (cross-stream events).  A member's partial buffer of segment k is
+// rewritten only in the next frame, after every member's last segment, which waited for
+// all segments >= k+1, so no buffer is read and rewritten concurrently.
 void group_step_device(const std::vector<Engine*>& members) {
     const int world = static_cast<int>(members.size());
     if (world < 1 || world > kMaxW) throw ArgError("shard group: 1..16 members");
@@ -1591,44 +1601,40 @@ void group_step_device(const std::vector<Engine*>& members) {
                 if (pe == cudaErrorPeerAccessAlreadyEnabled) (void)cudaGetLastError();
             }
     }
-    std::vector<cudaEvent_t> ev(static_cast<size_t>(world));
+    // two event sets (segment parity): member r's segment s waits for every member's
+    // segment s-1, whose gathers wrote the partial sums its forward kernel reads
+    std::vector<cudaEvent_t> ev(2 * static_cast<size_t>(world));
     for (int r = 0; r < world; ++r) {
         CK(cudaSetDevice(m[static_cast<size_t>(r)]->device));
-        CK(cudaEventCreateWithFlags(&ev[static_cast<size_t>(r)], cudaEventDisableTiming));
+        for (int e = 0; e < 2; ++e)
+            CK(cudaEventCreateWithFlags(&ev[static_cast<size_t>(e * world + r)], cudaEventDisableTiming));
     }
     auto run = [&](auto tag) {
         using T = decltype(tag);
-        const int nseg = m[0]->n_segments(), iters = m[0]->gp.iters;
-        const long long n_el = static_cast<long long>(m[0]->gp.n) * m[0]->batch;
-        const long long n_vec = n_el / (16 / static_cast<long long>(sizeof(T)));
+        const int nseg = m[0]->n_segments();
         for (int seg = 0; seg < nseg; ++seg) {
+            const int cur = seg & 1, prv = cur ^ 1;
             for (int r = 0; r < world; ++r) {
                 auto* P = m[static_cast<size_t>(r)];
                 CK(cudaSetDevice(P->device));
+                P->peer_sum.clear();
+                if (seg >= 1) {  // y of this segment's forward = sum of segment seg-1's partials
+                    for (int q = 0; q < world; ++q) {
+                        if (q != r) CK(cudaStreamWaitEvent(P->s(), ev[static_cast<size_t>(prv * world + q)], 0));
+                        P->peer_sum.push_back(m[static_cast<size_t>(q)]->ypart[static_cast<size_t>(seg - 1)]);
+                    }
+                }
                 P->launch_segment<T>(seg, P->s(), [](int) {});
-                CK(cudaEventRecord(ev[static_cast<size_t>(r)], P->s()));
+                P->peer_sum.clear();
+                CK(cudaEventRecord(ev[static_cast<size_t>(cur * world + r)], P->s()));
             }
-            if (seg > iters) break;
-            PeerParts parts{};
-            parts.world = world;
-            for (int r = 0; r < world; ++r) parts.p[r] = m[static_cast<size_t>(r)]->ypart[static_cast<size_t>(seg)];
-            for (int r = 0; r < world; ++r) {
-                auto* P = m[static_cast<size_t>(r)];
-                CK(cudaSetDevice(P->device));
-                for (int q = 0; q < world; ++q)
-                    if (q != r) CK(cudaStreamWaitEvent(P->s(), ev[static_cast<size_t>(q)], 0));
-                const int grid = static_cast<int>(std::min<long long>((n_vec + 255) / 256, 148 * 8));
-                k_exchange<T><<<grid, 256, 0, P->s()>>>(parts, P->state<T>().bf.y, n_vec);
-                CK(cudaGetLastError());
-            }
-            // the events are re-recorded by the next segment; the waits above already captured them
         }
     };
     if (m[0]->precision == 64) run(double{});
     else run(float{});
     for (int r = 0; r < world; ++r) {
         CK(cudaSetDevice(m[static_cast<size_t>(r)]->device));
-        CK(cudaEventDestroy(ev[static_cast<size_t>(r)]));
+        for (int e = 0; e < 2; ++e) CK(cudaEventDestroy(ev[static_cast<size_t>(e * world + r)]));
     }
 }
 

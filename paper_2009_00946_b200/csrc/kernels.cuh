@@ -654,35 +654,4 @@ __global__ void k_convert(const Src* in, Dst* out, size_t n) {
 }
 
 
-// ---------------------------------------------------------------------------
-// Per-WFS sharding: y = sum_r ypart_r, the adjoint layer sums of
-// the shard group's members added in rank order (identical on every member, so
-// the replicated PCG state stays bitwise equal).  `parts` holds the members'
-// partial buffers: local on one device, NVLink peer loads across devices with
-// peer access enabled.  16-byte vector loads; n_vec = elements / (16/sizeof(T)).
-// ---------------------------------------------------------------------------
-struct PeerParts {
-    const void* p[kMaxW];
-    int world;
-};
-
-template <typename T>
-__global__ void __launch_bounds__(256) k_exchange(const PeerParts parts, T* __restrict__ y, long long n_vec) {
-    using V = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
-    constexpr int E = 16 / sizeof(T);
-    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n_vec;
-         i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const V* p0 = static_cast<const V*>(parts.p[0]);
-        V acc = p0[i];
-        T* a = reinterpret_cast<T*>(&acc);
-        for (int r = 1; r < parts.world; ++r) {
-            const V v = static_cast<const V*>(parts.p[r])[i];
-            const T* b = reinterpret_cast<const T*>(&v);
-#pragma unroll
-            for (int e = 0; e < E; ++e) a[e] += b[e];
-        }
-        reinterpret_cast<V*>(y)[i] = acc;
-    }
-}
-
 }  // namespace fewha_gpu
