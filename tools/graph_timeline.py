@@ -18,6 +18,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import paper_2009_00946_b200 as fg  # noqa: E402
 
+if os.environ.get("FEWHA_LIB"):  # A/B of library builds
+    fg.LIB_PATH = os.environ["FEWHA_LIB"]
+
 ap = argparse.ArgumentParser()
 ap.add_argument("--preset", default=os.path.join(ROOT, "presets", "elt_mcao84_3dm.json"))
 ap.add_argument("--frames", type=int, default=20)
