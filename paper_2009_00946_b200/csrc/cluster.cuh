@@ -38,8 +38,7 @@ namespace cg = cooperative_groups;
 __device__ __forceinline__ void stamp(const GeoParams& gp, int k) {
     if (gp.stamps == nullptr || threadIdx.x != 0) return;
     unsigned long long t;
-    if (gp.stamp_clock) t = clock64();  // FEWHA_STAMP_CLOCK=1: SM cycles (per-CTA deltas)
-    else asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     const unsigned blk = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
     gp.stamps[blk * 16 + k] = t;
 }

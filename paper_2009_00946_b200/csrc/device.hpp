@@ -72,7 +72,6 @@ struct GeoParams {
     int o_bs;         // [((w*L+l)*kMaxGU + u)*4] psi source block {ilo, ihi, jlo, jhi} of each gather row group
     int bd_rows_max, bd_cols_max;
     unsigned long long* stamps;  // optional phase timestamps [block][16] (nullptr: off)
-    int stamp_clock;             // stamps record the SM clock (cycles) instead of %globaltimer
     const unsigned char* gblob;  // per-(w,l) gather blobs of the engine's precision (see cluster.cuh)
     int chunk_bytes;  // shared-memory bytes of the largest staged WFS chunk of the gather
     int nchunk;                 // WFS chunks of the gather: [gchunk[k], gchunk[k+1])

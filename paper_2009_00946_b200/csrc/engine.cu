@@ -946,7 +946,6 @@ struct EngineImpl {
         GeoParams g2 = gpf;
         if (stamp_slot >= 0 && stamp_slot < kStampSlots) {
             g2.stamps = stamp_buf + static_cast<size_t>(stamp_slot++) * kStampBlocks * 16;
-            g2.stamp_clock = std::getenv("FEWHA_STAMP_CLOCK") != nullptr ? 1 : 0;
         }
         return g2;
     }
