@@ -17,6 +17,7 @@
 #include "daubechies_table.h"
 #include "device.hpp"
 #include "cluster.cuh"
+#include "layer_whole.cuh"
 #include "clayout.hpp"
 #include "launch.hpp"
 #include "nccl_dl.hpp"
@@ -836,6 +837,13 @@ struct Launch {
         FEWHA_FLEN_SWITCH(flen, FEWHA_LAUNCH)
 #undef FEWHA_LAUNCH
     }
+    // whole-layer kernels (batched plans): grid (L, count)
+    static void whole(int flen, bool inverse, const GeoParams& gp, const Bufs<T>& bf, int mode, int it, int count,
+                      cudaStream_t st, int fit_term = 1) {
+#define FEWHA_LAUNCH(N) CK((launch_layer_whole<T, N>(inverse, gp, bf, mode, it, count, st, fit_term)))
+        FEWHA_FLEN_SWITCH(flen, FEWHA_LAUNCH)
+#undef FEWHA_LAUNCH
+    }
     // fused forward (fmode, fit) + inverse (imode, iit): one cooperative cluster launch
     static void fused(int flen, const GeoParams& gp, const Bufs<T>& bf, int fmode, int fit, int imode, int iit,
                       int count, cudaStream_t st, unsigned long long* bar) {
@@ -937,7 +945,10 @@ struct EngineImpl {
     // monotonic barrier counters
     bool fuse_ok = false;
     unsigned long long* fbar = nullptr;
-    bool fused_frame() const { return fuse_ok && !telemetry_on && !(sharded && !comm); }
+    // batched plans: layer transforms one CTA per (layer, instance) (layer_whole.cuh)
+    bool whole_layer = false;
+    bool use_whole() const { return whole_layer && !sharded && peer_sum.empty(); }
+    bool fused_frame() const { return fuse_ok && !whole_layer && !telemetry_on && !(sharded && !comm); }
     // optional per-phase timestamps of the cluster kernels (profiling only)
     unsigned long long* stamp_buf = nullptr;
     int stamp_slot = -1;  // < 0: stamping off
@@ -1071,6 +1082,11 @@ struct EngineImpl {
             bf.nsum = static_cast<int>(peer_sum.size());
             for (size_t r = 0; r < peer_sum.size(); ++r) bf.ysum[r] = static_cast<const T*>(peer_sum[r]);
         }
+        const bool wl = use_whole();
+        auto layer = [&](bool inverse, int mode, int k) {
+            if (wl) Launch<T>::whole(flen, inverse, gps(), bf, mode, k, B, st);
+            else Launch<T>::cl(flen, inverse, gps(), bf, mode, k, B, st);
+        };
         auto gather = [&] {
             Bufs<T> gb = bf;
             if (sharded) gb.y = static_cast<T*>(ypart[static_cast<size_t>(seg)]);  // partial sums
@@ -1101,15 +1117,15 @@ struct EngineImpl {
         }
         // W of the previous gather: the RHS (r += b1 - b) or PCG iteration seg-2
         if (seg == 1) {
-            Launch<T>::cl(flen, false, gps(), bf, kRhs, 0, B, st);
+            layer(false, kRhs, 0);
             mark(kKindFwdRhs);
         } else {
-            Launch<T>::cl(flen, false, gps(), bf, kPcg, seg - 2, B, st);
+            layer(false, kPcg, seg - 2);
             mark(kKindFwdPcg);
         }
         if (seg <= it) {  // fused PCG (pcg.hpp:68-106): update of k-1 fused into k's W^-1
             const int k = seg - 1;
-            Launch<T>::cl(flen, true, gps(), bf, kPcg, k, B, st);
+            layer(true, kPcg, k);
             mark(k == 0 ? kKindInvPcg0 : kKindInvPcg);
             Launch<T>::wfs(false, gps(), bf, 0, B, st);
             mark(kKindWfs);
@@ -1117,7 +1133,7 @@ struct EngineImpl {
             return;
         }
         // last update + fitting W^-1 c, then fit + control + rotation
-        Launch<T>::cl(flen, true, gps(), bf, kFit, 0, B, st);
+        layer(true, kFit, 0);
         mark(kKindInvFit);
         Launch<T>::fit(gpf, bf, 1, B, st);
         mark(kKindFit);
@@ -1442,6 +1458,15 @@ Engine::Engine(Geometry g, int precision, int batch, int device) : p_(std::make_
             const int cap = precision == 64 ? Launch<double>::fused_capacity(P.gp, P.flen, batch)
                                             : Launch<float>::fused_capacity(P.gp, P.flen, batch);
             P.fuse_ok = cap >= P.gp.L * batch;
+        }
+        // whole-layer transforms for batches (> 2 instances) when a layer fits one CTA's
+        // shared memory; FEWHA_WHOLE_LAYER=0/1 overrides (tests, A/B)
+        {
+            int maxopt = 0;
+            CK(cudaDeviceGetAttribute(&maxopt, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+            const bool fits = whole_layer_smem(P.gp.maxside, precision / 8) + 1024 <= static_cast<size_t>(maxopt);
+            const char* wv = std::getenv("FEWHA_WHOLE_LAYER");
+            P.whole_layer = fits && (wv ? wv[0] == '1' : batch > 2);
         }
         P.fbar = dalloc<unsigned long long>(static_cast<size_t>(batch));
         P.fr.add(P.fbar);
@@ -1907,6 +1932,7 @@ PlanInfo Engine::plan_info() const {
     pi.wfs_ctas_per_sm = P.batch <= 2 ? FEWHA_WFS_MINB_LAT : FEWHA_WFS_MINB_BATCH;
     pi.wfs_tiles = P.gp.wt_count;
     pi.launches_per_step = launches_per_step();
+    pi.whole_layer = P.use_whole() ? 1 : 0;
     return pi;
 }
 

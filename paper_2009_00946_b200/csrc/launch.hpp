@@ -24,6 +24,10 @@ template <typename T, int FLEN>
 cudaError_t fused_cluster_capacity(const GeoParams& gp, size_t smem, int* clusters);
 
 template <typename T, int FLEN>
+cudaError_t launch_layer_whole(bool inverse, const GeoParams& gp, const Bufs<T>& bf, int mode, int it, int count,
+                               cudaStream_t st, int fit_term);
+
+template <typename T, int FLEN>
 cudaError_t set_layer_cluster_attrs(size_t smem_inv, size_t smem_fwd);
 
 }  // namespace fewha_gpu

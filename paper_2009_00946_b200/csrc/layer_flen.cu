@@ -3,6 +3,7 @@
 
 #include "cluster.cuh"
 #include "launch.hpp"
+#include "layer_whole.cuh"
 
 #ifndef FEWHA_FLEN
 #error "compile with -DFEWHA_FLEN=<2|4|...|20>"
@@ -30,6 +31,25 @@ cudaError_t launch_layer_cluster(bool inverse, const GeoParams& gp, const Bufs<T
     cfg.numAttrs = 2;
     if (inverse) return cudaLaunchKernelEx(&cfg, k_inv_cluster<T, FLEN>, gp, bf, mode, it);
     return cudaLaunchKernelEx(&cfg, k_fwd_cluster<T, FLEN>, gp, bf, mode, it, fit_term);
+}
+
+// Whole-layer kernels of batched plans (layer_whole.cuh): grid (L, count), no cluster.
+template <typename T, int FLEN>
+cudaError_t launch_layer_whole(bool inverse, const GeoParams& gp, const Bufs<T>& bf, int mode, int it, int count,
+                               cudaStream_t st, int fit_term) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(gp.L, count, 1);
+    cfg.blockDim = dim3(kWlThreads, 1, 1);
+    cfg.dynamicSmemBytes = whole_layer_smem(gp.maxside, static_cast<int>(sizeof(T)));
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    const char* pdl = std::getenv("FEWHA_PDL");
+    attr[0].val.programmaticStreamSerializationAllowed = (pdl && pdl[0] == '0') ? 0 : 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (inverse) return cudaLaunchKernelEx(&cfg, k_inv_layer<T, FLEN>, gp, bf, mode, it);
+    return cudaLaunchKernelEx(&cfg, k_fwd_layer<T, FLEN>, gp, bf, mode, it, fit_term);
 }
 
 // Fused forward + inverse (k_fwd_inv_cluster): the cluster grid launched
@@ -94,6 +114,10 @@ cudaError_t set_layer_cluster_attrs(size_t smem_inv, size_t smem_fwd) {
     }
     cudaError_t e = opt_in_max(k_inv_cluster<T, FLEN>, smem_inv);
     if (e != cudaSuccess) return e;
+    e = opt_in_max(k_inv_layer<T, FLEN>, smem_inv);
+    if (e != cudaSuccess) return e;
+    e = opt_in_max(k_fwd_layer<T, FLEN>, smem_fwd);
+    if (e != cudaSuccess) return e;
     e = opt_in_max(k_fwd_inv_cluster<T, FLEN>, smem_fwd);
     if (e != cudaSuccess) return e;
     return opt_in_max(k_fwd_cluster<T, FLEN>, smem_fwd);
@@ -106,6 +130,8 @@ cudaError_t set_layer_cluster_attrs(size_t smem_inv, size_t smem_fwd) {
                                                              int, cudaStream_t, int, size_t, unsigned long long*, \
                                                              int);                                              \
     template cudaError_t fused_cluster_capacity<T, FEWHA_FLEN>(const GeoParams&, size_t, int*);                 \
+    template cudaError_t launch_layer_whole<T, FEWHA_FLEN>(bool, const GeoParams&, const Bufs<T>&, int, int, int,   \
+                                                           cudaStream_t, int);                                  \
     template cudaError_t set_layer_cluster_attrs<T, FEWHA_FLEN>(size_t, size_t);
 FEWHA_INST(double)
 FEWHA_INST(float)

@@ -168,8 +168,12 @@ def test_single_step_from_injected_state(oracles):
         assert rel_err(st_g[key], st_o[key]) <= 1e-10, key
 
 
-def test_bitwise_deterministic_and_batch_equivalent():
-    """Run-to-run bitwise determinism; batch instances == independent runs."""
+@pytest.mark.parametrize("whole", ["0", "1"])
+def test_bitwise_deterministic_and_batch_equivalent(whole, monkeypatch):
+    """Run-to-run bitwise determinism; batch instances == independent runs (cluster
+    transforms, whole = 0; whole-layer transforms for batch and single engines alike,
+    whole = 1)."""
+    monkeypatch.setenv("FEWHA_WHOLE_LAYER", whole)
     gd = np.load(os.path.join(GOLD, "small_mcao.npz"))
     meas = gd["loop_meas"]
     rng = np.random.default_rng(4)
@@ -387,6 +391,56 @@ def test_transforms_mixed_sides_and_orders(case, tmp_path, precision):
             tol_a = max(STEP_TOL[64], 10.0 * sens_a)
             assert rel_err(g.coeffs(), c_o) <= tol_c, ("c", k, rel_err(g.coeffs(), c_o), tol_c)
             assert rel_err(a_g, a_o) <= tol_a, ("a", k, rel_err(a_g, a_o), tol_a)
+
+
+@pytest.mark.parametrize("case", sorted(TRANSFORM_VARIANTS))
+def test_whole_layer_frames_mixed_sides_and_orders(case, tmp_path, precision, monkeypatch):
+    """The batched plans' whole-layer transform kernels (one CTA per layer and
+    instance, layer_whole.cuh) on the same layer-side / wavelet-order variants:
+    closed-loop frames of a 3-instance engine, each instance started from the
+    oracle's state (injected) on its own slope stream, against the oracle; the
+    tolerance as in the cluster test above (the coarse dense-sampling layers make the
+    reference's own frame ill-conditioned)."""
+    monkeypatch.setenv("FEWHA_WHOLE_LAYER", "1")
+    base, orders, wav = TRANSFORM_VARIANTS[case]
+    path = _variant(tmp_path, base, case, orders, wav)
+    try:
+        g = fg.Reconstructor(path, precision=precision, batch=3)
+    except fg.ConfigError as e:
+        pytest.skip(f"geometry not supported by the gather tables: {e}")
+    assert g.plan_info()["whole_layer"] == 1
+    B = 3
+    o = Oracle(path)
+    o.build_preconditioner()
+    g.build_preconditioner()
+    o2 = Oracle(path)
+    o2.build_preconditioner()
+    lay = [smooth_layers(o, 3 + i) for i in range(B)]
+    for k in range(2):
+        ss, refs, tols = [], [], []
+        for i in range(B):
+            s = noisy_slopes(o, lay[i], 100 + 7 * i + k, o.get_state()["a_prev2"])
+            st0 = o.get_state()
+            g.set_state(st0, instance=i)
+            c_o, a_o, rho_o = o.step(s)
+            o.set_state(st0)  # every instance starts from the same oracle state
+            sens_c = sens_a = 0.0
+            if precision == 64:
+                for j in range(2):
+                    o2.set_state(st0)
+                    jit = 1.0 + 1e-15 * np.random.default_rng(10 * k + j).standard_normal(s.shape)
+                    c_p, a_p, _ = o2.step(s * jit)
+                    sens_c, sens_a = max(sens_c, rel_err(c_p, c_o)), max(sens_a, rel_err(a_p, a_o))
+            ss.append(s)
+            refs.append((c_o, a_o, rho_o))
+            tols.append((max(STEP_TOL[precision], 10.0 * sens_c), max(STEP_TOL[precision], 10.0 * sens_a)))
+        a_g = g.step(np.stack(ss))
+        c_g = g.coeffs()
+        for i in range(B):
+            c_o, a_o, rho_o = refs[i]
+            assert rel_err(c_g[i], c_o) <= tols[i][0], ("c", k, i, rel_err(c_g[i], c_o), tols[i][0])
+            assert rel_err(a_g[i], a_o) <= tols[i][1], ("a", k, i, rel_err(a_g[i], a_o), tols[i][1])
+        o.step(ss[0])  # advance the oracle's loop state with instance 0's frame
 
 
 def test_step_telemetry():

@@ -56,6 +56,7 @@ def test_elt_batch_plan_per_instance_vs_oracle(precision):
     g = fg.Reconstructor(preset(name + ".json"), precision=precision, batch=B)
     plan = g.plan_info()
     assert plan["tail"] == 2 * plan["cluster_ctas"] and plan["inverse_staged"] == 0
+    assert plan["whole_layer"] == 1  # batches: whole-layer transforms (layer_whole.cuh)
     assert plan["gather_rows"] == 8 and plan["gather_ctas_per_sm"] == 3 and plan["wfs_ctas_per_sm"] == 4
     orc = [_oracle(name) for _ in range(B)]
     lay = [smooth_layers(orc[0], 30 + i) for i in range(B)]
@@ -75,8 +76,9 @@ def test_elt_batch_plan_per_instance_vs_oracle(precision):
             assert rel_err(g.last_rho[i], rho_o) <= tol, ("rho", k, i, rel_err(g.last_rho[i], rho_o))
 
 
+@pytest.mark.parametrize("whole", ["0", "1"])
 @pytest.mark.parametrize("precision", [64, 32])
-def test_batch_plan_instances_are_bitwise_single_engines(precision, monkeypatch):
+def test_batch_plan_instances_are_bitwise_single_engines(precision, whole, monkeypatch):
     """Every instance of the batch plan equals an independent single-instance
     engine bit for bit once that engine uses the same transform tail: the gather
     row groups and residency (4 vs 8 rows, 2 vs 3 CTAs/SM), the WFS-kernel
@@ -84,10 +86,14 @@ def test_batch_plan_instances_are_bitwise_single_engines(precision, monkeypatch)
     never an arithmetic order.  (The tail size itself moves the 32^2 level between
     the rank-0 tail and the distributed levels, where the compiler may contract
     the filter sums differently: 1e-16-level differences, covered against the
-    oracle by the other tests here.)  10 closed-loop ELT frames."""
+    oracle by the other tests here.)  whole = 1: the whole-layer transforms of the batch
+    plan, and single engines forced onto them; whole = 0: the batch plan on cluster
+    transforms.  10 closed-loop ELT frames."""
     path = preset("elt_mcao84_3dm.json")
     B = 4
+    monkeypatch.setenv("FEWHA_WHOLE_LAYER", whole)
     gb = fg.Reconstructor(path, precision=precision, batch=B)
+    assert gb.plan_info()["whole_layer"] == int(whole)
     monkeypatch.setenv("FEWHA_TAIL", str(gb.plan_info()["tail"]))
     singles = [fg.Reconstructor(path, precision=precision) for _ in range(B)]
     p1, pb = singles[0].plan_info(), gb.plan_info()
