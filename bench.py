@@ -314,6 +314,7 @@ def graph_function_profile(rec, frames, before, d, b, batch=1):
     before(f) runs ahead of frame f (slope load, L2 flush).  Returns
     {function: {launches, ms_per_frame, bytes_per_frame, ...}} and the frame ms."""
     rec.enable_telemetry(True)
+    whole = rec.plan_info().get("whole_layer", 0) == 1  # batched plans: whole-layer transform kernels
     acc, frame_ms = {}, []
     for f in range(frames + 2):
         before(f)
@@ -324,6 +325,8 @@ def graph_function_profile(rec, frames, before, d, b, batch=1):
         frame_ms.append(sum(t for _, t in lt))
         for kind, t in lt:
             fn = FUNC[kind]
+            if whole and fn in ("k_fwd_cluster", "k_inv_cluster"):
+                fn = fn.replace("_cluster", "_layer")
             e = acc.setdefault(fn, {"launches": 0, "ms": 0.0, "bytes": 0})
             e["launches"] += 1
             e["ms"] += t
@@ -541,6 +544,7 @@ def run_ours(args):
         B = 64
         fb = frame_bytes(d, b) * B
         KB = 30
+        plan_b = {}
 
         def time_split(parts):
             """64 instances per step as `parts` engines of 64/parts on their own streams."""
@@ -572,6 +576,7 @@ def run_ours(args):
             e1.record(st)
             torch.cuda.synchronize(dev)
             prof_b = None
+            plan_b.update(engs[0][0].plan_info())
             if parts == 1:  # per-function HBM roofline where the working set exceeds L2
                 engs[0][0].set_stream(st.cuda_stream)
                 prof_b, _ = graph_function_profile(engs[0][0], 3, lambda f: None, d, b, batch=B)
@@ -589,6 +594,8 @@ def run_ours(args):
                       "roofline_frac_frame_model": round(fb / (bms / 1000.0) / 1e9 / peak, 4),
                       "engines": 1 if one <= two else 2,
                       "ms_per_step_1x64": round(one, 4), "ms_per_step_2x32_two_streams": round(two, 4),
+                      "transforms": "whole-layer kernels (one CTA per layer and instance)" if plan_b.get("whole_layer")
+                      else "cluster kernels",
                       "roofline": roof_b,
                       "note": "64 instances per step, inputs resident, no flush between steps "
                               "(working set 64 x ~15 MB > L2); best of one 64-instance engine and two "

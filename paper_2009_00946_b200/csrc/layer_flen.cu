@@ -39,7 +39,7 @@ cudaError_t launch_layer_whole(bool inverse, const GeoParams& gp, const Bufs<T>&
                                cudaStream_t st, int fit_term) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(gp.L, count, 1);
-    cfg.blockDim = dim3(kWlThreads, 1, 1);
+    cfg.blockDim = dim3(Wl<T>::threads, 1, 1);
     cfg.dynamicSmemBytes = whole_layer_smem(gp.maxside, static_cast<int>(sizeof(T)));
     cfg.stream = st;
     cudaLaunchAttribute attr[1];

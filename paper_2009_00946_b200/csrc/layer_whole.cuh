@@ -18,7 +18,13 @@
 
 namespace fewha_gpu {
 
-constexpr int kWlThreads = 512;
+// Threads per CTA and resident CTAs per SM: the fp64 layer (132 KB at 128^2) allows one
+// CTA per SM, so 512 threads; the fp32 layer (66 KB) three, at 256 threads each.
+template <typename T>
+struct Wl {
+    static constexpr int threads = sizeof(T) == 8 ? 512 : 256;
+    static constexpr int minb = sizeof(T) == 8 ? 1 : 3;
+};
 
 // Visit every coefficient of layer side S in rank-blocked HBM order (coeff_perm,
 // engine.cu): f(o, row, col) with o the index inside the layer block and (row, col) its
@@ -129,7 +135,7 @@ __host__ __device__ constexpr size_t whole_layer_smem(int maxside, int elem) {
 // Inverse: grid (L, B).  kPlain: phi = W^-1 in; kPcg: [update it-1] z = r/J, rho
 // partial, phi = W^-1 z; kFit: [final update] phi = W^-1 c.
 template <typename T, int FLEN>
-__global__ void __launch_bounds__(kWlThreads, 1) k_inv_layer(const GeoParams gp, const Bufs<T> bf, int mode, int it) {
+__global__ void __launch_bounds__(Wl<T>::threads, Wl<T>::minb) k_inv_layer(const GeoParams gp, const Bufs<T> bf, int mode, int it) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ double s_red[32];
     __shared__ double s_beta, s_alpha;
@@ -272,7 +278,7 @@ __global__ void __launch_bounds__(kWlThreads, 1) k_inv_layer(const GeoParams gp,
 
 // Forward: grid (L, B).  buf <- y; W y in place; epilogue per mode (as fwd_phase).
 template <typename T, int FLEN>
-__global__ void __launch_bounds__(kWlThreads, 1) k_fwd_layer(const GeoParams gp, const Bufs<T> bf, int mode, int it,
+__global__ void __launch_bounds__(Wl<T>::threads, Wl<T>::minb) k_fwd_layer(const GeoParams gp, const Bufs<T> bf, int mode, int it,
                                                              int fit_term) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ double s_red[32];
@@ -287,7 +293,7 @@ __global__ void __launch_bounds__(kWlThreads, 1) k_fwd_layer(const GeoParams gp,
     pdl_wait();  // y of the predecessor (the gather) is complete
     pdl_launch_dependents();
     const T* __restrict__ y = bf.y + lbase;
-    if (S * S % (4 * kWlThreads) == 0 && S >= 4) {  // 4 vector loads in flight per thread per pass
+    if (S * S % (4 * Wl<T>::threads) == 0 && S >= 4) {  // 4 vector loads in flight per thread per pass
         constexpr int U = 4;
         for (int e0 = 4 * tid; e0 < S * S; e0 += 4 * U * blockDim.x) {
             Vec4<T> v[U];
