@@ -476,11 +476,11 @@ class Reconstructor:
         if enable_only:
             self._chk(-min(0, self._L.fewha_gpu_phase_stamps(self._h, None, 0)))
             return None
-        out = np.zeros(32 * 4096 * 16, np.uint64)
+        out = np.zeros(32 * 16384 * 16, np.uint64)
         n = self._L.fewha_gpu_phase_stamps(self._h, out.ctypes.data_as(C.c_void_p), out.size)
         if n < 0:
             self._chk(-n)
-        return out.reshape(32, 4096, 16)
+        return out.reshape(32, 16384, 16)
 
     KERNEL_KINDS = ("wfs_rhs", "adjoint", "fwd_rhs", "inv_pcg0", "inv_pcg", "wfs", "fwd_pcg", "inv_fit", "fit_control", "gather",
                     "fwd_rhs_inv0", "fwd_inv_pcg", "fwd_inv_fit")

@@ -952,7 +952,7 @@ struct EngineImpl {
     // optional per-phase timestamps of the cluster kernels (profiling only)
     unsigned long long* stamp_buf = nullptr;
     int stamp_slot = -1;  // < 0: stamping off
-    static constexpr int kStampSlots = 32, kStampBlocks = 4096;
+    static constexpr int kStampSlots = 32, kStampBlocks = 16384;
     GeoParams gps() {
         GeoParams g2 = gpf;
         if (stamp_slot >= 0 && stamp_slot < kStampSlots) {

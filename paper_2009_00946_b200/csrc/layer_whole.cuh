@@ -128,8 +128,12 @@ __device__ __forceinline__ void st4(T* p, const Vec4<T>& r) {
     }
 }
 
+// The coarse corner (levels <= kWlCorner) runs as fused 2-D passes (tail_forward /
+// tail_inverse, one CTA barrier per level instead of four) on a small scratch.
+constexpr int kWlCorner = 16;
+__host__ __device__ constexpr int wl_scratch_elems() { return 3 * kWlCorner * (kWlCorner + 1) + kWlCorner * kWlCorner; }
 __host__ __device__ constexpr size_t whole_layer_smem(int maxside, int elem) {
-    return static_cast<size_t>(maxside) * (maxside + 1) * elem;
+    return (static_cast<size_t>(maxside) * (maxside + 1) + wl_scratch_elems()) * elem;
 }
 
 // Inverse: grid (L, B).  kPlain: phi = W^-1 in; kPcg: [update it-1] z = r/J, rho
@@ -147,6 +151,7 @@ __global__ void __launch_bounds__(Wl<T>::threads, Wl<T>::minb) k_inv_layer(const
     const int slots = gp.L * C;
     const int upd = mode == kFit ? gp.iters : it;
     const int ci = b * (gp.iters + 1) + upd - 1;
+    stamp(gp, 0);
     __shared__ int s_off[kMaxLev + 1];
     const LayerMap lm = layer_map(S, C, D, s_off);  // (published by the barrier below)
     pdl_wait();  // the predecessor's outputs (Mz, mu partials; r at it = 0) are complete
@@ -175,6 +180,7 @@ __global__ void __launch_bounds__(Wl<T>::threads, Wl<T>::minb) k_inv_layer(const
         }
     }
     __syncthreads();
+    stamp(gp, 1);
     double racc = 0.0;
     if (mode == kPlain) {
         const T* in = bf.in + lbase;
@@ -267,13 +273,30 @@ __global__ void __launch_bounds__(Wl<T>::threads, Wl<T>::minb) k_inv_layer(const
     } else {
         __syncthreads();
     }
-    for (int s = 2; s <= S; s <<= 1) {  // columns, then rows (wavelet.hpp:170-196)
+    stamp(gp, 2);
+    int s0 = 2;
+    if (S >= kWlCorner) {  // levels 2..kWlCorner: fused 2-D passes on the corner copy
+        constexpr int K = kWlCorner;
+        T* zt = buf + S * P;  // K x K coefficients (pitch K), then two (K+1)-pitch buffers
+        T* b0 = zt + K * K;
+        T* b1 = b0 + K * (K + 1);
+        for (int e = tid; e < K * K; e += blockDim.x) zt[e] = buf[(e / K) * P + (e % K)];
+        __syncthreads();
+        const T* co = tail_inverse<T, FLEN>(gp, zt, K, b0, b1);
+        for (int e = tid; e < K * K; e += blockDim.x) buf[(e / K) * P + (e % K)] = co[(e / K) * (K + 1) + (e % K)];
+        __syncthreads();
+        s0 = 2 * K;
+    }
+    for (int s = s0; s <= S; s <<= 1) {  // columns, then rows (wavelet.hpp:170-196)
         synthesis_lines<T, FLEN, true>(buf, P, s, s, gp);
         synthesis_lines<T, FLEN, false>(buf, P, s, s, gp);
+        if (s == S / 2) stamp(gp, 3);
     }
+    stamp(gp, 4);
     T* __restrict__ phi = bf.phi + lbase;
     const int ls = ilog2(S);
     for (int e = tid; e < S * S; e += blockDim.x) phi[e] = buf[(e >> ls) * P + (e & (S - 1))];
+    stamp(gp, 5);
 }
 
 // Forward: grid (L, B).  buf <- y; W y in place; epilogue per mode (as fwd_phase).
@@ -287,14 +310,16 @@ __global__ void __launch_bounds__(Wl<T>::threads, Wl<T>::minb) k_fwd_layer(const
     const int S = gp.side[l], C = gp.ccl, D = gp.ctail, P = S + 1, ls = ilog2(S);
     T* buf = reinterpret_cast<T*>(smem_raw);
     const size_t lbase = static_cast<size_t>(b) * gp.n + gp.coff[l];
+    stamp(gp, 0);
     if (tid < 16 && tid <= gp.lorder[l]) s_ad[tid] = gp.td[gp.ti[gp.o_reg + l] + tid];
     __shared__ int s_off[kMaxLev + 1];
     const LayerMap lm = layer_map(S, C, D, s_off);  // (published by the barrier after the y load)
     pdl_wait();  // y of the predecessor (the gather) is complete
     pdl_launch_dependents();
     const T* __restrict__ y = bf.y + lbase;
-    if (S * S % (4 * Wl<T>::threads) == 0 && S >= 4) {  // 4 vector loads in flight per thread per pass
-        constexpr int U = 4;
+    stamp(gp, 1);
+    constexpr int U = 4;
+    if (S * S % (4 * U * Wl<T>::threads) == 0) {  // 4 vector loads in flight per thread per pass
         for (int e0 = 4 * tid; e0 < S * S; e0 += 4 * U * blockDim.x) {
             Vec4<T> v[U];
 #pragma unroll
@@ -311,10 +336,24 @@ __global__ void __launch_bounds__(Wl<T>::threads, Wl<T>::minb) k_fwd_layer(const
         for (int e = tid; e < S * S; e += blockDim.x) buf[(e >> ls) * P + (e & (S - 1))] = y[e];
     }
     __syncthreads();
-    for (int s = S; s >= 2; s >>= 1) {  // rows, then columns (wavelet.hpp:153-168)
+    stamp(gp, 2);
+    const int slo = S >= kWlCorner ? 2 * kWlCorner : 2;
+    for (int s = S; s >= slo; s >>= 1) {  // rows, then columns (wavelet.hpp:153-168)
         analysis_lines<T, FLEN, false>(buf, P, s, s, gp);
         analysis_lines<T, FLEN, true>(buf, P, s, s, gp);
+        if (s == S) stamp(gp, 3);
     }
+    if (S >= kWlCorner) {  // levels kWlCorner..2: fused 2-D passes, finals back into the corner
+        constexpr int K = kWlCorner;
+        T* fk = buf + S * P;  // K x K finals (pitch K), then two (K+1)-pitch buffers
+        T* b0 = fk + K * K;
+        T* b1 = b0 + K * (K + 1);
+        tail_forward<T, FLEN>(gp, buf, P, K, b0, b1, fk);
+        __syncthreads();
+        for (int e = tid; e < K * K; e += blockDim.x) buf[(e / K) * P + (e % K)] = fk[e];
+        __syncthreads();
+    }
+    stamp(gp, 4);
     const bool zero_piston = fit_term && gp.piston_exact;
     double macc = 0.0;
     T* __restrict__ out = bf.out + lbase;
@@ -382,6 +421,7 @@ __global__ void __launch_bounds__(Wl<T>::threads, Wl<T>::minb) k_fwd_layer(const
         double* mp = bf.mu_part + (static_cast<size_t>(b) * gp.iters + it) * (gp.L * C) + l * C;
         if (tid < C) mp[tid] = tid == 0 ? t : 0.0;
     }
+    stamp(gp, 5);
 }
 
 }  // namespace fewha_gpu
