@@ -760,7 +760,18 @@ inline bool pdl_enabled() {
 
 template <typename T>
 struct Launch {
-    static size_t wfs_smem(const GeoParams& gp) { return wfs_tile_smem<T>(std::max(gp.L, gp.M)); }
+    static size_t wfs_smem(const GeoParams& gp, int ni = 1) { return wfs_tile_smem<T>(std::max(gp.L, gp.M), ni); }
+    // instances per WFS-tile CTA for a batch of `count` (FEWHA_WFS_NI overrides)
+    static int wfs_ni(int count) {
+        static const int env = [] {
+            const char* v = std::getenv("FEWHA_WFS_NI");
+            return v ? std::atoi(v) : 0;
+        }();
+        if (count <= 2) return 1;
+        // batches: 2 instances per CTA in fp64 (B = 64: -8 % per step; 4 is equal), 4 in fp32
+        // (-17 %)
+        return env == 1 || env == 2 || env == 4 ? env : (sizeof(T) == 4 ? 4 : 2);
+    }
     static size_t gather_smem(const GeoParams& gp) {
         return ((static_cast<size_t>(gp.gbuf_bytes) + 15) & ~size_t(15)) + static_cast<size_t>(gp.chunk_bytes);
     }
@@ -823,6 +834,10 @@ struct Launch {
         opt_in(k_wfs<T, true, FEWHA_WFS_MINB_LAT>, wfs_smem(gp));
         opt_in(k_wfs<T, false, FEWHA_WFS_MINB_BATCH>, wfs_smem(gp));
         opt_in(k_wfs<T, true, FEWHA_WFS_MINB_BATCH>, wfs_smem(gp));
+        opt_in(k_wfs<T, false, 3, 2>, wfs_smem(gp, 2));
+        opt_in(k_wfs<T, true, 3, 2>, wfs_smem(gp, 2));
+        opt_in(k_wfs<T, false, 2, 4>, wfs_smem(gp, 4));
+        opt_in(k_wfs<T, true, 2, 4>, wfs_smem(gp, 4));
         opt_in(k_gather<T, 2>, gather_smem(gp));
         opt_in(k_gather<T, 3>, gather_smem(gp));
         opt_in(k_gather<T, 4>, gather_smem(gp));
@@ -884,18 +899,26 @@ struct Launch {
     }
     static void wfs(bool rhs, const GeoParams& gp, const Bufs<T>& bf, int with_dm, int count, cudaStream_t st) {
         cudaLaunchAttribute attr[1];
-        cudaLaunchConfig_t cfg = pdl_cfg(dim3(gp.wt_count, count), wfs_smem(gp), st, attr, kWfsThreads);
+        const int ni = wfs_ni(count);
+        cudaLaunchConfig_t cfg =
+            pdl_cfg(dim3(gp.wt_count, (count + ni - 1) / ni), wfs_smem(gp, ni), st, attr, kWfsThreads);
         constexpr int LAT = FEWHA_WFS_MINB_LAT, BAT = FEWHA_WFS_MINB_BATCH;
         static const bool bat_lat = [] {  // profiling: batches on the latency instantiation
             const char* v = std::getenv("FEWHA_WFS_BATCH_MINB");
             return v && std::atoi(v) == LAT;
         }();
-        if (count <= 2 || bat_lat) {
-            if (rhs) CK(cudaLaunchKernelEx(&cfg, k_wfs<T, true, LAT>, gp, bf, with_dm));
-            else CK(cudaLaunchKernelEx(&cfg, k_wfs<T, false, LAT>, gp, bf, with_dm));
+        if (ni == 2) {
+            if (rhs) CK(cudaLaunchKernelEx(&cfg, k_wfs<T, true, 3, 2>, gp, bf, with_dm, count));
+            else CK(cudaLaunchKernelEx(&cfg, k_wfs<T, false, 3, 2>, gp, bf, with_dm, count));
+        } else if (ni == 4) {
+            if (rhs) CK(cudaLaunchKernelEx(&cfg, k_wfs<T, true, 2, 4>, gp, bf, with_dm, count));
+            else CK(cudaLaunchKernelEx(&cfg, k_wfs<T, false, 2, 4>, gp, bf, with_dm, count));
+        } else if (count <= 2 || bat_lat) {
+            if (rhs) CK(cudaLaunchKernelEx(&cfg, k_wfs<T, true, LAT>, gp, bf, with_dm, count));
+            else CK(cudaLaunchKernelEx(&cfg, k_wfs<T, false, LAT>, gp, bf, with_dm, count));
         } else {
-            if (rhs) CK(cudaLaunchKernelEx(&cfg, k_wfs<T, true, BAT>, gp, bf, with_dm));
-            else CK(cudaLaunchKernelEx(&cfg, k_wfs<T, false, BAT>, gp, bf, with_dm));
+            if (rhs) CK(cudaLaunchKernelEx(&cfg, k_wfs<T, true, BAT>, gp, bf, with_dm, count));
+            else CK(cudaLaunchKernelEx(&cfg, k_wfs<T, false, BAT>, gp, bf, with_dm, count));
         }
     }
     // y = sum_w P^T psi_w: one CTA per gp.grows rows of every layer

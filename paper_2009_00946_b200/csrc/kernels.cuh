@@ -296,14 +296,17 @@ __host__ __device__ constexpr size_t wfs_tile_table_bytes(int screens) {
            ((static_cast<size_t>(screens) * 2 * H * sizeof(T) + 15) & ~size_t(15));
 }
 template <typename T>
-__host__ __device__ constexpr size_t wfs_tile_smem(int screens) {
+__host__ __device__ constexpr size_t wfs_tile_smem(int screens, int ni = 1) {
     constexpr int H = kWfsTile + 2, Q = kWfsTile + 1;
-    return wfs_tile_table_bytes<T>(screens) + static_cast<size_t>(H * H + 2 * Q * Q) * sizeof(T);
+    return wfs_tile_table_bytes<T>(screens) + static_cast<size_t>(ni) * (H * H + 2 * Q * Q) * sizeof(T);
 }
 
-template <typename T, bool RHS, int G = 9>
-__device__ __forceinline__ void wfs_tile(const GeoParams& gp, const Bufs<T>& bf, int with_dm, int tile, int b,
-                                         unsigned char* smem_raw) {
+// One WFS tile for NI consecutive instances b0 .. b0+NI-1 (batches: the tile's stencil
+// tables, index math and bilinear weights are shared by the instances, and each thread
+// keeps NI instances' loads in flight).
+template <typename T, bool RHS, int G = 9, int NI = 1>
+__device__ __forceinline__ void wfs_tile(const GeoParams& gp, const Bufs<T>& bf, int with_dm, int tile, int b0,
+                                         int ninst, unsigned char* smem_raw) {
     constexpr int TS = kWfsTile, H = TS + 2, Q = TS + 1;
     int w, i0, j0;
     if (gp.n_wtiles <= kMaxWtCode) {
@@ -326,9 +329,9 @@ __device__ __forceinline__ void wfs_tile(const GeoParams& gp, const Bufs<T>& bf,
     const int ib = (NS * 2 * H * static_cast<int>(sizeof(int)) + 15) & ~15;
     int* tix = reinterpret_cast<int*>(smem_raw);
     T* tw = reinterpret_cast<T*>(smem_raw + ib);
-    T* ph = tw + NS * 2 * H;
-    T* sx = ph + H * H;
-    T* sy = sx + Q * Q;
+    T* ph = tw + NS * 2 * H;  // [NI][H*H]
+    T* sx = ph + NI * H * H;  // [NI][Q*Q]
+    T* sy = sx + NI * Q * Q;
     __shared__ unsigned long long s_mbar;
     wstamp(gp, 0);
     if (screens_on) {
@@ -354,16 +357,19 @@ __device__ __forceinline__ void wfs_tile(const GeoParams& gp, const Bufs<T>& bf,
     __syncthreads();
     wstamp(gp, 1);
     // 1. wavefront on the tile + 1-node halo (propagate_point, operators.hpp:204-213)
-    const T* src = RHS ? bf.a_prev2 + static_cast<size_t>(b) * gp.A : bf.phi + static_cast<size_t>(b) * gp.n;
+    const size_t inst_stride = RHS ? static_cast<size_t>(gp.A) : static_cast<size_t>(gp.n);
+    const T* src = (RHS ? bf.a_prev2 : bf.phi) + static_cast<size_t>(b0) * inst_stride;
     for (int idx = tid; idx < H * H; idx += nthr) {
         const int a = idx / H, c = idx - a * H;
         const int i = i0 - 1 + a, j = j0 - 1 + c;
-        T v = T(0);
+        T v[NI];
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni) v[ni] = T(0);
         if (screens_on && i >= 0 && i < np && j >= 0 && j < np) {
-            // screens in unrolled groups of G: a group's 4G loads are in flight together
+            // screens in unrolled groups of G: a group's 4 G NI loads are in flight together
             // (padding screens of the last group read a valid node with weight 0)
             for (int s0 = 0; s0 < NS; s0 += G) {
-                T q00[G], q01[G], q10[G], q11[G], fy[G], fx[G];
+                T q00[G][NI], q01[G][NI], q10[G][NI], q11[G][NI], fy[G], fx[G];
 #pragma unroll
                 for (int u = 0; u < G; ++u) {
                     const int sc = min(s0 + u, NS - 1);
@@ -371,10 +377,14 @@ __device__ __forceinline__ void wfs_tile(const GeoParams& gp, const Bufs<T>& bf,
                     const T* wx = tw + sc * 2 * H;
                     const int stride = RHS ? gp.nact[sc] : gp.side[sc];
                     const T* r0 = src + (RHS ? gp.aoff[sc] : gp.coff[sc]) + tx[H + a] * stride + tx[c];
-                    q00[u] = r0[0];
-                    q01[u] = r0[1];
-                    q10[u] = r0[stride];
-                    q11[u] = r0[stride + 1];
+#pragma unroll
+                    for (int ni = 0; ni < NI; ++ni) {
+                        const T* rn = r0 + (ni < ninst ? ni : 0) * inst_stride;
+                        q00[u][ni] = rn[0];
+                        q01[u][ni] = rn[1];
+                        q10[u][ni] = rn[stride];
+                        q11[u][ni] = rn[stride + 1];
+                    }
                     fy[u] = s0 + u < NS ? wx[H + a] : T(0);
                     fx[u] = wx[c];
                 }
@@ -384,28 +394,33 @@ __device__ __forceinline__ void wfs_tile(const GeoParams& gp, const Bufs<T>& bf,
                     // bilinear(): w00 v00 + w01 v01 + w10 v10 + w11 v11 (operators.hpp:125-126)
                     const T w00 = (T(1) - fy[u]) * (T(1) - fx[u]), w01 = (T(1) - fy[u]) * fx[u];
                     const T w10 = fy[u] * (T(1) - fx[u]), w11 = fy[u] * fx[u];
-                    v += w00 * q00[u] + w01 * q01[u] + w10 * q10[u] + w11 * q11[u];
+#pragma unroll
+                    for (int ni = 0; ni < NI; ++ni)
+                        v[ni] += w00 * q00[u][ni] + w01 * q01[u][ni] + w10 * q10[u][ni] + w11 * q11[u][ni];
                 }
             }
         }
-        ph[idx] = v;
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni) ph[ni * H * H + idx] = v[ni];
     }
     __syncthreads();
     wstamp(gp, 2);
     // 2. weighted half-slopes on the (TS+1)^2 subapertures touching the tile
     const T iv = static_cast<T>(gp.inv_var[w]);
     const std::uint8_t* mask = gp.masks + gp.mkoff[w];
-    const double* meas = bf.meas + static_cast<size_t>(b) * gp.S + gp.moff[w];
-    for (int idx = tid; idx < Q * Q; idx += nthr) {
+    for (int e = tid; e < NI * Q * Q; e += nthr) {
+        const int ni = e / (Q * Q), idx = e - ni * Q * Q;
         const int a = idx / Q, c = idx - a * Q;
         const int i = i0 - 1 + a, j = j0 - 1 + c;
+        const T* phn = ph + ni * H * H;
         T x = T(0), y = T(0);
-        if (i >= 0 && i < ns && j >= 0 && j < ns && mask[i * ns + j]) {
-            const T p00 = ph[a * H + c], p01 = ph[a * H + c + 1];
-            const T p10 = ph[(a + 1) * H + c], p11 = ph[(a + 1) * H + c + 1];
+        if (ni < ninst && i >= 0 && i < ns && j >= 0 && j < ns && mask[i * ns + j]) {
+            const T p00 = phn[a * H + c], p01 = phn[a * H + c + 1];
+            const T p10 = phn[(a + 1) * H + c], p11 = phn[(a + 1) * H + c + 1];
             T gx = T(0.5) * ((p01 - p00) + (p11 - p10));  // sh_apply, operators.hpp:160-161
             T gy = T(0.5) * ((p10 - p00) + (p11 - p01));
             if (RHS) {
+                const double* meas = bf.meas + static_cast<size_t>(b0 + ni) * gp.S + gp.moff[w];
                 const int k = i * ns + j;
                 const T mx = static_cast<T>(meas[k]), my = static_cast<T>(meas[ns * ns + k]);
                 gx = with_dm ? mx + gx : mx;
@@ -414,36 +429,41 @@ __device__ __forceinline__ void wfs_tile(const GeoParams& gp, const Bufs<T>& bf,
             x = T(0.5) * (gx * iv);
             y = T(0.5) * (gy * iv);
         }
-        sx[idx] = x;
-        sy[idx] = y;
+        sx[e] = x;
+        sy[e] = y;
     }
     __syncthreads();
     wstamp(gp, 3);
     // 3. adjoint slopes: gather of the 4 neighbouring subapertures in the
     //    reference's scatter order (operators.hpp:176-187)
-    T* psi = bf.psi + static_cast<size_t>(b) * gp.Nw + gp.woff[w];
-    for (int idx = tid; idx < TS * TS; idx += nthr) {
+    for (int e = tid; e < NI * TS * TS; e += nthr) {
+        const int ni = e / (TS * TS), idx = e - ni * TS * TS;
         const int a = idx / TS, c = idx - a * TS;
         const int i = i0 + a, j = j0 + c;
-        if (i >= np || j >= np) continue;
-        T v = sx[a * Q + c] + sy[a * Q + c];
-        v += -sx[a * Q + c + 1] + sy[a * Q + c + 1];
-        v += sx[(a + 1) * Q + c] - sy[(a + 1) * Q + c];
-        v += -sx[(a + 1) * Q + c + 1] - sy[(a + 1) * Q + c + 1];
+        if (ni >= ninst || i >= np || j >= np) continue;
+        const T* sxn = sx + ni * Q * Q;
+        const T* syn = sy + ni * Q * Q;
+        T v = sxn[a * Q + c] + syn[a * Q + c];
+        v += -sxn[a * Q + c + 1] + syn[a * Q + c + 1];
+        v += sxn[(a + 1) * Q + c] - syn[(a + 1) * Q + c];
+        v += -sxn[(a + 1) * Q + c + 1] - syn[(a + 1) * Q + c + 1];
         if (gp.fault != 1.0) v *= static_cast<T>(gp.fault);
+        T* psi = bf.psi + static_cast<size_t>(b0 + ni) * gp.Nw + gp.woff[w];
         psi[i * np + j] = v;
     }
     wstamp(gp, 4);
 }
 
-template <typename T, bool RHS, int MINB>
-__global__ void __launch_bounds__(kWfsThreads, MINB) k_wfs(const GeoParams gp, const Bufs<T> bf, int with_dm) {
+// NI instances per CTA (grid.y = ceil(B / NI)).
+template <typename T, bool RHS, int MINB, int NI = 1>
+__global__ void __launch_bounds__(kWfsThreads, MINB) k_wfs(const GeoParams gp, const Bufs<T> bf, int with_dm, int count) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     // screens per unrolled load group: 7 for the latency plan (3 CTAs/SM, 72 registers; 9
     // spilled 16 bytes), 5 for batches (4 CTAs/SM, 56 registers; 9 spilled 44 bytes and
-    // was 5 % slower per launch at B = 64)
-    constexpr int G = (MINB >= 4 && sizeof(T) == 8) ? 5 : 7;
-    wfs_tile<T, RHS, G>(gp, bf, with_dm, gp.wt_base + blockIdx.x, blockIdx.y, smem_raw);
+    // was 5 % slower per launch at B = 64); 3 with two instances per CTA
+    constexpr int G = NI > 2 ? 2 : NI > 1 ? 3 : (MINB >= 4 && sizeof(T) == 8) ? 5 : 7;
+    const int b0 = blockIdx.y * NI;
+    wfs_tile<T, RHS, G, NI>(gp, bf, with_dm, gp.wt_base + blockIdx.x, b0, min(NI, count - b0), smem_raw);
 }
 
 // ---------------------------------------------------------------------------
