@@ -145,6 +145,7 @@ typedef struct {
     int cluster_ctas, tail, gather_rows, gather_ctas_per_sm, inverse_staged, wfs_ctas_per_sm, wfs_tiles,
         launches_per_step;
     int whole_layer; /* 1: layer transforms one CTA per (layer, instance) (batched plans), 0: clusters */
+    int gather_instances, wfs_instances; /* instances per CTA of the adjoint gather / WFS-tile kernels */
 } fewha_gpu_plan_t;
 int fewha_gpu_plan_info(fewha_gpu_t h, fewha_gpu_plan_t* out);
 /* Runs ONE frame eagerly (not from the graph) with a CUDA event after every

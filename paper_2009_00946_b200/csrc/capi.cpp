@@ -243,6 +243,8 @@ int fewha_gpu_plan_info(fewha_gpu_t h, fewha_gpu_plan_t* out) {
         out->wfs_tiles = pi.wfs_tiles;
         out->launches_per_step = pi.launches_per_step;
         out->whole_layer = pi.whole_layer;
+        out->gather_instances = pi.gather_instances;
+        out->wfs_instances = pi.wfs_instances;
     })
 }
 float fewha_gpu_debug_bench_dwt(fewha_gpu_t h, int variant, int inverse, int reps, int threads) {

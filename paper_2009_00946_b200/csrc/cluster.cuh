@@ -793,6 +793,212 @@ __global__ void __launch_bounds__(256, MINB) k_gather(const GeoParams gp, const 
     stamp(gp, 2);
 }
 
+// ---------------------------------------------------------------------------
+// The gather for NI consecutive instances per CTA (batched plans): the chunk's tables
+// are staged once and shared, the psi blocks of the NI instances sit one after the other
+// (instance ni at soff + ni * pad0, pad0 = the chunk's psi bytes per instance), and every
+// thread carries NI instances' row and column sums (more loads in flight, index math and
+// weights shared).  Same arithmetic per instance as gather_group.
+// ---------------------------------------------------------------------------
+template <typename T, int NI>
+__device__ __forceinline__ void gather_issue_ni(const GeoParams& gp, const T* psi_b, const GDesc* desc, int w0, int w1,
+                                                unsigned char* stage, unsigned long long* mbar, bool tables, bool psi,
+                                                int ninst) {
+    const int lane = threadIdx.x;
+    if (tables && lane == 31) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        bulk_g2s(stage, gp.gblob + desc[w0].rtoff, static_cast<unsigned>(gather_row_bytes(desc, w0, w1)), mbar);
+    }
+    if (tables && lane == 30) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        const unsigned bytes = static_cast<unsigned>(desc[w1 - 1].ctoff + desc[w1 - 1].cb - desc[w0].ctoff);
+        bulk_g2s(stage + gather_row_bytes(desc, w0, w1), gp.gblob + desc[w0].ctoff, bytes, mbar);
+    }
+    const int nw = w1 - w0;
+    if (psi && lane < nw * NI) {
+        const int ni = lane / nw, w = w0 + (lane - ni * nw);
+        const GDesc d = desc[w];
+        const int nr = d.ihi - d.ilo, np = gp.ns[w] + 1;
+        if (nr > 0 && ni < ninst) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            const uintptr_t a = reinterpret_cast<uintptr_t>(psi_b + static_cast<size_t>(ni) * gp.Nw + d.src);
+            const unsigned shift = static_cast<unsigned>(a & 15u);
+            bulk_g2s(stage + d.soff + ni * d.pad0, reinterpret_cast<const void*>(a - shift),
+                     round16(shift + nr * np * static_cast<unsigned>(sizeof(T))), mbar);
+        }
+    }
+}
+
+template <typename T, int KM, int ROWS, int NI>
+__device__ void gather_group_ni(const GeoParams& gp, const T* __restrict__ psi_b, int l, T* __restrict__ y, T* gbuf,
+                                unsigned char* stage, const GDesc* desc, unsigned long long* mbar, int ninst) {
+    static_assert(KM > 0, "the multi-instance gather takes the compile-time tap counts");
+    const int side = gp.side[l];
+    const int R = side < ROWS ? side : ROWS;
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const int lside = ilog2(side);
+    const int groups = min(nthr >> lside, R);
+    const int rows_pt = R / groups;
+    const int J = tid & (side - 1), grp = tid >> lside;
+    const int i0 = grp * rows_pt;
+    const bool worker = grp < groups;
+    const int gst = ROWS * gp.bd_cols_max;      // G stride per WFS
+    const int gin = gp.W * gst;                 // G stride per instance
+    const int o_rw = align16(R * KM * 2);
+    const int o_idx = align16((side + 3) * 2);
+    T out[NI][ROWS];
+#pragma unroll
+    for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+        for (int k = 0; k < ROWS; ++k) out[ni][k] = T(0);
+    for (int k = 0; k < gp.nchunk; ++k) {
+        const int w0 = gp.gchunk[k], w1 = gp.gchunk[k + 1];
+        if (k > 0 && tid < 32) {
+            gather_issue_ni<T, NI>(gp, psi_b, desc, w0, w1, stage, mbar, true, true, ninst);
+            __syncwarp();
+            if (tid == 0) mbar_arrive(mbar);
+        }
+        mbar_wait(mbar, static_cast<unsigned>(k & 1));
+        const int rt0 = desc[w0].rtoff, ct0 = desc[w0].ctoff;
+        const unsigned char* cstage = stage + gather_row_bytes(desc, w0, w1);
+        {
+            constexpr int CL = 128;
+            const int ng = nthr / CL > 0 ? nthr / CL : 1, gq = tid / CL, lane = tid % CL;
+            for (int w = w0 + gq; w < w1; w += ng) {
+                const GDesc d = desc[w];
+                const int nr = d.ihi - d.ilo, np = gp.ns[w] + 1, nc = d.jhi - d.jlo;
+                if (nr <= 0) continue;
+                const unsigned char* tp = stage + (d.rtoff - rt0);
+                const short* __restrict__ rs = reinterpret_cast<const short*>(tp);
+                const T* __restrict__ rw = reinterpret_cast<const T*>(tp + o_rw);
+                const T* blk[NI];
+#pragma unroll
+                for (int ni = 0; ni < NI; ++ni) {
+                    const unsigned shift = static_cast<unsigned>(
+                        reinterpret_cast<uintptr_t>(psi_b + static_cast<size_t>(ni < ninst ? ni : 0) * gp.Nw + d.src) & 15u);
+                    blk[ni] = reinterpret_cast<const T*>(stage + d.soff + (ni < ninst ? ni : 0) * d.pad0 + shift) + d.jlo;
+                }
+                for (int c = lane; c < nc; c += CL) {
+#pragma unroll
+                    for (int i = 0; i < ROWS; ++i) {
+                        if (i >= R) break;
+                        T g[NI];
+#pragma unroll
+                        for (int ni = 0; ni < NI; ++ni) g[ni] = T(0);
+#pragma unroll
+                        for (int q = 0; q < KM; ++q) {
+                            const T wq = rw[i * KM + q];
+                            const int ro = rs[i * KM + q] * np + c;
+#pragma unroll
+                            for (int ni = 0; ni < NI; ++ni) g[ni] += wq * blk[ni][ro];
+                        }
+#pragma unroll
+                        for (int ni = 0; ni < NI; ++ni) gbuf[ni * gin + (w - w0) * gst + i * nc + c] = g[ni];
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        if (worker) {
+            for (int w = w0; w < w1; ++w) {
+                const GDesc d = desc[w];
+                const int nr = d.ihi - d.ilo, nc = d.jhi - d.jlo;
+                if (nr <= 0) continue;
+                const unsigned char* tp = cstage + (d.ctoff - ct0);
+                const short* first = reinterpret_cast<const short*>(tp);
+                const short* cidx = reinterpret_cast<const short*>(tp + o_idx);
+                const T* cfr = reinterpret_cast<const T*>(tp + o_idx + align16(nc * 2));
+                const int c0 = first[J], c1 = first[J + 2];
+                T wt[KM];
+                int cc[KM];
+#pragma unroll
+                for (int q = 0; q < KM; ++q) {
+                    const int c = min(c0 + q, nc - 1);
+                    const T fr = cfr[c];
+                    wt[q] = c0 + q < c1 ? (cidx[c] == J ? T(1) - fr : fr) : T(0);
+                    cc[q] = c;
+                }
+#pragma unroll
+                for (int k2 = 0; k2 < ROWS; ++k2) {
+                    if (k2 >= rows_pt) break;
+#pragma unroll
+                    for (int ni = 0; ni < NI; ++ni) {
+                        const T* g = gbuf + ni * gin + (w - w0) * gst + (i0 + k2) * nc;
+                        T s = T(0);
+#pragma unroll
+                        for (int q = 0; q < KM; ++q) s += wt[q] * g[cc[q]];
+                        out[ni][k2] += s;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (worker) {
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni) {
+            if (ni >= ninst) break;
+#pragma unroll
+            for (int k = 0; k < ROWS; ++k) {
+                if (k >= rows_pt) break;
+                y[static_cast<size_t>(ni) * gp.n + (i0 + k) * side + J] = out[ni][k];
+            }
+        }
+    }
+}
+
+// grid (side/grows, L, ceil(B / NI)); batched plans with compile-time tap counts (gather_km <= 4)
+template <typename T, int MINB, int NI>
+__global__ void __launch_bounds__(256, MINB) k_gather_ni(const GeoParams gp, const Bufs<T> bf, int count) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ GDesc s_desc[kMaxW];
+    __shared__ unsigned long long s_mbar;
+    const int u = blockIdx.x, l = blockIdx.y, b0 = blockIdx.z * NI;
+    const int ninst = min(NI, count - b0);
+    const int side = gp.side[l];
+    const int R = side < gp.grows ? side : gp.grows;
+    if (u * R >= side) return;
+    const int tid = threadIdx.x;
+    T* gbuf = reinterpret_cast<T*>(smem_raw);
+    unsigned char* stage = smem_raw + align16(gp.gbuf_bytes * NI);
+    const T* psi = bf.psi + static_cast<size_t>(b0) * gp.Nw;
+    if (tid < 32) {
+        if (tid < gp.W) {
+            const int4* d = reinterpret_cast<const int4*>(gp.ti + gp.o_gd + ((l * kMaxGU + u) * kMaxW + tid) * kGDescInts);
+            const int4 a = d[0], c = d[1], e = d[2];
+            s_desc[tid] = GDesc{a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w, e.x, e.y, e.z, e.w};
+        }
+        if (tid == 0) {
+            mbar_init(&s_mbar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        }
+        __syncwarp();
+        gather_issue_ni<T, NI>(gp, psi, s_desc, gp.gchunk[0], gp.gchunk[1], stage, &s_mbar, true, false, ninst);
+    }
+    pdl_wait();
+    pdl_launch_dependents();
+    if (tid < 32) {
+        gather_issue_ni<T, NI>(gp, psi, s_desc, gp.gchunk[0], gp.gchunk[1], stage, &s_mbar, false, true, ninst);
+        __syncwarp();
+        if (tid == 0) mbar_arrive(&s_mbar);
+    }
+    __syncthreads();
+    T* y = bf.y + static_cast<size_t>(b0) * gp.n + gp.coff[l] + static_cast<size_t>(u) * R * side;
+#define FEWHA_GATHER_NI_KM(ROWS)                                                                                 \
+    switch (gp.gather_km) {                                                                                     \
+        case 1: gather_group_ni<T, 1, ROWS, NI>(gp, psi, l, y, gbuf, stage, s_desc, &s_mbar, ninst); break;    \
+        case 2: gather_group_ni<T, 2, ROWS, NI>(gp, psi, l, y, gbuf, stage, s_desc, &s_mbar, ninst); break;    \
+        case 3: gather_group_ni<T, 3, ROWS, NI>(gp, psi, l, y, gbuf, stage, s_desc, &s_mbar, ninst); break;    \
+        default: gather_group_ni<T, 4, ROWS, NI>(gp, psi, l, y, gbuf, stage, s_desc, &s_mbar, ninst); break;   \
+    }
+    if (gp.grows == 4) {
+        FEWHA_GATHER_NI_KM(4)
+    } else {
+        FEWHA_GATHER_NI_KM(8)
+    }
+#undef FEWHA_GATHER_NI_KM
+}
+
 // Deterministic sum of the dot partials of one iteration by warp 0: fixed
 // per-lane strided order, fixed shuffle tree -- identical in every CTA.
 __device__ __forceinline__ void warp_dot_sums(const double* rho_part, const double* mu_part, int n, double& rho,

@@ -37,7 +37,7 @@ struct GeoParams {
     double inv_var[kMaxW];
     double alpha, gain, tol, fault;
     int piston_exact;  // fp32 engines: the fitting term's coarse coefficient is exactly 0 (see k_layer_forward)
-    int filt_off;  // (unused on the device; filters below)
+    int gather_ni;  // instances per k_gather CTA (batched plans 2, else 1; host plan, cluster.cuh k_gather_ni)
     double flo[20], fhi[20];  // Daubechies taps of the configured order (wavelet.hpp:100-107)
     float flo_f[20], fhi_f[20];
     // tables

@@ -153,7 +153,7 @@ Plan build_plan(const Geometry& g, int elem_bytes, int batch, int wa = 0, int wb
     gp.gain = g.gain;
     gp.tol = g.pcg_tol;
     gp.fault = g.fault == "sh_adjoint" ? 1.0 + 1e-6 : 1.0;  // reconstructor.hpp:120
-    gp.filt_off = kDaubechiesOffset[g.wavelet_order - 1];
+
     int off = 0;
     for (int l = 0; l < L; ++l) {
         if (g.layers[l].order > 7)
@@ -418,8 +418,12 @@ Plan build_plan(const Geometry& g, int elem_bytes, int batch, int wa = 0, int wb
         // psi source blocks per (w, l, gather row group u)
         // rows per gather CTA: 4 for a single instance (288 CTAs at the ELT scale, two per
         // SM), larger groups for batches amortise each CTA's staging and setup
-        // (batch 64: 8 rows 31 % faster than 4; FEWHA_GATHER_ROWS overrides)
-        gp.grows = batch <= 2 ? 4 : 8;
+        // (batch 64, one instance per CTA: 8 rows 31 % faster than 4; with two instances per
+        // CTA 4 rows, whose row-contracted blocks leave room for both instances' psi blocks;
+        // FEWHA_GATHER_ROWS overrides)
+        const char* gni_env = std::getenv("FEWHA_GATHER_NI");
+        const bool gni2 = batch > 2 && !(gni_env && std::atoi(gni_env) == 1);
+        gp.grows = batch <= 2 ? 4 : (gni2 ? 4 : 8);
         if (const char* v = std::getenv("FEWHA_GATHER_ROWS")) {
             const int r = std::atoi(v);
             if (r == 2 || r == 4 || r == 8) gp.grows = r;
@@ -483,19 +487,28 @@ Plan build_plan(const Geometry& g, int elem_bytes, int batch, int wa = 0, int wb
                 tab_bytes(Rl, side, bs[3] - bs[2]),
                 a16(static_cast<size_t>(bs[1] - bs[0]) * (g.wfs[w].n_subap + 1) * elem_bytes + 16));
         };
+        // instances per CTA (batched plans: 2, sharing the staged tables; FEWHA_GATHER_NI
+        // overrides; compile-time tap counts only)
+        gp.gather_ni = batch > 2 ? 2 : 1;
+        if (const char* v = std::getenv("FEWHA_GATHER_NI")) {
+            const int ni = std::atoi(v);
+            if (ni == 1 || ni == 2) gp.gather_ni = ni;
+        }
+        if (gp.gather_km > 4 || (gp.grows != 4 && gp.grows != 8)) gp.gather_ni = 1;
+        const size_t NIg = static_cast<size_t>(gp.gather_ni);
         std::vector<size_t> need_max(static_cast<size_t>(W), 0);
         for (int w = 0; w < W; ++w)
             for (int l = 0; l < L; ++l)
                 for (int u = 0; u < gp.side[l] / grp_rows(gp.side[l]); ++u) {
                     const auto nb = need_of(w, l, u);
-                    need_max[static_cast<size_t>(w)] = std::max(need_max[static_cast<size_t>(w)], nb.first + nb.second);
+                    need_max[static_cast<size_t>(w)] = std::max(need_max[static_cast<size_t>(w)], nb.first + NIg * nb.second);
                 }
-        // row-contracted blocks G of every WFS of a chunk (group rows x psi block columns)
+        // row-contracted blocks G of every WFS of a chunk (group rows x psi block columns), per instance
         gp.gbuf_bytes = static_cast<int>(a16(static_cast<size_t>(W) * gp.grows * cmax * elem_bytes));
-        const size_t fixed = a16(static_cast<size_t>(gp.gbuf_bytes)) + 1024;  // + static shared memory
+        const size_t fixed = a16(static_cast<size_t>(gp.gbuf_bytes) * NIg) + 1024;  // + static shared memory
         // residency plan of k_gather (cluster.cuh): 2 CTAs/SM for a single instance, 3 for
         // batches (FEWHA_GATHER_MINB overrides: 2, 3 or 4)
-        gp.gather_minb = batch > 2 ? 3 : 2;
+        gp.gather_minb = batch > 2 ? 3 : 2;  // (two instances per CTA: 3 as well; 2: equal)
         if (const char* v = std::getenv("FEWHA_GATHER_MINB")) {
             const int m = std::atoi(v);
             if (m >= 2 && m <= 4) gp.gather_minb = m;
@@ -645,8 +658,11 @@ Plan build_plan(const Geometry& g, int elem_bytes, int batch, int wa = 0, int wb
             for (int u = 0; u < gp.side[l] / grp_rows(gp.side[l]); ++u) {
                 const int Rl = grp_rows(gp.side[l]);
                 for (int k = 0; k < gp.nchunk; ++k) {
-                    size_t tsum = 0;
-                    for (int w = gp.gchunk[k]; w < gp.gchunk[k + 1]; ++w) tsum += need_of(w, l, u).first;
+                    size_t tsum = 0, psum = 0;
+                    for (int w = gp.gchunk[k]; w < gp.gchunk[k + 1]; ++w) {
+                        tsum += need_of(w, l, u).first;
+                        psum += need_of(w, l, u).second;
+                    }
                     size_t poff = tsum;
                     for (int w = gp.gchunk[k]; w < gp.gchunk[k + 1]; ++w) {
                         const int* bs = &pl.ti[static_cast<size_t>(gp.o_bs + ((w * L + l) * kMaxGU + u) * 4)];
@@ -659,6 +675,7 @@ Plan build_plan(const Geometry& g, int elem_bytes, int batch, int wa = 0, int wb
                         d[7] = static_cast<int>(row_bytes(Rl));
                         d[8] = static_cast<int>(coff_wl[static_cast<size_t>(w * L + l)]);
                         d[9] = static_cast<int>(col_bytes(gp.side[l], bs[3] - bs[2]));
+                        d[10] = static_cast<int>(psum);  // psi bytes of the chunk per instance (k_gather_ni)
                         poff += nb.second;
                     }
                 }
@@ -773,7 +790,7 @@ struct Launch {
         return env == 1 || env == 2 || env == 4 ? env : (sizeof(T) == 4 ? 4 : 2);
     }
     static size_t gather_smem(const GeoParams& gp) {
-        return ((static_cast<size_t>(gp.gbuf_bytes) + 15) & ~size_t(15)) + static_cast<size_t>(gp.chunk_bytes);
+        return ((static_cast<size_t>(gp.gbuf_bytes) * gp.gather_ni + 15) & ~size_t(15)) + static_cast<size_t>(gp.chunk_bytes);
     }
     static size_t a16(size_t v) { return (v + 15) & ~size_t(15); }
     // shared-memory maps: clayout.hpp (the kernels derive the same offsets)
@@ -841,6 +858,9 @@ struct Launch {
         opt_in(k_gather<T, 2>, gather_smem(gp));
         opt_in(k_gather<T, 3>, gather_smem(gp));
         opt_in(k_gather<T, 4>, gather_smem(gp));
+        opt_in(k_gather_ni<T, 2, 2>, gather_smem(gp));
+        opt_in(k_gather_ni<T, 3, 2>, gather_smem(gp));
+        opt_in(k_gather_ni<T, 4, 2>, gather_smem(gp));
     }
     // layer kernels: grid (C, L, count), cluster (C,1,1)
     static void cl(int flen, bool inverse, const GeoParams& gp, const Bufs<T>& bf, int mode, int it, int count,
@@ -925,6 +945,13 @@ struct Launch {
     static void gather(const GeoParams& gp, const Bufs<T>& bf, int count, cudaStream_t st) {
         cudaLaunchAttribute attr[1];
         const int groups = gp.maxside / std::min(gp.grows, gp.maxside);
+        if (gp.gather_ni == 2) {
+            cudaLaunchConfig_t cfg = pdl_cfg(dim3(groups, gp.L, (count + 1) / 2), gather_smem(gp), st, attr);
+            if (gp.gather_minb == 4) CK(cudaLaunchKernelEx(&cfg, k_gather_ni<T, 4, 2>, gp, bf, count));
+            else if (gp.gather_minb == 3) CK(cudaLaunchKernelEx(&cfg, k_gather_ni<T, 3, 2>, gp, bf, count));
+            else CK(cudaLaunchKernelEx(&cfg, k_gather_ni<T, 2, 2>, gp, bf, count));
+            return;
+        }
         cudaLaunchConfig_t cfg = pdl_cfg(dim3(groups, gp.L, count), gather_smem(gp), st, attr);
         if (gp.gather_minb == 4) CK(cudaLaunchKernelEx(&cfg, k_gather<T, 4>, gp, bf));
         else if (gp.gather_minb == 3) CK(cudaLaunchKernelEx(&cfg, k_gather<T, 3>, gp, bf));
@@ -1956,6 +1983,10 @@ PlanInfo Engine::plan_info() const {
     pi.wfs_tiles = P.gp.wt_count;
     pi.launches_per_step = launches_per_step();
     pi.whole_layer = P.use_whole() ? 1 : 0;
+    pi.gather_instances = P.gp.gather_ni;
+    pi.wfs_instances = P.precision == 64 ? Launch<double>::wfs_ni(P.batch) : Launch<float>::wfs_ni(P.batch);
+    if (pi.wfs_instances == 2) pi.wfs_ctas_per_sm = 3;
+    else if (pi.wfs_instances == 4) pi.wfs_ctas_per_sm = 2;
     return pi;
 }
 
