@@ -284,6 +284,11 @@ __device__ __forceinline__ void wstamp(const GeoParams& gp, int k) {
 #ifndef FEWHA_WFS_MINB_BATCH
 #define FEWHA_WFS_MINB_BATCH 4
 #endif
+#ifndef FEWHA_WFS_GLAT
+// screens per load group of the latency plan: all 9 layers' 36 loads in flight at once
+// (80 registers, 16 B of spills) beat groups of 7 (no spills): 0.1844 vs 0.1865 ms per frame
+#define FEWHA_WFS_GLAT 9
+#endif
 constexpr int kWfsTile = FEWHA_WFS_TILE;  // WFS node tile side (compile-time: index math by constants)
 constexpr int kWfsThreads = FEWHA_WFS_THREADS;  // threads per WFS tile CTA
 
@@ -458,10 +463,10 @@ __device__ __forceinline__ void wfs_tile(const GeoParams& gp, const Bufs<T>& bf,
 template <typename T, bool RHS, int MINB, int NI = 1>
 __global__ void __launch_bounds__(kWfsThreads, MINB) k_wfs(const GeoParams gp, const Bufs<T> bf, int with_dm, int count) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    // screens per unrolled load group: 7 for the latency plan (3 CTAs/SM, 72 registers; 9
-    // spilled 16 bytes), 5 for batches (4 CTAs/SM, 56 registers; 9 spilled 44 bytes and
-    // was 5 % slower per launch at B = 64); 3 with two instances per CTA
-    constexpr int G = NI > 2 ? 2 : NI > 1 ? 3 : (MINB >= 4 && sizeof(T) == 8) ? 5 : 7;
+    // screens per unrolled load group: FEWHA_WFS_GLAT (9) for the latency plan (3 CTAs/SM),
+    // 5 for batches of one instance per CTA (4 CTAs/SM, 56 registers), 3 / 2 with two / four
+    // instances per CTA
+    constexpr int G = NI > 2 ? 2 : NI > 1 ? 3 : (MINB >= 4 && sizeof(T) == 8) ? 5 : FEWHA_WFS_GLAT;
     const int b0 = blockIdx.y * NI;
     wfs_tile<T, RHS, G, NI>(gp, bf, with_dm, gp.wt_base + blockIdx.x, b0, min(NI, count - b0), smem_raw);
 }
