@@ -842,8 +842,7 @@ __device__ void gather_group_ni(const GeoParams& gp, const T* __restrict__ psi_b
     const int J = tid & (side - 1), grp = tid >> lside;
     const int i0 = grp * rows_pt;
     const bool worker = grp < groups;
-    const int gst = ROWS * gp.bd_cols_max;      // G stride per WFS
-    const int gin = gp.W * gst;                 // G stride per instance
+    const int gin = gp.gbuf_bytes / static_cast<int>(sizeof(T));  // G stride per instance (blocks at desc[w].pad1)
     const int o_rw = align16(R * KM * 2);
     const int o_idx = align16((side + 3) * 2);
     T out[NI][ROWS];
@@ -893,7 +892,7 @@ __device__ void gather_group_ni(const GeoParams& gp, const T* __restrict__ psi_b
                             for (int ni = 0; ni < NI; ++ni) g[ni] += wq * blk[ni][ro];
                         }
 #pragma unroll
-                        for (int ni = 0; ni < NI; ++ni) gbuf[ni * gin + (w - w0) * gst + i * nc + c] = g[ni];
+                        for (int ni = 0; ni < NI; ++ni) gbuf[ni * gin + d.pad1 + i * nc + c] = g[ni];
                     }
                 }
             }
@@ -923,7 +922,7 @@ __device__ void gather_group_ni(const GeoParams& gp, const T* __restrict__ psi_b
                     if (k2 >= rows_pt) break;
 #pragma unroll
                     for (int ni = 0; ni < NI; ++ni) {
-                        const T* g = gbuf + ni * gin + (w - w0) * gst + (i0 + k2) * nc;
+                        const T* g = gbuf + ni * gin + d.pad1 + (i0 + k2) * nc;
                         T s = T(0);
 #pragma unroll
                         for (int q = 0; q < KM; ++q) s += wt[q] * g[cc[q]];

@@ -418,12 +418,10 @@ Plan build_plan(const Geometry& g, int elem_bytes, int batch, int wa = 0, int wb
         // psi source blocks per (w, l, gather row group u)
         // rows per gather CTA: 4 for a single instance (288 CTAs at the ELT scale, two per
         // SM), larger groups for batches amortise each CTA's staging and setup
-        // (batch 64, one instance per CTA: 8 rows 31 % faster than 4; with two instances per
-        // CTA 4 rows, whose row-contracted blocks leave room for both instances' psi blocks;
-        // FEWHA_GATHER_ROWS overrides)
-        const char* gni_env = std::getenv("FEWHA_GATHER_NI");
-        const bool gni2 = batch > 2 && !(gni_env && std::atoi(gni_env) == 1);
-        gp.grows = batch <= 2 ? 4 : (gni2 ? 4 : 8);
+        // (batch 64: 8 rows, one or two instances per CTA -- with the per-chunk G blocks of
+        // the multi-instance gather 8 rows are 4-8 % faster than 4; FEWHA_GATHER_ROWS overrides)
+        // (runtime tap counts, gather_km > 4, keep one instance per CTA and 4 rows)
+        gp.grows = batch <= 2 || km > 4 ? 4 : 8;
         if (const char* v = std::getenv("FEWHA_GATHER_ROWS")) {
             const int r = std::atoi(v);
             if (r == 2 || r == 4 || r == 8) gp.grows = r;
@@ -503,12 +501,29 @@ Plan build_plan(const Geometry& g, int elem_bytes, int batch, int wa = 0, int wb
                     const auto nb = need_of(w, l, u);
                     need_max[static_cast<size_t>(w)] = std::max(need_max[static_cast<size_t>(w)], nb.first + NIg * nb.second);
                 }
-        // row-contracted blocks G of every WFS of a chunk (group rows x psi block columns), per instance
+        // row-contracted blocks G of every WFS of a chunk (group rows x psi block columns), per
+        // instance.  Single-instance plans size G for all W at the widest block; the
+        // multi-instance gather sizes it per chunk (WFS w's block at its own widest column
+        // count, offset gofs[w] inside the chunk), which is what lets several WFS share a chunk
+        std::vector<size_t> gw(static_cast<size_t>(W), 0), gofs(static_cast<size_t>(W), 0);
+        for (int w = 0; w < W; ++w) {
+            int cw = 1;
+            for (int l = 0; l < L; ++l) {
+                const int* bs = &pl.ti[static_cast<size_t>(gp.o_bs + ((w * L + l) * kMaxGU + 0) * 4)];
+                cw = std::max(cw, bs[3] - bs[2]);
+            }
+            gw[static_cast<size_t>(w)] = NIg > 1 ? a16(static_cast<size_t>(gp.grows) * cw * elem_bytes)
+                                                 : static_cast<size_t>(gp.grows) * cmax * elem_bytes;
+        }
+        if (NIg > 1)
+            for (int w = 0; w < W; ++w) need_max[static_cast<size_t>(w)] += NIg * gw[static_cast<size_t>(w)];
         gp.gbuf_bytes = static_cast<int>(a16(static_cast<size_t>(W) * gp.grows * cmax * elem_bytes));
-        const size_t fixed = a16(static_cast<size_t>(gp.gbuf_bytes) * NIg) + 1024;  // + static shared memory
+        const size_t fixed = (NIg > 1 ? 0 : a16(static_cast<size_t>(gp.gbuf_bytes) * NIg)) + 1024;  // + static shared memory
         // residency plan of k_gather (cluster.cuh): 2 CTAs/SM for a single instance, 3 for
         // batches (FEWHA_GATHER_MINB overrides: 2, 3 or 4)
-        gp.gather_minb = batch > 2 ? 3 : 2;  // (two instances per CTA: 3 as well; 2: equal)
+        // (batch 64, two instances per CTA, 8 rows: fp64 3 per SM 2.62 ms per step vs 2.79 at
+        // 4 and 2.85 at 2; fp32 4 per SM 1.66 vs 1.70 at 3)
+        gp.gather_minb = batch > 2 ? (elem_bytes == 4 && gp.gather_ni > 1 ? 4 : 3) : 2;
         if (const char* v = std::getenv("FEWHA_GATHER_MINB")) {
             const int m = std::atoi(v);
             if (m >= 2 && m <= 4) gp.gather_minb = m;
@@ -530,6 +545,28 @@ Plan build_plan(const Geometry& g, int elem_bytes, int batch, int wa = 0, int wb
         }
         gp.gchunk[++gp.nchunk] = wb;
         gp.chunk_bytes = static_cast<int>(chunk_max);
+        {  // G offsets inside each chunk; per-instance G bytes = the largest chunk's
+            size_t gmax = 0;
+            for (int k = 0; k < gp.nchunk; ++k) {
+                size_t o = 0;
+                for (int w = gp.gchunk[k]; w < gp.gchunk[k + 1]; ++w) {
+                    gofs[static_cast<size_t>(w)] = o;
+                    o += gw[static_cast<size_t>(w)];
+                }
+                gmax = std::max(gmax, o);
+            }
+            if (NIg > 1) {  // chunk_bytes counted the G blocks: keep only tables + psi there
+                gp.gbuf_bytes = static_cast<int>(gmax);
+                size_t cb = 0;
+                for (int k = 0; k < gp.nchunk; ++k) {
+                    size_t u = 0;
+                    for (int w = gp.gchunk[k]; w < gp.gchunk[k + 1]; ++w)
+                        u += need_max[static_cast<size_t>(w)] - NIg * gw[static_cast<size_t>(w)];
+                    cb = std::max(cb, u);
+                }
+                gp.chunk_bytes = static_cast<int>(cb);
+            }
+        }
         // gather tables (mirrors k_gather() in cluster.cuh), in gblob:
         //   column stencils, once per (layer, WFS), WFS ascending within a layer:
         //     [first int16 side+3][col idx int16 nc][col frac nc]
@@ -676,6 +713,7 @@ Plan build_plan(const Geometry& g, int elem_bytes, int batch, int wa = 0, int wb
                         d[8] = static_cast<int>(coff_wl[static_cast<size_t>(w * L + l)]);
                         d[9] = static_cast<int>(col_bytes(gp.side[l], bs[3] - bs[2]));
                         d[10] = static_cast<int>(psum);  // psi bytes of the chunk per instance (k_gather_ni)
+                        d[11] = static_cast<int>(gofs[static_cast<size_t>(w)] / elem_bytes);  // G block offset (k_gather_ni)
                         poff += nb.second;
                     }
                 }

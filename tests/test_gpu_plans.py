@@ -57,7 +57,7 @@ def test_elt_batch_plan_per_instance_vs_oracle(precision):
     plan = g.plan_info()
     assert plan["tail"] == 2 * plan["cluster_ctas"] and plan["inverse_staged"] == 0
     assert plan["whole_layer"] == 1  # batches: whole-layer transforms (layer_whole.cuh)
-    assert plan["gather_rows"] == 4 and plan["gather_ctas_per_sm"] == 3
+    assert plan["gather_rows"] == 8 and plan["gather_ctas_per_sm"] == (3 if precision == 64 else 4)
     assert plan["gather_instances"] == 2 and plan["wfs_instances"] == (2 if precision == 64 else 4)
     orc = [_oracle(name) for _ in range(B)]
     lay = [smooth_layers(orc[0], 30 + i) for i in range(B)]
