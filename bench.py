@@ -316,7 +316,7 @@ def graph_function_profile(rec, frames, before, d, b, batch=1):
     rec.enable_telemetry(True)
     plan = rec.plan_info()
     whole = plan.get("whole_layer", 0) == 1  # batched plans: whole-layer transform kernels
-    gni = plan.get("gather_instances", 1) > 1  # ... and the multi-instance gather (k_gather_ni)
+    gdirect = plan.get("gather_direct", 0) == 1  # the direct gather (k_gather_direct)
     acc, frame_ms = {}, []
     for f in range(frames + 2):
         before(f)
@@ -329,8 +329,8 @@ def graph_function_profile(rec, frames, before, d, b, batch=1):
             fn = FUNC[kind]
             if whole and fn in ("k_fwd_cluster", "k_inv_cluster"):
                 fn = fn.replace("_cluster", "_layer")
-            if gni and fn == "k_gather":
-                fn = "k_gather_ni"
+            if gdirect and fn == "k_gather":
+                fn = "k_gather_direct"
             e = acc.setdefault(fn, {"launches": 0, "ms": 0.0, "bytes": 0})
             e["launches"] += 1
             e["ms"] += t

@@ -146,6 +146,7 @@ typedef struct {
         launches_per_step;
     int whole_layer; /* 1: layer transforms one CTA per (layer, instance) (batched plans), 0: clusters */
     int gather_instances, wfs_instances; /* instances per CTA of the adjoint gather / WFS-tile kernels */
+    int gather_direct; /* 1: the direct gather (compile-time taps), 0: the row-contracted k_gather */
 } fewha_gpu_plan_t;
 int fewha_gpu_plan_info(fewha_gpu_t h, fewha_gpu_plan_t* out);
 /* Runs ONE frame eagerly (not from the graph) with a CUDA event after every

@@ -83,7 +83,7 @@ class _Telemetry(C.Structure):
 class _Plan(C.Structure):
     _fields_ = [(k, C.c_int) for k in ("cluster_ctas", "tail", "gather_rows", "gather_ctas_per_sm", "inverse_staged",
                                        "wfs_ctas_per_sm", "wfs_tiles", "launches_per_step", "whole_layer",
-                                       "gather_instances", "wfs_instances")]
+                                       "gather_instances", "wfs_instances", "gather_direct")]
 
 
 class _DevBufs(C.Structure):

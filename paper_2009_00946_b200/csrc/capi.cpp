@@ -245,6 +245,7 @@ int fewha_gpu_plan_info(fewha_gpu_t h, fewha_gpu_plan_t* out) {
         out->whole_layer = pi.whole_layer;
         out->gather_instances = pi.gather_instances;
         out->wfs_instances = pi.wfs_instances;
+        out->gather_direct = pi.gather_direct;
     })
 }
 float fewha_gpu_debug_bench_dwt(fewha_gpu_t h, int variant, int inverse, int reps, int threads) {

@@ -794,16 +794,21 @@ __global__ void __launch_bounds__(256, MINB) k_gather(const GeoParams gp, const 
 }
 
 // ---------------------------------------------------------------------------
-// The gather for NI consecutive instances per CTA (batched plans): the chunk's tables
-// are staged once and shared, the psi blocks of the NI instances sit one after the other
-// (instance ni at soff + ni * pad0, pad0 = the chunk's psi bytes per instance), and every
-// thread carries NI instances' row and column sums (more loads in flight, index math and
-// weights shared).  Same arithmetic per instance as gather_group.
+// The direct gather (batched plans, gp.gather_direct): no row-contracted block in
+// shared memory.  Per WFS a thread (layer column J, rows i0..i0+rows_pt-1) forms
+//   h(r) = sum_b cw(J, b) psi(r, c0(J) + b)        for the psi rows r its rows touch,
+//   y(i, J) += sum_a rw(i, a) h(r0(i) + a),
+// the source runs [r0, r0 + KM) / [c0, c0 + KM) contiguous and zero-padded (host tables,
+// engine.cu run_table).  r0 ascends with i, so the KM values h(r0(i) + .) live in a
+// register ring that only moves forward: each psi value is read once per thread and
+// instance, with no barrier between the two contractions and the staging budget all
+// for psi blocks.  NI instances per CTA share the tables (instance ni's psi blocks at
+// soff + ni * pad0, pad0 = the chunk's psi bytes per instance).
 // ---------------------------------------------------------------------------
 template <typename T, int NI>
-__device__ __forceinline__ void gather_issue_ni(const GeoParams& gp, const T* psi_b, const GDesc* desc, int w0, int w1,
-                                                unsigned char* stage, unsigned long long* mbar, bool tables, bool psi,
-                                                int ninst) {
+__device__ __forceinline__ void gather_issue_direct(const GeoParams& gp, const T* psi_b, const GDesc* desc, int w0,
+                                                    int w1, unsigned char* stage, unsigned long long* mbar,
+                                                    bool tables, bool psi, int ninst) {
     const int lane = threadIdx.x;
     if (tables && lane == 31) {
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -815,8 +820,9 @@ __device__ __forceinline__ void gather_issue_ni(const GeoParams& gp, const T* ps
         bulk_g2s(stage + gather_row_bytes(desc, w0, w1), gp.gblob + desc[w0].ctoff, bytes, mbar);
     }
     const int nw = w1 - w0;
-    if (psi && lane < nw * NI) {
-        const int ni = lane / nw, w = w0 + (lane - ni * nw);
+    if (!psi) return;
+    for (int t = lane; t < nw * NI; t += 32) {
+        const int ni = t / nw, w = w0 + (t - ni * nw);
         const GDesc d = desc[w];
         const int nr = d.ihi - d.ilo, np = gp.ns[w] + 1;
         if (nr > 0 && ni < ninst) {
@@ -830,9 +836,8 @@ __device__ __forceinline__ void gather_issue_ni(const GeoParams& gp, const T* ps
 }
 
 template <typename T, int KM, int ROWS, int NI>
-__device__ void gather_group_ni(const GeoParams& gp, const T* __restrict__ psi_b, int l, T* __restrict__ y, T* gbuf,
-                                unsigned char* stage, const GDesc* desc, unsigned long long* mbar, int ninst) {
-    static_assert(KM > 0, "the multi-instance gather takes the compile-time tap counts");
+__device__ void gather_direct_group(const GeoParams& gp, const T* __restrict__ psi_b, int l, T* __restrict__ y,
+                                    unsigned char* stage, const GDesc* desc, unsigned long long* mbar, int ninst) {
     const int side = gp.side[l];
     const int R = side < ROWS ? side : ROWS;
     const int tid = threadIdx.x, nthr = blockDim.x;
@@ -842,103 +847,97 @@ __device__ void gather_group_ni(const GeoParams& gp, const T* __restrict__ psi_b
     const int J = tid & (side - 1), grp = tid >> lside;
     const int i0 = grp * rows_pt;
     const bool worker = grp < groups;
-    const int gin = gp.gbuf_bytes / static_cast<int>(sizeof(T));  // G stride per instance (blocks at desc[w].pad1)
-    const int o_rw = align16(R * KM * 2);
-    const int o_idx = align16((side + 3) * 2);
-    T out[NI][ROWS];
+    const int o_rw = align16(R * 2);     // row table: [r0 int16 R][rw R x KM]
+    const int o_cw = align16(side * 2);  // column table: [c0 int16 side][cw side x KM]
+    constexpr int RP = ROWS / 2;  // rows per thread: side <= 128 (host plan), 256 threads
+    T out[NI][RP];
 #pragma unroll
     for (int ni = 0; ni < NI; ++ni)
 #pragma unroll
-        for (int k = 0; k < ROWS; ++k) out[ni][k] = T(0);
+        for (int k = 0; k < RP; ++k) out[ni][k] = T(0);
     for (int k = 0; k < gp.nchunk; ++k) {
         const int w0 = gp.gchunk[k], w1 = gp.gchunk[k + 1];
         if (k > 0 && tid < 32) {
-            gather_issue_ni<T, NI>(gp, psi_b, desc, w0, w1, stage, mbar, true, true, ninst);
+            gather_issue_direct<T, NI>(gp, psi_b, desc, w0, w1, stage, mbar, true, true, ninst);
             __syncwarp();
             if (tid == 0) mbar_arrive(mbar);
         }
         mbar_wait(mbar, static_cast<unsigned>(k & 1));
         const int rt0 = desc[w0].rtoff, ct0 = desc[w0].ctoff;
         const unsigned char* cstage = stage + gather_row_bytes(desc, w0, w1);
-        {
-            constexpr int CL = 128;
-            const int ng = nthr / CL > 0 ? nthr / CL : 1, gq = tid / CL, lane = tid % CL;
-            for (int w = w0 + gq; w < w1; w += ng) {
-                const GDesc d = desc[w];
-                const int nr = d.ihi - d.ilo, np = gp.ns[w] + 1, nc = d.jhi - d.jlo;
-                if (nr <= 0) continue;
-                const unsigned char* tp = stage + (d.rtoff - rt0);
-                const short* __restrict__ rs = reinterpret_cast<const short*>(tp);
-                const T* __restrict__ rw = reinterpret_cast<const T*>(tp + o_rw);
-                const T* blk[NI];
-#pragma unroll
-                for (int ni = 0; ni < NI; ++ni) {
-                    const unsigned shift = static_cast<unsigned>(
-                        reinterpret_cast<uintptr_t>(psi_b + static_cast<size_t>(ni < ninst ? ni : 0) * gp.Nw + d.src) & 15u);
-                    blk[ni] = reinterpret_cast<const T*>(stage + d.soff + (ni < ninst ? ni : 0) * d.pad0 + shift) + d.jlo;
-                }
-                for (int c = lane; c < nc; c += CL) {
-#pragma unroll
-                    for (int i = 0; i < ROWS; ++i) {
-                        if (i >= R) break;
-                        T g[NI];
-#pragma unroll
-                        for (int ni = 0; ni < NI; ++ni) g[ni] = T(0);
-#pragma unroll
-                        for (int q = 0; q < KM; ++q) {
-                            const T wq = rw[i * KM + q];
-                            const int ro = rs[i * KM + q] * np + c;
-#pragma unroll
-                            for (int ni = 0; ni < NI; ++ni) g[ni] += wq * blk[ni][ro];
-                        }
-#pragma unroll
-                        for (int ni = 0; ni < NI; ++ni) gbuf[ni * gin + d.pad1 + i * nc + c] = g[ni];
-                    }
-                }
-            }
-        }
-        __syncthreads();
         if (worker) {
             for (int w = w0; w < w1; ++w) {
                 const GDesc d = desc[w];
-                const int nr = d.ihi - d.ilo, nc = d.jhi - d.jlo;
+                const int nr = d.ihi - d.ilo, np = gp.ns[w] + 1, nc = d.jhi - d.jlo;
                 if (nr <= 0) continue;
-                const unsigned char* tp = cstage + (d.ctoff - ct0);
-                const short* first = reinterpret_cast<const short*>(tp);
-                const short* cidx = reinterpret_cast<const short*>(tp + o_idx);
-                const T* cfr = reinterpret_cast<const T*>(tp + o_idx + align16(nc * 2));
-                const int c0 = first[J], c1 = first[J + 2];
-                T wt[KM];
+                const unsigned char* rt = stage + (d.rtoff - rt0);
+                const unsigned char* ct = cstage + (d.ctoff - ct0);
+                const int c0 = reinterpret_cast<const short*>(ct)[J];
+                const T* __restrict__ cwp = reinterpret_cast<const T*>(ct + o_cw) + J * KM;
+                T cw[KM];
                 int cc[KM];
 #pragma unroll
-                for (int q = 0; q < KM; ++q) {
-                    const int c = min(c0 + q, nc - 1);
-                    const T fr = cfr[c];
-                    wt[q] = c0 + q < c1 ? (cidx[c] == J ? T(1) - fr : fr) : T(0);
-                    cc[q] = c;
+                for (int b = 0; b < KM; ++b) {
+                    cw[b] = cwp[b];
+                    cc[b] = min(c0 + b, nc - 1);
                 }
+                const T* blk[NI];
 #pragma unroll
-                for (int k2 = 0; k2 < ROWS; ++k2) {
-                    if (k2 >= rows_pt) break;
+                for (int ni = 0; ni < NI; ++ni) {
+                    const int nj = ni < ninst ? ni : 0;
+                    const unsigned shift = static_cast<unsigned>(
+                        reinterpret_cast<uintptr_t>(psi_b + static_cast<size_t>(nj) * gp.Nw + d.src) & 15u);
+                    blk[ni] = reinterpret_cast<const T*>(stage + d.soff + nj * d.pad0 + shift) + d.jlo;
+                }
+                const short* __restrict__ r0t = reinterpret_cast<const short*>(rt);
+                const T* __restrict__ rwt = reinterpret_cast<const T*>(rt + o_rw);
+                auto hrow = [&](int r, T (&h)[NI]) {
+                    const int ro = min(r, nr - 1) * np;
 #pragma unroll
                     for (int ni = 0; ni < NI; ++ni) {
-                        const T* g = gbuf + ni * gin + d.pad1 + (i0 + k2) * nc;
                         T s = T(0);
 #pragma unroll
-                        for (int q = 0; q < KM; ++q) s += wt[q] * g[cc[q]];
+                        for (int b = 0; b < KM; ++b) s += cw[b] * blk[ni][ro + cc[b]];
+                        h[ni] = s;
+                    }
+                };
+                int cur = r0t[i0];
+                T h[KM][NI];
+#pragma unroll
+                for (int a = 0; a < KM; ++a) hrow(cur + a, h[a]);
+#pragma unroll
+                for (int k2 = 0; k2 < RP; ++k2) {
+                    if (k2 >= rows_pt) break;
+                    const int r = r0t[i0 + k2];
+                    while (cur < r) {  // advance the ring (first sources ascend with the row)
+                        ++cur;
+#pragma unroll
+                        for (int a = 0; a + 1 < KM; ++a)
+#pragma unroll
+                            for (int ni = 0; ni < NI; ++ni) h[a][ni] = h[a + 1][ni];
+                        hrow(cur + KM - 1, h[KM - 1]);
+                    }
+                    T wa[KM];
+#pragma unroll
+                    for (int a = 0; a < KM; ++a) wa[a] = rwt[(i0 + k2) * KM + a];
+#pragma unroll
+                    for (int ni = 0; ni < NI; ++ni) {
+                        T s = T(0);
+#pragma unroll
+                        for (int a = 0; a < KM; ++a) s += wa[a] * h[a][ni];
                         out[ni][k2] += s;
                     }
                 }
             }
         }
-        __syncthreads();
+        __syncthreads();  // chunk consumed before the next one is staged
     }
     if (worker) {
 #pragma unroll
         for (int ni = 0; ni < NI; ++ni) {
             if (ni >= ninst) break;
 #pragma unroll
-            for (int k = 0; k < ROWS; ++k) {
+            for (int k = 0; k < RP; ++k) {
                 if (k >= rows_pt) break;
                 y[static_cast<size_t>(ni) * gp.n + (i0 + k) * side + J] = out[ni][k];
             }
@@ -946,9 +945,9 @@ __device__ void gather_group_ni(const GeoParams& gp, const T* __restrict__ psi_b
     }
 }
 
-// grid (side/grows, L, ceil(B / NI)); batched plans with compile-time tap counts (gather_km <= 4)
+// grid (side/grows, L, ceil(B / NI)); plans with gp.gather_direct (compile-time taps, km <= 4)
 template <typename T, int MINB, int NI>
-__global__ void __launch_bounds__(256, MINB) k_gather_ni(const GeoParams gp, const Bufs<T> bf, int count) {
+__global__ void __launch_bounds__(256, MINB) k_gather_direct(const GeoParams gp, const Bufs<T> bf, int count, int late) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ GDesc s_desc[kMaxW];
     __shared__ unsigned long long s_mbar;
@@ -958,8 +957,7 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ni(const GeoParams gp, con
     const int R = side < gp.grows ? side : gp.grows;
     if (u * R >= side) return;
     const int tid = threadIdx.x;
-    T* gbuf = reinterpret_cast<T*>(smem_raw);
-    unsigned char* stage = smem_raw + align16(gp.gbuf_bytes * NI);
+    unsigned char* stage = smem_raw;
     const T* psi = bf.psi + static_cast<size_t>(b0) * gp.Nw;
     if (tid < 32) {
         if (tid < gp.W) {
@@ -972,30 +970,33 @@ __global__ void __launch_bounds__(256, MINB) k_gather_ni(const GeoParams gp, con
             asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         }
         __syncwarp();
-        gather_issue_ni<T, NI>(gp, psi, s_desc, gp.gchunk[0], gp.gchunk[1], stage, &s_mbar, true, false, ninst);
+        gather_issue_direct<T, NI>(gp, psi, s_desc, gp.gchunk[0], gp.gchunk[1], stage, &s_mbar, true, false, ninst);
     }
     pdl_wait();
-    pdl_launch_dependents();
+    if (!late) pdl_launch_dependents();
     if (tid < 32) {
-        gather_issue_ni<T, NI>(gp, psi, s_desc, gp.gchunk[0], gp.gchunk[1], stage, &s_mbar, false, true, ninst);
+        gather_issue_direct<T, NI>(gp, psi, s_desc, gp.gchunk[0], gp.gchunk[1], stage, &s_mbar, false, true, ninst);
         __syncwarp();
         if (tid == 0) mbar_arrive(&s_mbar);
     }
     __syncthreads();
     T* y = bf.y + static_cast<size_t>(b0) * gp.n + gp.coff[l] + static_cast<size_t>(u) * R * side;
-#define FEWHA_GATHER_NI_KM(ROWS)                                                                                 \
-    switch (gp.gather_km) {                                                                                     \
-        case 1: gather_group_ni<T, 1, ROWS, NI>(gp, psi, l, y, gbuf, stage, s_desc, &s_mbar, ninst); break;    \
-        case 2: gather_group_ni<T, 2, ROWS, NI>(gp, psi, l, y, gbuf, stage, s_desc, &s_mbar, ninst); break;    \
-        case 3: gather_group_ni<T, 3, ROWS, NI>(gp, psi, l, y, gbuf, stage, s_desc, &s_mbar, ninst); break;    \
-        default: gather_group_ni<T, 4, ROWS, NI>(gp, psi, l, y, gbuf, stage, s_desc, &s_mbar, ninst); break;   \
+#define FEWHA_GATHER_D_KM(ROWS)                                                                                   \
+    switch (gp.gather_km) {                                                                                       \
+        case 1: gather_direct_group<T, 1, ROWS, NI>(gp, psi, l, y, stage, s_desc, &s_mbar, ninst); break;        \
+        case 2: gather_direct_group<T, 2, ROWS, NI>(gp, psi, l, y, stage, s_desc, &s_mbar, ninst); break;        \
+        case 3: gather_direct_group<T, 3, ROWS, NI>(gp, psi, l, y, stage, s_desc, &s_mbar, ninst); break;        \
+        default: gather_direct_group<T, 4, ROWS, NI>(gp, psi, l, y, stage, s_desc, &s_mbar, ninst); break;       \
     }
-    if (gp.grows == 4) {
-        FEWHA_GATHER_NI_KM(4)
+    if (gp.grows == 2) {
+        FEWHA_GATHER_D_KM(2)
+    } else if (gp.grows == 4) {
+        FEWHA_GATHER_D_KM(4)
     } else {
-        FEWHA_GATHER_NI_KM(8)
+        FEWHA_GATHER_D_KM(8)
     }
-#undef FEWHA_GATHER_NI_KM
+#undef FEWHA_GATHER_D_KM
+    if (late) pdl_launch_dependents();
 }
 
 // Deterministic sum of the dot partials of one iteration by warp 0: fixed

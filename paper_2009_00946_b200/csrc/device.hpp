@@ -70,7 +70,8 @@ struct GeoParams {
     int inv_staged;   // inverse kernel: operands staged in shared memory by TMA (1) or read from global (0)
     int gather_km;    // max gather taps per layer row/column
     int o_bs;         // [((w*L+l)*kMaxGU + u)*4] psi source block {ilo, ihi, jlo, jhi} of each gather row group
-    int bd_rows_max, bd_cols_max;
+    int gather_direct;  // 1: k_gather_direct and its tables (batched plans), 0: k_gather / k_gather_ni
+    int bd_cols_max;
     unsigned long long* stamps;  // optional phase timestamps [block][16] (nullptr: off)
     const unsigned char* gblob;  // per-(w,l) gather blobs of the engine's precision (see cluster.cuh)
     int chunk_bytes;  // shared-memory bytes of the largest staged WFS chunk of the gather

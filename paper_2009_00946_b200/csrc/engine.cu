@@ -415,17 +415,24 @@ Plan build_plan(const Geometry& g, int elem_bytes, int batch, int wa = 0, int wb
             }
         // (km > 4: coarse layers under dense aperture sampling take the runtime-tap path)
         gp.gather_km = km;
+        // the direct gather (cluster.cuh k_gather_direct) wherever the tap counts are
+        // compile-time (km <= 4), else k_gather (runtime taps); FEWHA_GATHER_DIRECT = 0 forces
+        // k_gather.  Measured (ELT MCAO-84, fp64): single frame 0.1864 -> 0.180 ms, batch-64
+        // gather launch 145 -> 113 us
+        int direct = km <= 4;
+        if (const char* v = std::getenv("FEWHA_GATHER_DIRECT")) direct = std::atoi(v) == 1 && km <= 4;
+        gp.gather_direct = direct;
         // psi source blocks per (w, l, gather row group u)
         // rows per gather CTA: 4 for a single instance (288 CTAs at the ELT scale, two per
-        // SM), larger groups for batches amortise each CTA's staging and setup
-        // (batch 64: 8 rows, one or two instances per CTA -- with the per-chunk G blocks of
-        // the multi-instance gather 8 rows are 4-8 % faster than 4; FEWHA_GATHER_ROWS overrides)
-        // (runtime tap counts, gather_km > 4, keep one instance per CTA and 4 rows)
+        // SM; 8: 0.1945 ms), 8 for batches (batch 64, 4 instances per CTA: 2.48 vs 2.63 ms per
+        // step); FEWHA_GATHER_ROWS overrides
         gp.grows = batch <= 2 || km > 4 ? 4 : 8;
         if (const char* v = std::getenv("FEWHA_GATHER_ROWS")) {
             const int r = std::atoi(v);
             if (r == 2 || r == 4 || r == 8) gp.grows = r;
         }
+        // (k_gather_direct: layer sides <= 128 -- at most half the group rows per thread)
+        if (pl.maxside > 128) direct = gp.gather_direct = 0;
         auto grp_rows = [&](int side) { return std::min(gp.grows, side); };
         gp.o_bs = static_cast<int>(pl.ti.size());
         pl.ti.resize(pl.ti.size() + static_cast<size_t>(W * L * kMaxGU * 4), 0);
@@ -463,15 +470,19 @@ Plan build_plan(const Geometry& g, int elem_bytes, int batch, int wa = 0, int wb
                     }
                 }
             }
-        gp.bd_rows_max = rmax;
+        (void)rmax;
         gp.bd_cols_max = cmax;
         // staged bytes per WFS (mirrors gather_tab_bytes()/psi_bytes() in cluster.cuh)
         auto a16 = [](size_t v) { return (v + 15) & ~size_t(15); };
         // row-tap table of one (layer, row group, WFS) and column stencil of one (layer, WFS)
+        // (direct gather: [first source int16 per node][km weights per node], for the R group
+        // rows and for the side layer columns)
         auto row_bytes = [&](int R) {
+            if (direct) return a16(static_cast<size_t>(R) * 2) + a16(static_cast<size_t>(R) * km * elem_bytes);
             return a16(static_cast<size_t>(R) * km * 2) + a16(static_cast<size_t>(R) * km * elem_bytes);
         };
         auto col_bytes = [&](int side, int nc) {
+            if (direct) return a16(static_cast<size_t>(side) * 2) + a16(static_cast<size_t>(side) * km * elem_bytes);
             return a16(static_cast<size_t>(side + 3) * 2) + a16(static_cast<size_t>(nc) * 2) +
                    a16(static_cast<size_t>(nc) * elem_bytes);
         };
@@ -485,14 +496,14 @@ Plan build_plan(const Geometry& g, int elem_bytes, int batch, int wa = 0, int wb
                 tab_bytes(Rl, side, bs[3] - bs[2]),
                 a16(static_cast<size_t>(bs[1] - bs[0]) * (g.wfs[w].n_subap + 1) * elem_bytes + 16));
         };
-        // instances per CTA (batched plans: 2, sharing the staged tables; FEWHA_GATHER_NI
-        // overrides; compile-time tap counts only)
-        gp.gather_ni = batch > 2 ? 2 : 1;
+        // instances per CTA of the direct gather (batched plans: 4, sharing the staged tables;
+        // batch 64 fp64: 2.48 ms per step vs 2.54 with 2; FEWHA_GATHER_NI = 1, 2 or 4 overrides)
+        gp.gather_ni = batch > 2 ? 4 : 1;
         if (const char* v = std::getenv("FEWHA_GATHER_NI")) {
             const int ni = std::atoi(v);
-            if (ni == 1 || ni == 2) gp.gather_ni = ni;
+            if (ni == 1 || ni == 2 || ni == 4) gp.gather_ni = ni;
         }
-        if (gp.gather_km > 4 || (gp.grows != 4 && gp.grows != 8)) gp.gather_ni = 1;
+        if (!direct) gp.gather_ni = 1;
         const size_t NIg = static_cast<size_t>(gp.gather_ni);
         std::vector<size_t> need_max(static_cast<size_t>(W), 0);
         for (int w = 0; w < W; ++w)
@@ -501,29 +512,15 @@ Plan build_plan(const Geometry& g, int elem_bytes, int batch, int wa = 0, int wb
                     const auto nb = need_of(w, l, u);
                     need_max[static_cast<size_t>(w)] = std::max(need_max[static_cast<size_t>(w)], nb.first + NIg * nb.second);
                 }
-        // row-contracted blocks G of every WFS of a chunk (group rows x psi block columns), per
-        // instance.  Single-instance plans size G for all W at the widest block; the
-        // multi-instance gather sizes it per chunk (WFS w's block at its own widest column
-        // count, offset gofs[w] inside the chunk), which is what lets several WFS share a chunk
-        std::vector<size_t> gw(static_cast<size_t>(W), 0), gofs(static_cast<size_t>(W), 0);
-        for (int w = 0; w < W; ++w) {
-            int cw = 1;
-            for (int l = 0; l < L; ++l) {
-                const int* bs = &pl.ti[static_cast<size_t>(gp.o_bs + ((w * L + l) * kMaxGU + 0) * 4)];
-                cw = std::max(cw, bs[3] - bs[2]);
-            }
-            gw[static_cast<size_t>(w)] = NIg > 1 ? a16(static_cast<size_t>(gp.grows) * cw * elem_bytes)
-                                                 : static_cast<size_t>(gp.grows) * cmax * elem_bytes;
-        }
-        if (NIg > 1)
-            for (int w = 0; w < W; ++w) need_max[static_cast<size_t>(w)] += NIg * gw[static_cast<size_t>(w)];
-        gp.gbuf_bytes = static_cast<int>(a16(static_cast<size_t>(W) * gp.grows * cmax * elem_bytes));
-        const size_t fixed = (NIg > 1 ? 0 : a16(static_cast<size_t>(gp.gbuf_bytes) * NIg)) + 1024;  // + static shared memory
-        // residency plan of k_gather (cluster.cuh): 2 CTAs/SM for a single instance, 3 for
-        // batches (FEWHA_GATHER_MINB overrides: 2, 3 or 4)
-        // (batch 64, two instances per CTA, 8 rows: fp64 3 per SM 2.62 ms per step vs 2.79 at
-        // 4 and 2.85 at 2; fp32 4 per SM 1.66 vs 1.70 at 3)
-        gp.gather_minb = batch > 2 ? (elem_bytes == 4 && gp.gather_ni > 1 ? 4 : 3) : 2;
+        // k_gather's row-contracted blocks G of every WFS of a chunk (group rows x widest psi
+        // block); the direct gather has none
+        gp.gbuf_bytes = direct ? 0 : static_cast<int>(a16(static_cast<size_t>(W) * gp.grows * cmax * elem_bytes));
+        const size_t fixed = a16(static_cast<size_t>(gp.gbuf_bytes)) + 1024;  // + static shared memory
+        // residency plan of the gather (cluster.cuh gather_smem_kb): 2 CTAs/SM for a single
+        // instance (direct: 0.180 ms vs 0.184 at 3); batches of the direct gather, 4 instances
+        // per CTA: fp64 2 (2.48 ms per step vs 2.64 at 3, which spills), fp32 4 (1.58 vs 1.62
+        // at 2); k_gather batches 3.  FEWHA_GATHER_MINB overrides: 2, 3 or 4
+        gp.gather_minb = batch <= 2 ? 2 : !direct ? 3 : elem_bytes == 4 ? 4 : 2;
         if (const char* v = std::getenv("FEWHA_GATHER_MINB")) {
             const int m = std::atoi(v);
             if (m >= 2 && m <= 4) gp.gather_minb = m;
@@ -545,28 +542,6 @@ Plan build_plan(const Geometry& g, int elem_bytes, int batch, int wa = 0, int wb
         }
         gp.gchunk[++gp.nchunk] = wb;
         gp.chunk_bytes = static_cast<int>(chunk_max);
-        {  // G offsets inside each chunk; per-instance G bytes = the largest chunk's
-            size_t gmax = 0;
-            for (int k = 0; k < gp.nchunk; ++k) {
-                size_t o = 0;
-                for (int w = gp.gchunk[k]; w < gp.gchunk[k + 1]; ++w) {
-                    gofs[static_cast<size_t>(w)] = o;
-                    o += gw[static_cast<size_t>(w)];
-                }
-                gmax = std::max(gmax, o);
-            }
-            if (NIg > 1) {  // chunk_bytes counted the G blocks: keep only tables + psi there
-                gp.gbuf_bytes = static_cast<int>(gmax);
-                size_t cb = 0;
-                for (int k = 0; k < gp.nchunk; ++k) {
-                    size_t u = 0;
-                    for (int w = gp.gchunk[k]; w < gp.gchunk[k + 1]; ++w)
-                        u += need_max[static_cast<size_t>(w)] - NIg * gw[static_cast<size_t>(w)];
-                    cb = std::max(cb, u);
-                }
-                gp.chunk_bytes = static_cast<int>(cb);
-            }
-        }
         // gather tables (mirrors k_gather() in cluster.cuh), in gblob:
         //   column stencils, once per (layer, WFS), WFS ascending within a layer:
         //     [first int16 side+3][col idx int16 nc][col frac nc]
@@ -628,10 +603,57 @@ Plan build_plan(const Geometry& g, int elem_bytes, int batch, int wa = 0, int wb
             pl.gblob.insert(pl.gblob.end(), b, b + n);
         };
         auto pad16 = [&](size_t start) { pl.gblob.resize(start + a16(pl.gblob.size() - start), 0); };
+        // direct-gather tables: per layer node (row or column) the first source of its
+        // contiguous source run and km weights (zero-padded); first sources ascend with the
+        // node (empty nodes carry their neighbour's), which the kernel's row ring relies on
+        auto run_table = [&](const std::vector<std::vector<Entry>>& tab, std::vector<int>& first,
+                             std::vector<double>& wt) {
+            const int side = static_cast<int>(tab.size());
+            first.assign(static_cast<size_t>(side), 0);
+            wt.assign(static_cast<size_t>(side) * km, 0.0);
+            int carry = 0;
+            for (const auto& v : tab)
+                if (!v.empty()) { carry = v.front().src; break; }
+            for (int I = 0; I < side; ++I) {
+                if (!tab[I].empty()) carry = tab[I].front().src;
+                first[static_cast<size_t>(I)] = carry;
+                for (const auto& en : tab[I]) {
+                    const int a = en.src - carry;
+                    if (a < 0 || a >= km) throw std::logic_error("gather tables: non-contiguous taps");
+                    wt[static_cast<size_t>(I) * km + a] = en.w;
+                }
+                if (I > 0 && first[static_cast<size_t>(I)] < first[static_cast<size_t>(I - 1)])
+                    throw std::logic_error("gather tables: descending taps");
+            }
+        };
+        auto put_first = [&](const std::vector<int>& first, int i0, int n, int rel, int lim) {
+            const size_t start = pl.gblob.size();
+            for (int I = i0; I < i0 + n; ++I) {
+                const int v = std::min(std::max(first[static_cast<size_t>(I)] - rel, 0), std::max(lim - 1, 0));
+                if (v > 32767) throw ConfigError("invalid geometry: gather index overflow");
+                const short s16 = static_cast<short>(v);
+                const auto* p = reinterpret_cast<const unsigned char*>(&s16);
+                pl.gblob.insert(pl.gblob.end(), p, p + 2);
+            }
+            pl.gblob.resize(start + a16(pl.gblob.size() - start), 0);
+        };
         // column stencils: jlo/jhi of a (w, l) are the same in every row group (bs[2], bs[3])
         std::vector<size_t> coff_wl(static_cast<size_t>(W * L), 0);
+        std::vector<int> dfirst;
+        std::vector<double> dwt;
         for (int l = 0; l < L; ++l)
-            for (int w = 0; w < W; ++w) {
+            for (int w = 0; w < W && direct; ++w) {
+                const int side = gp.side[l];
+                const int* bs = &pl.ti[static_cast<size_t>(gp.o_bs + ((w * L + l) * kMaxGU + 0) * 4)];
+                const size_t start = pl.gblob.size();
+                coff_wl[static_cast<size_t>(w * L + l)] = start;
+                run_table(cols[w * L + l], dfirst, dwt);
+                put_first(dfirst, 0, side, bs[2], bs[3] - bs[2]);
+                put_wt(dwt, 0, side);
+                if (pl.gblob.size() - start != col_bytes(side, bs[3] - bs[2])) throw std::logic_error("gather tables: size mismatch");
+            }
+        for (int l = 0; l < L; ++l)
+            for (int w = 0; w < W && !direct; ++w) {
                 const int side = gp.side[l];
                 const int* bs = &pl.ti[static_cast<size_t>(gp.o_bs + ((w * L + l) * kMaxGU + 0) * 4)];
                 const int jlo = bs[2], nc = bs[3] - bs[2];
@@ -677,8 +699,13 @@ Plan build_plan(const Geometry& g, int elem_bytes, int batch, int wa = 0, int wb
                 for (int w = 0; w < W; ++w) {
                     const int* bs = &pl.ti[static_cast<size_t>(gp.o_bs + ((w * L + l) * kMaxGU + u) * 4)];
                     const size_t start = pl.gblob.size();
-                    padded(rows[w * L + l], rsrc, rwt);
-                    put_i16(rsrc, I0, Rl, bs[0], bs[1] - bs[0]);
+                    if (direct) {
+                        run_table(rows[w * L + l], rsrc, rwt);
+                        put_first(rsrc, I0, Rl, bs[0], bs[1] - bs[0]);
+                    } else {
+                        padded(rows[w * L + l], rsrc, rwt);
+                        put_i16(rsrc, I0, Rl, bs[0], bs[1] - bs[0]);
+                    }
                     put_wt(rwt, I0, Rl);
                     if (pl.gblob.size() - start != row_bytes(Rl)) throw std::logic_error("gather tables: size mismatch");
                 }
@@ -712,8 +739,7 @@ Plan build_plan(const Geometry& g, int elem_bytes, int batch, int wa = 0, int wb
                         d[7] = static_cast<int>(row_bytes(Rl));
                         d[8] = static_cast<int>(coff_wl[static_cast<size_t>(w * L + l)]);
                         d[9] = static_cast<int>(col_bytes(gp.side[l], bs[3] - bs[2]));
-                        d[10] = static_cast<int>(psum);  // psi bytes of the chunk per instance (k_gather_ni)
-                        d[11] = static_cast<int>(gofs[static_cast<size_t>(w)] / elem_bytes);  // G block offset (k_gather_ni)
+                        d[10] = static_cast<int>(psum);  // psi bytes of the chunk per instance (k_gather_direct)
                         poff += nb.second;
                     }
                 }
@@ -896,9 +922,11 @@ struct Launch {
         opt_in(k_gather<T, 2>, gather_smem(gp));
         opt_in(k_gather<T, 3>, gather_smem(gp));
         opt_in(k_gather<T, 4>, gather_smem(gp));
-        opt_in(k_gather_ni<T, 2, 2>, gather_smem(gp));
-        opt_in(k_gather_ni<T, 3, 2>, gather_smem(gp));
-        opt_in(k_gather_ni<T, 4, 2>, gather_smem(gp));
+#define FEWHA_GD_OPT(M, N) opt_in(k_gather_direct<T, M, N>, gather_smem(gp));
+        FEWHA_GD_OPT(2, 1) FEWHA_GD_OPT(3, 1) FEWHA_GD_OPT(4, 1)
+        FEWHA_GD_OPT(2, 2) FEWHA_GD_OPT(3, 2) FEWHA_GD_OPT(4, 2)
+        FEWHA_GD_OPT(2, 4) FEWHA_GD_OPT(3, 4) FEWHA_GD_OPT(4, 4)
+#undef FEWHA_GD_OPT
     }
     // layer kernels: grid (C, L, count), cluster (C,1,1)
     static void cl(int flen, bool inverse, const GeoParams& gp, const Bufs<T>& bf, int mode, int it, int count,
@@ -983,11 +1011,29 @@ struct Launch {
     static void gather(const GeoParams& gp, const Bufs<T>& bf, int count, cudaStream_t st) {
         cudaLaunchAttribute attr[1];
         const int groups = gp.maxside / std::min(gp.grows, gp.maxside);
-        if (gp.gather_ni == 2) {
-            cudaLaunchConfig_t cfg = pdl_cfg(dim3(groups, gp.L, (count + 1) / 2), gather_smem(gp), st, attr);
-            if (gp.gather_minb == 4) CK(cudaLaunchKernelEx(&cfg, k_gather_ni<T, 4, 2>, gp, bf, count));
-            else if (gp.gather_minb == 3) CK(cudaLaunchKernelEx(&cfg, k_gather_ni<T, 3, 2>, gp, bf, count));
-            else CK(cudaLaunchKernelEx(&cfg, k_gather_ni<T, 2, 2>, gp, bf, count));
+        if (gp.gather_direct) {
+            const int ni = gp.gather_ni;
+            // dependents launched after the contraction for batches (batch 64 fp64: 2.48 vs
+            // 2.63 ms per step with the early trigger, whose waiting forward CTAs slow the
+            // gather's last waves), at the start for single frames; FEWHA_GATHER_LATE overrides
+            static const int late_env = [] {
+                const char* v = std::getenv("FEWHA_GATHER_LATE");
+                return v ? std::atoi(v) : -1;
+            }();
+            const int late = late_env >= 0 ? late_env : count > 2;
+            cudaLaunchConfig_t cfg = pdl_cfg(dim3(groups, gp.L, (count + ni - 1) / ni), gather_smem(gp), st, attr);
+#define FEWHA_GD_LAUNCH(N)                                                                            \
+    if (gp.gather_minb == 4) CK(cudaLaunchKernelEx(&cfg, k_gather_direct<T, 4, N>, gp, bf, count, late));      \
+    else if (gp.gather_minb == 3) CK(cudaLaunchKernelEx(&cfg, k_gather_direct<T, 3, N>, gp, bf, count, late)); \
+    else CK(cudaLaunchKernelEx(&cfg, k_gather_direct<T, 2, N>, gp, bf, count, late));
+            if (ni == 4) {
+                FEWHA_GD_LAUNCH(4)
+            } else if (ni == 2) {
+                FEWHA_GD_LAUNCH(2)
+            } else {
+                FEWHA_GD_LAUNCH(1)
+            }
+#undef FEWHA_GD_LAUNCH
             return;
         }
         cudaLaunchConfig_t cfg = pdl_cfg(dim3(groups, gp.L, count), gather_smem(gp), st, attr);
@@ -2022,6 +2068,7 @@ PlanInfo Engine::plan_info() const {
     pi.launches_per_step = launches_per_step();
     pi.whole_layer = P.use_whole() ? 1 : 0;
     pi.gather_instances = P.gp.gather_ni;
+    pi.gather_direct = P.gp.gather_direct;
     pi.wfs_instances = P.precision == 64 ? Launch<double>::wfs_ni(P.batch) : Launch<float>::wfs_ni(P.batch);
     if (pi.wfs_instances == 2) pi.wfs_ctas_per_sm = 3;
     else if (pi.wfs_instances == 4) pi.wfs_ctas_per_sm = 2;

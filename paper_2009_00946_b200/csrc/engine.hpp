@@ -23,7 +23,8 @@ struct StepTelemetry {
 // Execution plan an engine chose for its batch size (engine.cu build_plan / Launch)
 struct PlanInfo {
     int cluster_ctas = 0, tail = 0, gather_rows = 0, gather_ctas_per_sm = 0, inverse_staged = 0, wfs_ctas_per_sm = 0,
-        wfs_tiles = 0, launches_per_step = 0, whole_layer = 0, gather_instances = 1, wfs_instances = 1;
+        wfs_tiles = 0, launches_per_step = 0, whole_layer = 0, gather_instances = 1, wfs_instances = 1,
+        gather_direct = 0;
 };
 
 class Engine;

@@ -516,9 +516,9 @@ def test_fused_forward_inverse_is_bitwise_the_split_frame(name, precision, monke
 @pytest.mark.parametrize("rows,minb", [(2, 4), (4, 3), (8, 2)])
 def test_gather_plans_are_bitwise_equal(rows, minb, monkeypatch):
     """The adjoint gather's row-group size and residency plan (FEWHA_GATHER_ROWS /
-    FEWHA_GATHER_MINB; defaults 4 rows at 2 CTAs/SM for one instance, 8 at 3 for
-    batches) change only the work split: every layer node still sums its WFS in
-    ascending order, so frames are bitwise equal."""
+    FEWHA_GATHER_MINB; defaults 4 rows at 2 CTAs/SM for one instance, 8 rows with 4
+    instances per CTA for batches) change only the work split: every layer node still
+    sums its WFS in ascending order, so frames are bitwise equal."""
     path = preset("elt_mcao84_3dm.json")
     g0 = fg.Reconstructor(path)
     monkeypatch.setenv("FEWHA_GATHER_ROWS", str(rows))
@@ -529,6 +529,29 @@ def test_gather_plans_are_bitwise_equal(rows, minb, monkeypatch):
         s = rng.standard_normal(g0.dims.S) * 0.01
         assert np.array_equal(g0.step(s), g1.step(s))
         assert np.array_equal(g0.coeffs(), g1.coeffs())
+
+
+def test_direct_gather_matches_row_contracted_gather(monkeypatch):
+    """The direct gather (k_gather_direct, the default wherever the taps are
+    compile-time) and the row-contracted k_gather (FEWHA_GATHER_DIRECT=0, the path
+    of the runtime-tap geometries) sum the same products in a different order: the
+    RHS agrees to 1e-13, closed-loop frames within the frame tolerance 1e-9 (measured
+    ~1e-11: the piston-like coarse coefficient is ill-conditioned); single and batch."""
+    path = preset("elt_mcao84_3dm.json")
+    for B in (1, 4):
+        g0 = fg.Reconstructor(path, batch=B)
+        monkeypatch.setenv("FEWHA_GATHER_DIRECT", "0")
+        g1 = fg.Reconstructor(path, batch=B)
+        monkeypatch.delenv("FEWHA_GATHER_DIRECT")
+        assert g0.plan_info()["gather_direct"] == 1 and g1.plan_info()["gather_direct"] == 0
+        rng = np.random.default_rng(9)
+        if B == 1:
+            m = rng.standard_normal(g0.dims.S)
+            assert rel_err(g0.build_rhs(m), g1.build_rhs(m)) <= 1e-13
+        for _ in range(3):
+            s = rng.standard_normal((B, g0.dims.S) if B > 1 else g0.dims.S) * 0.01
+            a0, a1 = g0.step(s), g1.step(s)
+            assert rel_err(a0, a1) <= STEP_TOL[64] and rel_err(g0.coeffs(), g1.coeffs()) <= STEP_TOL[64]
 
 
 @pytest.mark.parametrize("precision_", [64, 32])

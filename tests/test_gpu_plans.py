@@ -57,8 +57,9 @@ def test_elt_batch_plan_per_instance_vs_oracle(precision):
     plan = g.plan_info()
     assert plan["tail"] == 2 * plan["cluster_ctas"] and plan["inverse_staged"] == 0
     assert plan["whole_layer"] == 1  # batches: whole-layer transforms (layer_whole.cuh)
-    assert plan["gather_rows"] == 8 and plan["gather_ctas_per_sm"] == (3 if precision == 64 else 4)
-    assert plan["gather_instances"] == 2 and plan["wfs_instances"] == (2 if precision == 64 else 4)
+    assert plan["gather_rows"] == 8 and plan["gather_ctas_per_sm"] == (2 if precision == 64 else 4)
+    assert plan["gather_direct"] == 1
+    assert plan["gather_instances"] == 4 and plan["wfs_instances"] == (2 if precision == 64 else 4)
     orc = [_oracle(name) for _ in range(B)]
     lay = [smooth_layers(orc[0], 30 + i) for i in range(B)]
     frames, tol = (10, 1e-9) if precision == 64 else (6, 1e-4)
@@ -82,7 +83,7 @@ def test_elt_batch_plan_per_instance_vs_oracle(precision):
 def test_batch_plan_instances_are_bitwise_single_engines(precision, whole, monkeypatch):
     """Every instance of the batch plan equals an independent single-instance
     engine bit for bit once that engine uses the same transform tail: the gather
-    row groups and residency (4 vs 8 rows, 2 vs 3 CTAs/SM), the WFS-kernel
+    row groups and instances per CTA (4 vs 8 rows, 1 vs 4), the WFS-kernel
     residency and TMA-staged vs streamed inverse operands change the work split,
     never an arithmetic order.  (The tail size itself moves the 32^2 level between
     the rank-0 tail and the distributed levels, where the compiler may contract
@@ -99,7 +100,7 @@ def test_batch_plan_instances_are_bitwise_single_engines(precision, whole, monke
     singles = [fg.Reconstructor(path, precision=precision) for _ in range(B)]
     p1, pb = singles[0].plan_info(), gb.plan_info()
     assert p1["gather_instances"] != pb["gather_instances"] and p1["inverse_staged"] != pb["inverse_staged"]
-    assert p1["wfs_instances"] != pb["wfs_instances"] and p1["gather_ctas_per_sm"] != pb["gather_ctas_per_sm"]
+    assert p1["wfs_instances"] != pb["wfs_instances"] and p1["gather_rows"] != pb["gather_rows"]
     rng = np.random.default_rng(77)
     for k in range(10):
         s = rng.standard_normal((B, gb.dims.S)) * 0.02
