@@ -957,6 +957,7 @@ __global__ void __launch_bounds__(256, MINB) k_gather_direct(const GeoParams gp,
     const int R = side < gp.grows ? side : gp.grows;
     if (u * R >= side) return;
     const int tid = threadIdx.x;
+    stamp(gp, 0);
     unsigned char* stage = smem_raw;
     const T* psi = bf.psi + static_cast<size_t>(b0) * gp.Nw;
     if (tid < 32) {
@@ -980,6 +981,7 @@ __global__ void __launch_bounds__(256, MINB) k_gather_direct(const GeoParams gp,
         if (tid == 0) mbar_arrive(&s_mbar);
     }
     __syncthreads();
+    stamp(gp, 12);
     T* y = bf.y + static_cast<size_t>(b0) * gp.n + gp.coff[l] + static_cast<size_t>(u) * R * side;
 #define FEWHA_GATHER_D_KM(ROWS)                                                                                   \
     switch (gp.gather_km) {                                                                                       \
@@ -997,6 +999,7 @@ __global__ void __launch_bounds__(256, MINB) k_gather_direct(const GeoParams gp,
     }
 #undef FEWHA_GATHER_D_KM
     if (late) pdl_launch_dependents();
+    stamp(gp, 2);
 }
 
 // Deterministic sum of the dot partials of one iteration by warp 0: fixed
