@@ -315,7 +315,7 @@ def graph_function_profile(rec, frames, before, d, b, batch=1):
     {function: {launches, ms_per_frame, bytes_per_frame, ...}} and the frame ms."""
     rec.enable_telemetry(True)
     plan = rec.plan_info()
-    whole = plan.get("whole_layer", 0) == 1  # batched plans: whole-layer transform kernels
+    whole = plan.get("whole_layer", 0) >= 1  # batched plans: whole-layer transform kernels (2: fwd+inv fused)
     gdirect = plan.get("gather_direct", 0) == 1  # the direct gather (k_gather_direct)
     acc, frame_ms = {}, []
     for f in range(frames + 2):
@@ -327,7 +327,7 @@ def graph_function_profile(rec, frames, before, d, b, batch=1):
         frame_ms.append(sum(t for _, t in lt))
         for kind, t in lt:
             fn = FUNC[kind]
-            if whole and fn in ("k_fwd_cluster", "k_inv_cluster"):
+            if whole and fn in ("k_fwd_cluster", "k_inv_cluster", "k_fwd_inv_cluster"):
                 fn = fn.replace("_cluster", "_layer")
             if gdirect and fn == "k_gather":
                 fn = "k_gather_direct"
@@ -598,8 +598,10 @@ def run_ours(args):
                       "roofline_frac_frame_model": round(fb / (bms / 1000.0) / 1e9 / peak, 4),
                       "engines": 1 if one <= two else 2,
                       "ms_per_step_1x64": round(one, 4), "ms_per_step_2x32_two_streams": round(two, 4),
-                      "transforms": "whole-layer kernels (one CTA per layer and instance)" if plan_b.get("whole_layer")
-                      else "cluster kernels",
+                      "transforms": {2: "whole-layer kernels (one CTA per layer and instance), forward(k) + "
+                                        "inverse(k+1) fused in one cluster of the layer CTAs per instance",
+                                     1: "whole-layer kernels (one CTA per layer and instance)"}.get(
+                          plan_b.get("whole_layer", 0), "cluster kernels"),
                       "roofline": roof_b,
                       "note": "64 instances per step, inputs resident, no flush between steps "
                               "(working set 64 x ~15 MB > L2); best of one 64-instance engine and two "

@@ -144,7 +144,8 @@ int fewha_gpu_launches_per_step(fewha_gpu_t h);
 typedef struct {
     int cluster_ctas, tail, gather_rows, gather_ctas_per_sm, inverse_staged, wfs_ctas_per_sm, wfs_tiles,
         launches_per_step;
-    int whole_layer; /* 1: layer transforms one CTA per (layer, instance) (batched plans), 0: clusters */
+    int whole_layer; /* 1: layer transforms one CTA per (layer, instance) (batched plans), 2: the same with
+                        forward(k) + inverse(k+1) fused in one launch (k_fwd_inv_layer), 0: clusters */
     int gather_instances, wfs_instances; /* instances per CTA of the adjoint gather / WFS-tile kernels */
     int gather_direct; /* 1: the direct gather (compile-time taps), 0: the row-contracted k_gather */
 } fewha_gpu_plan_t;

@@ -945,6 +945,21 @@ struct Launch {
         FEWHA_FLEN_SWITCH(flen, FEWHA_LAUNCH)
 #undef FEWHA_LAUNCH
     }
+    // whole-layer fused forward (fmode, fit) + inverse (imode, iit): one launch, the L layer
+    // CTAs of an instance meet at a ticketed barrier (k_fwd_inv_layer; ctr: count + 1 counters)
+    static void whole_fused(int flen, const GeoParams& gp, const Bufs<T>& bf, int fmode, int fit, int imode, int iit,
+                            int count, cudaStream_t st, unsigned long long* ctr) {
+#define FEWHA_LAUNCH(N) CK((launch_layer_whole_fused<T, N>(gp, bf, fmode, fit, imode, iit, count, st, 1, ctr)))
+        FEWHA_FLEN_SWITCH(flen, FEWHA_LAUNCH)
+#undef FEWHA_LAUNCH
+    }
+    static int whole_fused_per_sm(const GeoParams& gp, int flen) {
+        int per_sm = 0;
+#define FEWHA_CAP(N) CK((whole_fused_capacity<T, N>(gp, &per_sm)))
+        FEWHA_FLEN_SWITCH(flen, FEWHA_CAP)
+#undef FEWHA_CAP
+        return per_sm;
+    }
     // fused forward (fmode, fit) + inverse (imode, iit): one cooperative cluster launch
     static void fused(int flen, const GeoParams& gp, const Bufs<T>& bf, int fmode, int fit, int imode, int iit,
                       int count, cudaStream_t st, unsigned long long* bar) {
@@ -1082,6 +1097,11 @@ struct EngineImpl {
     // batched plans: layer transforms one CTA per (layer, instance) (layer_whole.cuh)
     bool whole_layer = false;
     bool use_whole() const { return whole_layer && !sharded && peer_sum.empty(); }
+    // whole-layer plans: forward(k) + inverse(k+1) in one launch (k_fwd_inv_layer), opt-in
+    // (FEWHA_FUSE_WHOLE=1; measured no faster than the split launches)
+    bool whole_fuse = false;
+    unsigned long long* wbar = nullptr;  // [batch] instance barrier counters + the ticket counter
+    bool use_whole_fused() const { return whole_fuse && use_whole(); }
     bool fused_frame() const { return fuse_ok && !whole_layer && !telemetry_on && !(sharded && !comm); }
     // optional per-phase timestamps of the cluster kernels (profiling only)
     unsigned long long* stamp_buf = nullptr;
@@ -1217,6 +1237,23 @@ struct EngineImpl {
             for (size_t r = 0; r < peer_sum.size(); ++r) bf.ysum[r] = static_cast<const T*>(peer_sum[r]);
         }
         const bool wl = use_whole();
+        if (seg >= 1 && use_whole_fused()) {  // W of the previous gather and the next W^-1 in one launch
+            const int fmode = seg == 1 ? kRhs : kPcg, fit = seg == 1 ? 0 : seg - 2;
+            if (seg <= it) {
+                Launch<T>::whole_fused(flen, gps(), bf, fmode, fit, kPcg, seg - 1, B, st, wbar);
+                mark(seg == 1 ? kKindFwdRhsInv0 : kKindFwdInvPcg);
+                Launch<T>::wfs(false, gps(), bf, 0, B, st);
+                mark(kKindWfs);
+                Launch<T>::gather(gps(), bf, B, st);
+                mark(kKindGather);
+                return;
+            }
+            Launch<T>::whole_fused(flen, gps(), bf, fmode, fit, kFit, 0, B, st, wbar);
+            mark(kKindFwdInvFit);
+            Launch<T>::fit(gpf, bf, 1, B, st);
+            mark(kKindFit);
+            return;
+        }
         auto layer = [&](bool inverse, int mode, int k) {
             if (wl) Launch<T>::whole(flen, inverse, gps(), bf, mode, k, B, st);
             else Launch<T>::cl(flen, inverse, gps(), bf, mode, k, B, st);
@@ -1601,10 +1638,23 @@ Engine::Engine(Geometry g, int precision, int batch, int device) : p_(std::make_
             const bool fits = whole_layer_smem(P.gp.maxside, precision / 8) + 1024 <= static_cast<size_t>(maxopt);
             const char* wv = std::getenv("FEWHA_WHOLE_LAYER");
             P.whole_layer = fits && (wv ? wv[0] == '1' : batch > 2);
+            const char* fw = std::getenv("FEWHA_FUSE_WHOLE");
+            if (P.whole_layer && fw && fw[0] == '1') {
+                int sms = 0;
+                CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+                const int per_sm = precision == 64 ? Launch<double>::whole_fused_per_sm(P.gp, P.flen)
+                                                   : Launch<float>::whole_fused_per_sm(P.gp, P.flen);
+                // the ticketed barrier needs more than L CTAs resident at once; opt-in
+                // (FEWHA_FUSE_WHOLE=1): batch 64 fp64 -0.8 %, fp32 +4 % per step
+                P.whole_fuse = fw && fw[0] == '1' && per_sm * sms > P.gp.L;
+            }
         }
         P.fbar = dalloc<unsigned long long>(static_cast<size_t>(batch));
         P.fr.add(P.fbar);
         CK(cudaMemset(P.fbar, 0, sizeof(unsigned long long) * static_cast<size_t>(batch)));
+        P.wbar = dalloc<unsigned long long>(static_cast<size_t>(batch) + 1);
+        P.fr.add(P.wbar);
+        CK(cudaMemset(P.wbar, 0, sizeof(unsigned long long) * (static_cast<size_t>(batch) + 1)));
     }
     // the table uploads and zero fills above ran on the legacy stream: let them land
     // before anything is issued on the (non-blocking) frame stream
@@ -2066,7 +2116,7 @@ PlanInfo Engine::plan_info() const {
     pi.wfs_ctas_per_sm = P.batch <= 2 ? FEWHA_WFS_MINB_LAT : FEWHA_WFS_MINB_BATCH;
     pi.wfs_tiles = P.gp.wt_count;
     pi.launches_per_step = launches_per_step();
-    pi.whole_layer = P.use_whole() ? 1 : 0;
+    pi.whole_layer = P.use_whole_fused() ? 2 : P.use_whole() ? 1 : 0;
     pi.gather_instances = P.gp.gather_ni;
     pi.gather_direct = P.gp.gather_direct;
     pi.wfs_instances = P.precision == 64 ? Launch<double>::wfs_ni(P.batch) : Launch<float>::wfs_ni(P.batch);
@@ -2077,7 +2127,7 @@ PlanInfo Engine::plan_info() const {
 
 int Engine::launches_per_step() const {
     const int it = p_->gp.iters;
-    return p_->fused_frame() ? 4 + 3 * it : 5 + 4 * it;
+    return (p_->fused_frame() || p_->use_whole_fused()) ? 4 + 3 * it : 5 + 4 * it;
 }
 
 int Engine::profile_step(float* ms, int* kinds, int max) {

@@ -28,6 +28,13 @@ cudaError_t launch_layer_whole(bool inverse, const GeoParams& gp, const Bufs<T>&
                                cudaStream_t st, int fit_term);
 
 template <typename T, int FLEN>
+cudaError_t launch_layer_whole_fused(const GeoParams& gp, const Bufs<T>& bf, int fmode, int fit, int imode, int iit,
+                                     int count, cudaStream_t st, int fit_term, unsigned long long* ctr);
+
+template <typename T, int FLEN>
+cudaError_t whole_fused_capacity(const GeoParams& gp, int* per_sm);
+
+template <typename T, int FLEN>
 cudaError_t set_layer_cluster_attrs(size_t smem_inv, size_t smem_fwd);
 
 }  // namespace fewha_gpu

@@ -52,6 +52,30 @@ cudaError_t launch_layer_whole(bool inverse, const GeoParams& gp, const Bufs<T>&
     return cudaLaunchKernelEx(&cfg, k_fwd_layer<T, FLEN>, gp, bf, mode, it, fit_term);
 }
 
+// Fused whole-layer forward + inverse (k_fwd_inv_layer): grid (L, count), ticketed CTAs.
+template <typename T, int FLEN>
+cudaError_t launch_layer_whole_fused(const GeoParams& gp, const Bufs<T>& bf, int fmode, int fit, int imode, int iit,
+                                     int count, cudaStream_t st, int fit_term, unsigned long long* ctr) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(gp.L, count, 1);
+    cfg.blockDim = dim3(Wl<T>::threads, 1, 1);
+    cfg.dynamicSmemBytes = whole_layer_smem(gp.maxside, static_cast<int>(sizeof(T)));
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    const char* pdl = std::getenv("FEWHA_PDL");
+    attr[0].val.programmaticStreamSerializationAllowed = (pdl && pdl[0] == '0') ? 0 : 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_fwd_inv_layer<T, FLEN>, gp, bf, fmode, fit, imode, iit, fit_term, ctr);
+}
+// CTAs of the fused whole-layer kernel resident per SM (0: it does not fit)
+template <typename T, int FLEN>
+cudaError_t whole_fused_capacity(const GeoParams& gp, int* per_sm) {
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_fwd_inv_layer<T, FLEN>, Wl<T>::threads,
+                                                         whole_layer_smem(gp.maxside, static_cast<int>(sizeof(T))));
+}
+
 // Fused forward + inverse (k_fwd_inv_cluster): the cluster grid launched
 // cooperatively so the instance barrier's CTAs are co-resident.
 template <typename T, int FLEN>
@@ -120,6 +144,8 @@ cudaError_t set_layer_cluster_attrs(size_t smem_inv, size_t smem_fwd) {
     if (e != cudaSuccess) return e;
     e = opt_in_max(k_fwd_inv_cluster<T, FLEN>, smem_fwd);
     if (e != cudaSuccess) return e;
+    e = opt_in_max(k_fwd_inv_layer<T, FLEN>, smem_fwd);
+    if (e != cudaSuccess) return e;
     return opt_in_max(k_fwd_cluster<T, FLEN>, smem_fwd);
 }
 
@@ -132,6 +158,9 @@ cudaError_t set_layer_cluster_attrs(size_t smem_inv, size_t smem_fwd) {
     template cudaError_t fused_cluster_capacity<T, FEWHA_FLEN>(const GeoParams&, size_t, int*);                 \
     template cudaError_t launch_layer_whole<T, FEWHA_FLEN>(bool, const GeoParams&, const Bufs<T>&, int, int, int,   \
                                                            cudaStream_t, int);                                  \
+    template cudaError_t launch_layer_whole_fused<T, FEWHA_FLEN>(const GeoParams&, const Bufs<T>&, int, int, int, int, \
+                                                                 int, cudaStream_t, int, unsigned long long*); \
+    template cudaError_t whole_fused_capacity<T, FEWHA_FLEN>(const GeoParams&, int*);                           \
     template cudaError_t set_layer_cluster_attrs<T, FEWHA_FLEN>(size_t, size_t);
 FEWHA_INST(double)
 FEWHA_INST(float)

@@ -408,7 +408,7 @@ def test_whole_layer_frames_mixed_sides_and_orders(case, tmp_path, precision, mo
         g = fg.Reconstructor(path, precision=precision, batch=3)
     except fg.ConfigError as e:
         pytest.skip(f"geometry not supported by the gather tables: {e}")
-    assert g.plan_info()["whole_layer"] == 1
+    assert g.plan_info()["whole_layer"] >= 1  # 2: forward + inverse fused (k_fwd_inv_layer)
     B = 3
     o = Oracle(path)
     o.build_preconditioner()
