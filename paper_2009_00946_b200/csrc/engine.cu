@@ -915,10 +915,10 @@ struct Launch {
         opt_in(k_wfs<T, true, FEWHA_WFS_MINB_LAT>, wfs_smem(gp));
         opt_in(k_wfs<T, false, FEWHA_WFS_MINB_BATCH>, wfs_smem(gp));
         opt_in(k_wfs<T, true, FEWHA_WFS_MINB_BATCH>, wfs_smem(gp));
-        opt_in(k_wfs<T, false, 3, 2>, wfs_smem(gp, 2));
-        opt_in(k_wfs<T, true, 3, 2>, wfs_smem(gp, 2));
-        opt_in(k_wfs<T, false, 2, 4>, wfs_smem(gp, 4));
-        opt_in(k_wfs<T, true, 2, 4>, wfs_smem(gp, 4));
+        opt_in(k_wfs<T, false, kWfsNi2Minb, 2>, wfs_smem(gp, 2));
+        opt_in(k_wfs<T, true, kWfsNi2Minb, 2>, wfs_smem(gp, 2));
+        opt_in(k_wfs<T, false, kWfsNi4Minb, 4>, wfs_smem(gp, 4));
+        opt_in(k_wfs<T, true, kWfsNi4Minb, 4>, wfs_smem(gp, 4));
         opt_in(k_gather<T, 2>, gather_smem(gp));
         opt_in(k_gather<T, 3>, gather_smem(gp));
         opt_in(k_gather<T, 4>, gather_smem(gp));
@@ -1009,11 +1009,11 @@ struct Launch {
             return v && std::atoi(v) == LAT;
         }();
         if (ni == 2) {
-            if (rhs) CK(cudaLaunchKernelEx(&cfg, k_wfs<T, true, 3, 2>, gp, bf, with_dm, count));
-            else CK(cudaLaunchKernelEx(&cfg, k_wfs<T, false, 3, 2>, gp, bf, with_dm, count));
+            if (rhs) CK(cudaLaunchKernelEx(&cfg, k_wfs<T, true, kWfsNi2Minb, 2>, gp, bf, with_dm, count));
+            else CK(cudaLaunchKernelEx(&cfg, k_wfs<T, false, kWfsNi2Minb, 2>, gp, bf, with_dm, count));
         } else if (ni == 4) {
-            if (rhs) CK(cudaLaunchKernelEx(&cfg, k_wfs<T, true, 2, 4>, gp, bf, with_dm, count));
-            else CK(cudaLaunchKernelEx(&cfg, k_wfs<T, false, 2, 4>, gp, bf, with_dm, count));
+            if (rhs) CK(cudaLaunchKernelEx(&cfg, k_wfs<T, true, kWfsNi4Minb, 4>, gp, bf, with_dm, count));
+            else CK(cudaLaunchKernelEx(&cfg, k_wfs<T, false, kWfsNi4Minb, 4>, gp, bf, with_dm, count));
         } else if (count <= 2 || bat_lat) {
             if (rhs) CK(cudaLaunchKernelEx(&cfg, k_wfs<T, true, LAT>, gp, bf, with_dm, count));
             else CK(cudaLaunchKernelEx(&cfg, k_wfs<T, false, LAT>, gp, bf, with_dm, count));
@@ -2120,8 +2120,8 @@ PlanInfo Engine::plan_info() const {
     pi.gather_instances = P.gp.gather_ni;
     pi.gather_direct = P.gp.gather_direct;
     pi.wfs_instances = P.precision == 64 ? Launch<double>::wfs_ni(P.batch) : Launch<float>::wfs_ni(P.batch);
-    if (pi.wfs_instances == 2) pi.wfs_ctas_per_sm = 3;
-    else if (pi.wfs_instances == 4) pi.wfs_ctas_per_sm = 2;
+    if (pi.wfs_instances == 2) pi.wfs_ctas_per_sm = kWfsNi2Minb;
+    else if (pi.wfs_instances == 4) pi.wfs_ctas_per_sm = kWfsNi4Minb;
     return pi;
 }
 

@@ -271,7 +271,8 @@ __device__ __forceinline__ void wstamp(const GeoParams& gp, int k) {
 // WFS tiles: 14 x 14 nodes, (14+2)^2 = 256 wavefront nodes = one per thread of a
 // 256-thread CTA in the dominant phase (16 x 16 tiles on 512 threads left 37 % of
 // the warps waiting at the barrier).  Resident CTAs per SM: 3 for single-instance
-// plans, 4 for batches (more tiles in flight); no spills in either (k_wfs below).
+// plans; batches take two (fp64) or four (fp32) instances per CTA at 6 / 4 CTAs per SM
+// (kWfsNi2Minb / kWfsNi4Minb: more tiles in flight; k_wfs below).
 #ifndef FEWHA_WFS_TILE
 #define FEWHA_WFS_TILE 14
 #endif
@@ -289,6 +290,12 @@ __device__ __forceinline__ void wstamp(const GeoParams& gp, int k) {
 // (80 registers, 16 B of spills) beat groups of 7 (no spills): 0.1844 vs 0.1865 ms per frame
 #define FEWHA_WFS_GLAT 9
 #endif
+// Batches: resident CTAs per SM with two (fp64) / four (fp32) instances per CTA, loads in
+// groups of 2 screens (40 / 48 registers, no spills).  Batch 64 fp64 per step: 3/SM with
+// groups of 3 (72 registers) 2.429 ms, 4/SM 2.359, 5/SM 2.294, 6/SM 2.292; fp32 four
+// instances 2/SM 1.531, 4/SM 1.522 (profiles/r02_experiments.md, fourth session).
+constexpr int kWfsNi2Minb = 6;
+constexpr int kWfsNi4Minb = 4;
 constexpr int kWfsTile = FEWHA_WFS_TILE;  // WFS node tile side (compile-time: index math by constants)
 constexpr int kWfsThreads = FEWHA_WFS_THREADS;  // threads per WFS tile CTA
 
@@ -464,9 +471,9 @@ template <typename T, bool RHS, int MINB, int NI = 1>
 __global__ void __launch_bounds__(kWfsThreads, MINB) k_wfs(const GeoParams gp, const Bufs<T> bf, int with_dm, int count) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     // screens per unrolled load group: FEWHA_WFS_GLAT (9) for the latency plan (3 CTAs/SM),
-    // 5 for batches of one instance per CTA (4 CTAs/SM, 56 registers), 3 / 2 with two / four
-    // instances per CTA
-    constexpr int G = NI > 2 ? 2 : NI > 1 ? 3 : (MINB >= 4 && sizeof(T) == 8) ? 5 : FEWHA_WFS_GLAT;
+    // 5 for batches of one instance per CTA (4 CTAs/SM, 56 registers), 2 with two / four
+    // instances per CTA (kWfsNi2Minb / kWfsNi4Minb CTAs/SM)
+    constexpr int G = NI > 1 ? 2 : (MINB >= 4 && sizeof(T) == 8) ? 5 : FEWHA_WFS_GLAT;
     const int b0 = blockIdx.y * NI;
     wfs_tile<T, RHS, G, NI>(gp, bf, with_dm, gp.wt_base + blockIdx.x, b0, min(NI, count - b0), smem_raw);
 }
