@@ -21,3 +21,12 @@ ls gpurun_out | grep r02e
 ncu --set full --import-source on --clock-control none -k regex:k_wfs -s 6 -c 1 -o gpurun_out/r02e_wfs_b64 $P64 > /dev/null 2>&1
 ncu --set full --import-source on --clock-control none -k regex:k_wfs -s 5 -c 1 -o gpurun_out/r02e_wfs_b1 $P1 > /dev/null 2>&1
 ls gpurun_out | grep r02e
+# keep the merge under 64 MiB: export the captures' pages and drop the reports
+for r in gpurun_out/r02e_*.ncu-rep; do
+  b=${r%.ncu-rep}
+  ncu -i $r --page details --csv > ${b}_details.csv 2>/dev/null
+  ncu -i $r --page raw --csv > ${b}_raw.csv 2>/dev/null
+  ncu -i $r --page source --csv --print-source sass > ${b}_source.csv 2>/dev/null
+  rm -f $r
+done
+du -sh gpurun_out
