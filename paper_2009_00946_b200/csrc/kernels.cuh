@@ -271,8 +271,8 @@ __device__ __forceinline__ void wstamp(const GeoParams& gp, int k) {
 // WFS tiles: 14 x 14 nodes, (14+2)^2 = 256 wavefront nodes = one per thread of a
 // 256-thread CTA in the dominant phase (16 x 16 tiles on 512 threads left 37 % of
 // the warps waiting at the barrier).  Resident CTAs per SM: 3 for single-instance
-// plans; batches take two (fp64) or four (fp32) instances per CTA at 6 / 4 CTAs per SM
-// (kWfsNi2Minb / kWfsNi4Minb: more tiles in flight; k_wfs below).
+// plans; batches take four instances per CTA at 4 (fp64) / 6 (fp32) CTAs per SM
+// (kWfsNi4Minb: more tiles in flight; k_wfs below).
 #ifndef FEWHA_WFS_TILE
 #define FEWHA_WFS_TILE 14
 #endif
@@ -290,12 +290,14 @@ __device__ __forceinline__ void wstamp(const GeoParams& gp, int k) {
 // (80 registers, 16 B of spills) beat groups of 7 (no spills): 0.1844 vs 0.1865 ms per frame
 #define FEWHA_WFS_GLAT 9
 #endif
-// Batches: resident CTAs per SM with two (fp64) / four (fp32) instances per CTA, loads in
-// groups of 2 screens (40 / 48 registers, no spills).  Batch 64 fp64 per step: 3/SM with
-// groups of 3 (72 registers) 2.429 ms, 4/SM 2.359, 5/SM 2.294, 6/SM 2.292; fp32 four
-// instances 2/SM 1.531, 4/SM 1.522 (profiles/r02_experiments.md, fourth session).
+// Batches: resident CTAs per SM with two / four instances per CTA, loads in groups of 2
+// screens (no spills).  Batch 64 per step (profiles/r02_experiments.md, fourth session):
+// fp64 two instances at 3/SM with groups of 3 (72 registers) 2.429 ms, 4/SM 2.359, 5/SM
+// 2.294, 6/SM 2.292; four instances at 4/SM (64 registers) 2.229, 6/SM 2.294; fp32 four
+// instances 2/SM 1.531, 4/SM 1.520, 6/SM (40 registers) 1.511.
 constexpr int kWfsNi2Minb = 6;
-constexpr int kWfsNi4Minb = 4;
+template <typename T>
+constexpr int kWfsNi4Minb = sizeof(T) == 8 ? 4 : 6;
 constexpr int kWfsTile = FEWHA_WFS_TILE;  // WFS node tile side (compile-time: index math by constants)
 constexpr int kWfsThreads = FEWHA_WFS_THREADS;  // threads per WFS tile CTA
 

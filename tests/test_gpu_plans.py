@@ -59,7 +59,7 @@ def test_elt_batch_plan_per_instance_vs_oracle(precision):
     assert plan["whole_layer"] == 1  # batches: whole-layer transforms (layer_whole.cuh)
     assert plan["gather_rows"] == 8 and plan["gather_ctas_per_sm"] == (2 if precision == 64 else 4)
     assert plan["gather_direct"] == 1
-    assert plan["gather_instances"] == 4 and plan["wfs_instances"] == (2 if precision == 64 else 4)
+    assert plan["gather_instances"] == 4 and plan["wfs_instances"] == 4
     orc = [_oracle(name) for _ in range(B)]
     lay = [smooth_layers(orc[0], 30 + i) for i in range(B)]
     frames, tol = (10, 1e-9) if precision == 64 else (6, 1e-4)
