@@ -590,22 +590,29 @@ def run_ours(args):
             return e0.elapsed_time(e1) / KB, prof_b
 
         one, prof_b = time_split(1)
-        two, _ = time_split(2)
-        bms = min(one, two)
+        splits = {1: one}
+        for parts in (2, 4, 8):
+            splits[parts], _ = time_split(parts)
+        best = min(splits, key=splits.get)
+        bms = splits[best]
+        two = splits[2]
         roof_b = roofline_object(prof_b, peak, peak_kind, f"fp{args.precision}_b64",
                                  "event-record nodes of the 64-instance frame graph (3 frames, working set > L2)")
         batch_info = {"batch": B, "ms_per_step": round(bms, 4), "recon_per_s": round(B * 1000.0 / bms, 1),
                       "roofline_frac_frame_model": round(fb / (bms / 1000.0) / 1e9 / peak, 4),
-                      "engines": 1 if one <= two else 2,
+                      "engines": best,
                       "ms_per_step_1x64": round(one, 4), "ms_per_step_2x32_two_streams": round(two, 4),
+                      "ms_per_step_4x16_four_streams": round(splits[4], 4),
+                      "ms_per_step_8x8_eight_streams": round(splits[8], 4),
                       "transforms": {2: "whole-layer kernels (one CTA per layer and instance), forward(k) + "
                                         "inverse(k+1) fused in one cluster of the layer CTAs per instance",
                                      1: "whole-layer kernels (one CTA per layer and instance)"}.get(
                           plan_b.get("whole_layer", 0), "cluster kernels"),
                       "roofline": roof_b,
                       "note": "64 instances per step, inputs resident, no flush between steps "
-                              "(working set 64 x ~15 MB > L2); best of one 64-instance engine and two "
-                              "32-instance engines on two streams"}
+                              "(working set 64 x ~15 MB > L2); best of one 64-instance engine and 2 / 4 / 8 "
+                              "engines of 32 / 16 / 8 instances on as many concurrent streams (small engines' "
+                              "latency-bound and bandwidth-bound kernels overlap across streams)"}
 
     # ---- the other BASELINE configs (rank 0, N=1): single-frame latency -------------
     configs = None

@@ -275,3 +275,48 @@ def test_failed_solve_produces_no_command_and_keeps_history():
     # the caller may reset and carry on, like catching the reference's exception
     g.reset()
     g.step(np.random.default_rng(1).standard_normal(d.S))
+
+
+@pytest.mark.parametrize("precision", [64, 32])
+def test_concurrent_engines_on_streams_match_serial(precision):
+    """The bench's split of the 64-instance step into small engines on concurrent streams
+    (8 engines of 8 instances in fp32): four 4-instance engines stepped on four torch
+    streams at once (device-resident slopes, step_device) end every frame bitwise equal
+    to the same engines stepped one after another -- engines share no state."""
+    import torch
+
+    path = preset("elt_mcao84_3dm.json")
+    E, B = 4, 4
+    dev = torch.device("cuda:0")
+    rng = np.random.default_rng(21)
+    frames = 5
+    probe = fg.Reconstructor(path, precision=precision, batch=B)
+    S = probe.dims.S
+    probe.close()
+    slopes = [torch.tensor(rng.standard_normal((frames, B, S)) * 0.02, dtype=torch.float64, device=dev)
+              for _ in range(E)]
+
+    def run(concurrent):
+        engs = []
+        for e in range(E):
+            r = fg.Reconstructor(path, precision=precision, batch=B)
+            s = torch.cuda.Stream(dev) if concurrent else torch.cuda.current_stream(dev)
+            r.set_stream(s.cuda_stream)
+            engs.append((r, s))
+        torch.cuda.synchronize(dev)
+        out = []
+        for k in range(frames):
+            for e, (r, s) in enumerate(engs):
+                with torch.cuda.stream(s):
+                    r.step_device(slopes[e][k].data_ptr())
+            torch.cuda.synchronize(dev)
+            out.append([np.concatenate([np.concatenate([st["c"], st["a_prev"]])
+                                        for st in (r.get_state(i) for i in range(B))]) for r, _ in engs])
+        for r, _ in engs:
+            r.close()
+        return out
+
+    ser, con = run(False), run(True)
+    for k in range(frames):
+        for e in range(E):
+            assert np.array_equal(ser[k][e], con[k][e]), (k, e)
