@@ -520,15 +520,19 @@ __device__ __forceinline__ void fit_actuator(const GeoParams& gp, const Bufs<T>&
     const int i = idx / na, j = idx % na;
     const size_t g = static_cast<size_t>(b) * gp.A + k;
     const int ofit = live ? gp.ti[gp.o_fit + m] : -1;
-    // bilinear resampling of each layer of the DM's group (ascending layer order)
-    int src[kMaxL], sd[kMaxL];
-    T fy[kMaxL], fx[kMaxL];
+    // bilinear resampling of each layer of the DM's group (ascending layer order); the
+    // stencils of the first kFitPre layers are resolved before the programmatic-launch
+    // wait (register arrays; 16 of them held 128 registers and capped the kernel at 16
+    // warps per SM), any further layers of the group (LTAO: all nine) after it
+    constexpr int kFitPre = 4;
+    int src[kFitPre], sd[kFitPre];
+    T fy[kFitPre], fx[kFitPre];
     int cnt = 0;
+    const T* tw = weights<T>(gp);
     if (live && ofit >= 0) {
-        const T* tw = weights<T>(gp);
         cnt = gp.ti[ofit];
 #pragma unroll
-        for (int q = 0; q < kMaxL; ++q) {
+        for (int q = 0; q < kFitPre; ++q) {
             src[q] = -1;
             sd[q] = 0;
             fy[q] = fx[q] = T(0);
@@ -564,10 +568,16 @@ __device__ __forceinline__ void fit_actuator(const GeoParams& gp, const Bufs<T>&
     } else {
         at = T(0);
 #pragma unroll
-        for (int q = 0; q < kMaxL; ++q) {
+        for (int q = 0; q < kFitPre; ++q) {
             if (q >= cnt) break;
             if (src[q] < 0) continue;
             at += bilinear<T>(phi_b + src[q], sd[q], 0, 0, fy[q], fx[q]);
+        }
+        for (int q = kFitPre; q < cnt; ++q) {
+            const int l = gp.ti[ofit + 1 + 3 * q], ox = gp.ti[ofit + 2 + 3 * q], oy = gp.ti[ofit + 3 + 3 * q];
+            const int ii = gp.ti[oy + i], jj = gp.ti[ox + j];
+            if (ii < 0 || jj < 0) continue;
+            at += bilinear<T>(phi_b + gp.coff[l] + ii * gp.side[l] + jj, gp.side[l], 0, 0, tw[oy + i], tw[ox + j]);
         }
     }
     if (!step) {
